@@ -1,0 +1,530 @@
+// Hierarchical depth filter (filtering.py:60-147) + frame assembly
+// (render.py:146-161) + U-Net input packing (weights.ts:90-95, bridge.ts:37-44).
+//
+// Per frame (fast path) this is L+1 launches:
+//   k_assemble_pyramid  one CTA per 32x32 pixel block: integer-mean colours,
+//                       f32 depth/alpha, sentinel conversion and up to five 2x2
+//                       min-pool levels in shared memory; consumes and resets the
+//                       projection buffers for the next frame.
+//   k_filter_step<F>    one thread per COARSE pixel: Laplacian edge + reference
+//                       depth of the parent (3x3 window), keep test of its <= 4
+//                       children, renormalised bilinear fill (non-final steps).
+//                       The final step applies the mask to the frame and writes
+//                       the U-Net input.
+// Each output pixel depends only on a 3x3 coarse window, so every step is a
+// pure stencil; the working set (<= 8 MB at 1080p) stays in L2.
+#include <cuda_bf16.h>
+
+#include "ls_common.cuh"
+
+namespace ls {
+
+__device__ __forceinline__ float sentinel(float d) { return d <= 0.0f ? INFINITY : d; }
+
+// _native.pyx:173-196 at one pixel
+__device__ __forceinline__ bool lap_edge(const float *__restrict__ img, int64_t h, int64_t w,
+                                         int64_t y, int64_t x, double thr) {
+    const double c = (double)img[y * w + x];
+    if (!finite_d(c)) return false;
+    double up = y > 0 ? (double)img[(y - 1) * w + x] : c;
+    double dn = y + 1 < h ? (double)img[(y + 1) * w + x] : c;
+    double lf = x > 0 ? (double)img[y * w + x - 1] : c;
+    double rt = x + 1 < w ? (double)img[y * w + x + 1] : c;
+    if (!finite_d(up)) up = c;
+    if (!finite_d(dn)) dn = c;
+    if (!finite_d(lf)) lf = c;
+    if (!finite_d(rt)) rt = c;
+    const double resp = dsub(dadd(dadd(dadd(up, dn), lf), rt), dmul(4.0, c));
+    return fabs(resp) > dmul(thr, c);
+}
+
+// _native.pyx:205-220: reference depth of coarse pixel (cy,cx)
+__device__ __forceinline__ double parent_ref(const float *__restrict__ coarse, int64_t ch,
+                                             int64_t cw, int64_t cy, int64_t cx, bool edge) {
+    const double c = (double)coarse[cy * cw + cx];
+    double ref = finite_d(c) ? c : -INFINITY;
+    if (edge) {
+        for (int64_t ny = cy - 1; ny <= cy + 1; ++ny) {
+            if (ny < 0 || ny >= ch) continue;
+            for (int64_t nx = cx - 1; nx <= cx + 1; ++nx) {
+                if (nx < 0 || nx >= cw || (ny == cy && nx == cx)) continue;
+                const double v = (double)coarse[ny * cw + nx];
+                if (finite_d(v) && v > ref) ref = v;
+            }
+        }
+    }
+    return ref;
+}
+
+__device__ __forceinline__ bool keep_test(float f, double ref, double fs) {
+    const double fd = (double)f;
+    return finite_d(fd) && finite_d(ref) && dsub(fd, ref) <= dmul(fs, ref);
+}
+
+// _native.pyx:240-297 at one fine pixel (called only for holes)
+__device__ __forceinline__ float bilinear_at(const float *__restrict__ coarse, int64_t ch,
+                                             int64_t cw, int64_t y, int64_t x) {
+    const double gy = dsub(dmul(0.5, (double)y), 0.25);
+    const int64_t y0r = (int64_t)floor(gy);
+    const double wy1 = dsub(gy, (double)y0r), wy0 = dsub(1.0, wy1);
+    const int64_t y0 = min(max(y0r, (int64_t)0), ch - 1), y1 = min(max(y0r + 1, (int64_t)0), ch - 1);
+    const double gx = dsub(dmul(0.5, (double)x), 0.25);
+    const int64_t x0r = (int64_t)floor(gx);
+    const double wx1 = dsub(gx, (double)x0r), wx0 = dsub(1.0, wx1);
+    const int64_t x0 = min(max(x0r, (int64_t)0), cw - 1), x1 = min(max(x0r + 1, (int64_t)0), cw - 1);
+    double num = 0.0, den = 0.0;
+    const int64_t yy[2] = {y0, y1};
+    const int64_t xx[2] = {x0, x1};
+    const double wy[2] = {wy0, wy1};
+    const double wx[2] = {wx0, wx1};
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const double v = (double)coarse[yy[a] * cw + xx[b]];
+            if (finite_d(v)) {
+                const double wgt = dmul(wy[a], wx[b]);
+                num = dadd(num, dmul(wgt, v));
+                den = dadd(den, wgt);
+            }
+        }
+    }
+    return den > 0.0 ? __double2float_rn(ddiv(num, den)) : INFINITY;
+}
+
+// ----------------------------------------------------------------- twins ---
+
+__global__ void k_min_pool(const float *__restrict__ img, int64_t h, int64_t w,
+                           float *__restrict__ out) {
+    const int64_t oh = (h + 1) / 2, ow = (w + 1) / 2;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < oh * ow;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = p / ow, x = p - y * ow;
+        float m = INFINITY;
+        for (int dy = 0; dy < 2; ++dy) {
+            if (2 * y + dy >= h) break;
+            for (int dx = 0; dx < 2; ++dx) {
+                if (2 * x + dx >= w) break;
+                const float v = img[(2 * y + dy) * w + 2 * x + dx];
+                if (v < m) m = v;
+            }
+        }
+        out[p] = m;
+    }
+}
+
+__global__ void k_laplacian(const float *__restrict__ img, int64_t h, int64_t w, double thr,
+                            uint8_t *__restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < h * w;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = p / w, x = p - y * w;
+        out[p] = lap_edge(img, h, w, y, x, thr) ? 1 : 0;
+    }
+}
+
+__global__ void k_keep(const float *__restrict__ coarse, int64_t ch, int64_t cw,
+                       const uint8_t *__restrict__ edges, const float *__restrict__ fine,
+                       int64_t fh, int64_t fw, double fs, float *__restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < fh * fw;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = p / fw, x = p - y * fw;
+        const int64_t cy = y >> 1, cx = x >> 1;
+        float o = INFINITY;
+        if (cy < ch && cx < cw) {
+            const double ref = parent_ref(coarse, ch, cw, cy, cx, edges[cy * cw + cx] != 0);
+            if (keep_test(fine[p], ref, fs)) o = fine[p];
+        }
+        out[p] = o;
+    }
+}
+
+__global__ void k_fill(const float *__restrict__ coarse, int64_t ch, int64_t cw,
+                       const float *__restrict__ fine, int64_t fh, int64_t fw,
+                       float *__restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < fh * fw;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const float f = fine[p];
+        if (finite_f(f)) {
+            out[p] = f;
+        } else {
+            const int64_t y = p / fw, x = p - y * fw;
+            out[p] = bilinear_at(coarse, ch, cw, y, x);
+        }
+    }
+}
+
+// ---------------------------------------------------------- fused frame ---
+
+struct Levels {
+    float *img[8];  // pooled^1 .. pooled^L (index k-1)
+    int64_t h[9], w[9];  // h[k] = size after k pools, k = 0..L
+    int L;
+};
+
+// 32x32 pixel block per CTA, 256 threads, 2x2 pixels per thread.
+__global__ void __launch_bounds__(256) k_assemble_pyramid(
+    unsigned long long *__restrict__ minz, unsigned long long *__restrict__ acc, int64_t H,
+    int64_t W, Levels lv, int pool_levels, float *__restrict__ rgb, float *__restrict__ depth,
+    uint8_t *__restrict__ alpha, int *__restrict__ flags) {
+    __shared__ float s1[16][17];
+    __shared__ float s2[8][9];
+    __shared__ float s3[4][5];
+    __shared__ float s4[2][3];
+    const int gy = threadIdx.x >> 4, gx = threadIdx.x & 15;
+    const int64_t by = blockIdx.y, bx = blockIdx.x;
+    float m = INFINITY;
+    bool overflow = false;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+        const int64_t y = by * 32 + 2 * gy + dy;
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            const int64_t x = bx * 32 + 2 * gx + dx;
+            if (y >= H || x >= W) continue;
+            const int64_t p = y * W + x;
+            const unsigned long long key = minz[p];
+            const unsigned long long w_rg = acc[2 * p], w_bn = acc[2 * p + 1];
+            minz[p] = kInfBits;
+            acc[2 * p] = 0ull;
+            acc[2 * p + 1] = 0ull;
+            const unsigned long long cnt = w_bn >> 32;
+            float d = 0.0f;
+            if (cnt > 0) {
+                overflow |= cnt > LS_PACKED_COUNT_LIMIT;
+                const double denom = dmul((double)cnt, 255.0);
+                rgb[3 * p + 0] = __double2float_rn(ddiv((double)(w_rg & 0xffffffffull), denom));
+                rgb[3 * p + 1] = __double2float_rn(ddiv((double)(w_rg >> 32), denom));
+                rgb[3 * p + 2] = __double2float_rn(ddiv((double)(w_bn & 0xffffffffull), denom));
+                d = __double2float_rn(__longlong_as_double((long long)key));
+                alpha[p] = 1;
+            } else {
+                rgb[3 * p + 0] = rgb[3 * p + 1] = rgb[3 * p + 2] = 0.0f;
+                alpha[p] = 0;
+            }
+            depth[p] = d;
+            const float sv = sentinel(d);
+            m = sv < m ? sv : m;
+        }
+    }
+    if (overflow) atomicOr(flags, 1);
+    if (pool_levels < 1) return;
+    // level 1
+    {
+        const int64_t y = by * 16 + gy, x = bx * 16 + gx;
+        if (y < lv.h[1] && x < lv.w[1]) lv.img[0][y * lv.w[1] + x] = m;
+        s1[gy][gx] = m;  // out-of-image entries are +inf == skipped children
+    }
+    if (pool_levels < 2) return;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;
+        float v = fminf(fminf(s1[2 * ty][2 * tx], s1[2 * ty][2 * tx + 1]),
+                        fminf(s1[2 * ty + 1][2 * tx], s1[2 * ty + 1][2 * tx + 1]));
+        s2[ty][tx] = v;
+        const int64_t y = by * 8 + ty, x = bx * 8 + tx;
+        if (y < lv.h[2] && x < lv.w[2]) lv.img[1][y * lv.w[2] + x] = v;
+    }
+    if (pool_levels < 3) return;
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        const int ty = threadIdx.x >> 2, tx = threadIdx.x & 3;
+        float v = fminf(fminf(s2[2 * ty][2 * tx], s2[2 * ty][2 * tx + 1]),
+                        fminf(s2[2 * ty + 1][2 * tx], s2[2 * ty + 1][2 * tx + 1]));
+        s3[ty][tx] = v;
+        const int64_t y = by * 4 + ty, x = bx * 4 + tx;
+        if (y < lv.h[3] && x < lv.w[3]) lv.img[2][y * lv.w[3] + x] = v;
+    }
+    if (pool_levels < 4) return;
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        const int ty = threadIdx.x >> 1, tx = threadIdx.x & 1;
+        float v = fminf(fminf(s3[2 * ty][2 * tx], s3[2 * ty][2 * tx + 1]),
+                        fminf(s3[2 * ty + 1][2 * tx], s3[2 * ty + 1][2 * tx + 1]));
+        s4[ty][tx] = v;
+        const int64_t y = by * 2 + ty, x = bx * 2 + tx;
+        if (y < lv.h[4] && x < lv.w[4]) lv.img[3][y * lv.w[4] + x] = v;
+    }
+    if (pool_levels < 5) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float v = fminf(fminf(s4[0][0], s4[0][1]), fminf(s4[1][0], s4[1][1]));
+        if (by < lv.h[5] && bx < lv.w[5]) lv.img[4][by * lv.w[5] + bx] = v;
+    }
+}
+
+// One thread per coarse pixel; FINAL reads the full-resolution frame.
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_filter_step(
+    const float *__restrict__ coarse, int64_t ch, int64_t cw, const float *__restrict__ fine,
+    int64_t fh, int64_t fw, double fs, double et, float *__restrict__ out,
+    // FINAL-only arguments
+    const float *__restrict__ rgb, const uint8_t *__restrict__ alpha, float *__restrict__ frgb,
+    float *__restrict__ fdepth, uint8_t *__restrict__ falpha, uint8_t *__restrict__ keep_out,
+    __nv_bfloat16 *__restrict__ unet_in, int unet_c, double znear) {
+    const int64_t n = ch * cw;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t cy = q / cw, cx = q - cy * cw;
+        const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
+        const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+            const int64_t y = 2 * cy + dy;
+            if (y >= fh) break;
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                const int64_t x = 2 * cx + dx;
+                if (x >= fw) break;
+                const int64_t p = y * fw + x;
+                if (!FINAL) {
+                    const float f = fine[p];
+                    const bool k = keep_test(f, ref, fs);
+                    out[p] = k ? f : bilinear_at(coarse, ch, cw, y, x);
+                } else {
+                    const float d = fine[p];  // frame depth (0 = empty)
+                    const bool k = keep_test(sentinel(d), ref, fs);
+                    if (keep_out) keep_out[p] = (uint8_t)k;
+                    if (!rgb) continue;  // mask-only (filter_depth_image)
+                    // filtering.py:141-147: multiply by the f32 0/1 mask
+                    const float mk = k ? 1.0f : 0.0f;
+                    const float r = rgb[3 * p] * mk, g = rgb[3 * p + 1] * mk,
+                                b = rgb[3 * p + 2] * mk, dd = d * mk;
+                    const uint8_t a = (uint8_t)(alpha[p] * (uint8_t)k);
+                    if (frgb) {
+                        frgb[3 * p] = r;
+                        frgb[3 * p + 1] = g;
+                        frgb[3 * p + 2] = b;
+                    }
+                    if (fdepth) fdepth[p] = dd;
+                    if (falpha) falpha[p] = a;
+                    if (unet_in) {
+                        // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
+                        const float dn =
+                            dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear)))
+                                      : 0.0f;
+                        __nv_bfloat16 *o = unet_in + p * unet_c;
+                        __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
+                        __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
+                        __nv_bfloat162 v45 = __floats2bfloat162_rn((float)a, 0.0f);
+                        __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
+                        __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(o);
+                        o2[0] = v01;
+                        o2[1] = v23;
+                        o2[2] = v45;
+                        for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
+                    }
+                }
+            }
+        }
+    }
+}
+
+inline int step_grid(int64_t n) { return grid_for(n, 256, 8); }
+
+inline void level_sizes(int64_t H, int64_t W, int L, int64_t *h, int64_t *w) {
+    h[0] = H;
+    w[0] = W;
+    for (int k = 1; k <= L; ++k) {
+        h[k] = (h[k - 1] + 1) / 2;
+        w[k] = (w[k - 1] + 1) / 2;
+    }
+}
+
+// Pyramid + steps over an existing sentinel-able depth image.  `lvl` holds
+// pooled^1..pooled^L, `up` the filled images of steps 1..L-1.
+int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, int64_t H,
+                     int64_t W, double fs, double et, float *keep_as_out, const float *rgb,
+                     const uint8_t *alpha, float *frgb, float *fdepth, uint8_t *falpha,
+                     uint8_t *keep, __nv_bfloat16 *unet_in, int unet_c, double znear,
+                     cudaStream_t st) {
+    const int L = lv.L;
+    const float *coarse = lv.img[L - 1];  // pyr.levels[0]
+    float *up = up_base;
+    for (int i = 1; i <= L; ++i) {
+        const int64_t ch = lv.h[L - i + 1], cw = lv.w[L - i + 1];
+        const int64_t fh = lv.h[L - i], fw = lv.w[L - i];
+        if (i < L) {
+            const float *fine = lv.img[L - i - 1];
+            k_filter_step<false><<<step_grid(ch * cw), 256, 0, st>>>(
+                coarse, ch, cw, fine, fh, fw, fs, et, up, nullptr, nullptr, nullptr, nullptr,
+                nullptr, nullptr, nullptr, 0, 0.0);
+            LS_LAUNCH_CHECK();
+            coarse = up;
+            up += fh * fw;
+        } else {
+            k_filter_step<true><<<step_grid(ch * cw), 256, 0, st>>>(
+                coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, rgb, alpha, frgb, fdepth,
+                falpha, keep, unet_in, unet_c, znear);
+            LS_LAUNCH_CHECK();
+        }
+    }
+    return 0;
+}
+
+__global__ void k_to_sentinel_pool(const float *__restrict__ depth, int64_t h, int64_t w,
+                                   float *__restrict__ out) {
+    const int64_t oh = (h + 1) / 2, ow = (w + 1) / 2;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < oh * ow;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t y = p / ow, x = p - y * ow;
+        float m = INFINITY;
+        for (int dy = 0; dy < 2; ++dy) {
+            if (2 * y + dy >= h) break;
+            for (int dx = 0; dx < 2; ++dx) {
+                if (2 * x + dx >= w) break;
+                const float v = sentinel(depth[(2 * y + dy) * w + 2 * x + dx]);
+                if (v < m) m = v;
+            }
+        }
+        out[p] = m;
+    }
+}
+
+bool setup_levels(int64_t H, int64_t W, int L, float *pyr, Levels &lv, float *&up_base) {
+    if (L < 1 || L > 8) return false;
+    if (H < (int64_t(1) << L) || W < (int64_t(1) << L)) return false;  // filtering.py:75-78
+    lv.L = L;
+    level_sizes(H, W, L, lv.h, lv.w);
+    float *p = pyr;
+    for (int k = 1; k <= L; ++k) {
+        lv.img[k - 1] = p;
+        p += lv.h[k] * lv.w[k];
+    }
+    up_base = p;
+    return true;
+}
+
+}  // namespace ls
+
+using namespace ls;
+
+extern "C" {
+
+int ls_min_pool_2x2(const float *d_img, int64_t h, int64_t w, float *d_out, void *stream) {
+    if (h <= 0 || w <= 0) return LS_EINVAL;
+    const int64_t n = ((h + 1) / 2) * ((w + 1) / 2);
+    k_min_pool<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(d_img, h, w, d_out);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_laplacian_edges(const float *d_img, int64_t h, int64_t w, double threshold,
+                       uint8_t *d_out, void *stream) {
+    if (h <= 0 || w <= 0) return LS_EINVAL;
+    k_laplacian<<<grid_for(h * w, 256), 256, 0, (cudaStream_t)stream>>>(d_img, h, w, threshold,
+                                                                        d_out);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_filter_keep(const float *d_coarse, int64_t ch, int64_t cw, const uint8_t *d_edges,
+                   const float *d_fine, int64_t fh, int64_t fw, double filter_strength,
+                   float *d_out, void *stream) {
+    if (ch <= 0 || cw <= 0 || fh <= 0 || fw <= 0) return LS_EINVAL;
+    k_keep<<<grid_for(fh * fw, 256), 256, 0, (cudaStream_t)stream>>>(
+        d_coarse, ch, cw, d_edges, d_fine, fh, fw, filter_strength, d_out);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_bilinear_fill(const float *d_coarse, int64_t ch, int64_t cw, const float *d_fine,
+                     int64_t fh, int64_t fw, float *d_out, void *stream) {
+    if (ch <= 0 || cw <= 0 || fh <= 0 || fw <= 0) return LS_EINVAL;
+    k_fill<<<grid_for(fh * fw, 256), 256, 0, (cudaStream_t)stream>>>(d_coarse, ch, cw, d_fine,
+                                                                     fh, fw, d_out);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n) {
+    if (levels_n < 1 || levels_n > 8 || height <= 0 || width <= 0) return -1;
+    int64_t h[9], w[9];
+    level_sizes(height, width, levels_n, h, w);
+    int64_t total = 0;
+    for (int k = 1; k <= levels_n; ++k) total += 2 * h[k] * w[k];
+    return total;
+}
+
+int ls_frame_finish(uint64_t *d_minz_bits, uint64_t *d_accum2, int64_t width, int64_t height,
+                    const ls_filter_params *filter, float *d_rgb, float *d_depth,
+                    uint8_t *d_alpha, float *d_frgb, float *d_fdepth, uint8_t *d_falpha,
+                    uint8_t *d_keep, uint16_t *d_unet_in, int64_t unet_h, int32_t unet_c,
+                    double unet_znear, float *d_pyramid, int32_t *d_flags, void *stream) {
+    if (width <= 0 || height <= 0 || !d_rgb || !d_depth || !d_alpha || !d_flags) return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Levels lv{};
+    float *up_base = nullptr;
+    int L = 0;
+    if (filter) {
+        if (!d_pyramid || filter->filter_strength < 0 || filter->edge_threshold <= 0)
+            return LS_EINVAL;
+        if (!setup_levels(height, width, filter->levels_n, d_pyramid, lv, up_base))
+            return LS_EINVAL;
+        if (d_unet_in && (unet_h < height || unet_c < 6 || (unet_c & 1))) return LS_EINVAL;
+        L = filter->levels_n;
+    }
+    dim3 grid((unsigned)((width + 31) / 32), (unsigned)((height + 31) / 32));
+    const int in_block = L < 5 ? L : 5;
+    k_assemble_pyramid<<<grid, 256, 0, st>>>((unsigned long long *)d_minz_bits,
+                                             (unsigned long long *)d_accum2, height, width, lv,
+                                             in_block, d_rgb, d_depth, d_alpha, d_flags);
+    LS_LAUNCH_CHECK();
+    if (!filter) return 0;
+    for (int k = 6; k <= L; ++k) {  // levels beyond the in-block five
+        k_min_pool<<<grid_for(lv.h[k] * lv.w[k], 256), 256, 0, st>>>(lv.img[k - 2], lv.h[k - 1],
+                                                                     lv.w[k - 1], lv.img[k - 1]);
+        LS_LAUNCH_CHECK();
+    }
+    return run_filter_steps(lv, up_base, d_depth, height, width, filter->filter_strength,
+                            filter->edge_threshold, nullptr, d_rgb, d_alpha, d_frgb, d_fdepth,
+                            d_falpha, d_keep, reinterpret_cast<__nv_bfloat16 *>(d_unet_in),
+                            unet_c, unet_znear, st);
+}
+
+int ls_filter_depth_image(const float *d_depth, int64_t height, int64_t width,
+                          const ls_filter_params *filter, uint8_t *d_keep, float *d_pyramid,
+                          void *stream) {
+    if (!filter || !d_keep || !d_pyramid || height <= 0 || width <= 0) return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Levels lv{};
+    float *up_base = nullptr;
+    if (!setup_levels(height, width, filter->levels_n, d_pyramid, lv, up_base)) return LS_EINVAL;
+    const int L = lv.L;
+    k_to_sentinel_pool<<<grid_for(lv.h[1] * lv.w[1], 256), 256, 0, st>>>(d_depth, height, width,
+                                                                         lv.img[0]);
+    LS_LAUNCH_CHECK();
+    for (int k = 2; k <= L; ++k) {
+        k_min_pool<<<grid_for(lv.h[k] * lv.w[k], 256), 256, 0, st>>>(lv.img[k - 2], lv.h[k - 1],
+                                                                     lv.w[k - 1], lv.img[k - 1]);
+        LS_LAUNCH_CHECK();
+    }
+    return run_filter_steps(lv, up_base, d_depth, height, width, filter->filter_strength,
+                            filter->edge_threshold, nullptr, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, d_keep, nullptr, 0, 0.0, st);
+}
+
+int ls_depth_filter_frame(const float *d_rgb, const float *d_depth, const uint8_t *d_alpha,
+                          int64_t height, int64_t width, const ls_filter_params *filter,
+                          float *d_frgb, float *d_fdepth, uint8_t *d_falpha, uint8_t *d_keep,
+                          float *d_pyramid, void *stream) {
+    if (!filter || !d_rgb || !d_depth || !d_alpha || !d_pyramid || height <= 0 || width <= 0)
+        return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    Levels lv{};
+    float *up_base = nullptr;
+    if (!setup_levels(height, width, filter->levels_n, d_pyramid, lv, up_base)) return LS_EINVAL;
+    const int L = lv.L;
+    k_to_sentinel_pool<<<grid_for(lv.h[1] * lv.w[1], 256), 256, 0, st>>>(d_depth, height, width,
+                                                                         lv.img[0]);
+    LS_LAUNCH_CHECK();
+    for (int k = 2; k <= L; ++k) {
+        k_min_pool<<<grid_for(lv.h[k] * lv.w[k], 256), 256, 0, st>>>(lv.img[k - 2], lv.h[k - 1],
+                                                                     lv.w[k - 1], lv.img[k - 1]);
+        LS_LAUNCH_CHECK();
+    }
+    return run_filter_steps(lv, up_base, d_depth, height, width, filter->filter_strength,
+                            filter->edge_threshold, nullptr, d_rgb, d_alpha, d_frgb, d_fdepth,
+                            d_falpha, d_keep, nullptr, 0, 0.0, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+// Projection: the two-pass deterministic soft z-buffer (render.py:84-161).
+//
+// Pass 1 folds the per-pixel minimum camera depth with a 64-bit atomicMin on
+// the f64 bit pattern of zc (zc >= z_near > 0, and positive IEEE doubles order
+// like unsigned integers), preceded by a plain L2 read so only improving points
+// pay for an atomic.  Pass 2 recomputes pixel and depth (cheaper than the
+// reference's 16 B/point pix_cache/z_cache round trip) and integer-accumulates
+// colours of every point within the soft tolerance.  Both reductions are
+// order-free, so the result is bit-identical to the reference for any
+// schedule (reference render.py:1-12).
+//
+// Fast path layout: warp tiles of LS_TILE_POINTS = 128 cell-major points; each
+// lane owns 4 consecutive points = 48 contiguous bytes (3 x LDG.128) of xyz and
+// 12 bytes (3 x LDG.32) of rgb.  Per-tile occupied-cell spans (built once per
+// scan) let a warp skip a fully culled tile without touching its points.
+#include "ls_common.cuh"
+
+namespace ls {
+
+// ---------------------------------------------------------------------------
+// (i) twins with the reference's range/cache interface
+// ---------------------------------------------------------------------------
+
+// Exclusive prefix of range lengths (n_ranges is small; one CTA, serial carry).
+__global__ void k_range_prefix(const int64_t *__restrict__ starts, const int64_t *__restrict__ ends,
+                               int64_t nr, int64_t *__restrict__ prefix) {
+    __shared__ int64_t carry;
+    __shared__ int64_t warp_tot[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nr; base += blockDim.x) {
+        int64_t r = base + threadIdx.x;
+        int64_t len = r < nr ? ends[r] - starts[r] : 0;
+        // block inclusive scan
+        int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        int64_t v = len;
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (lane == 31) warp_tot[wid] = v;
+        __syncthreads();
+        if (wid == 0) {
+            int64_t t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t u = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += u;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        int64_t incl = v + (wid > 0 ? warp_tot[wid - 1] : 0) + carry;
+        if (r < nr) prefix[r] = incl - len;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry = incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) prefix[nr] = carry;
+}
+
+__device__ __forceinline__ int64_t find_range(const int64_t *__restrict__ prefix, int64_t nr,
+                                              int64_t k) {
+    // largest r with prefix[r] <= k (ranges may be empty)
+    int64_t lo = 0, hi = nr - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (prefix[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void k_twin_pass1(const float *__restrict__ pos, const int64_t *__restrict__ starts,
+                             const int64_t *__restrict__ prefix, int64_t nr, ProjCam c,
+                             unsigned long long *__restrict__ minz, int64_t *__restrict__ pix_cache,
+                             double *__restrict__ z_cache) {
+    const int64_t n = prefix[nr];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = find_range(prefix, nr, k);
+        int64_t i = starts[r] + (k - prefix[r]);
+        double zc;
+        int64_t pix = project_point(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], c, zc);
+        z_cache[k] = zc;
+        pix_cache[k] = pix;
+        if (pix >= 0) {
+            // caller minz is f64; comparisons on bits are valid for zc > 0 and
+            // any non-negative minz (the only values a z_near > 0 pass produces)
+            unsigned long long key = (unsigned long long)__double_as_longlong(zc);
+            if (key < __ldcg(minz + pix)) atomicMin(minz + pix, key);
+        }
+    }
+}
+
+__global__ void k_twin_pass2(const uint8_t *__restrict__ col, const int64_t *__restrict__ starts,
+                             const int64_t *__restrict__ prefix, int64_t nr,
+                             const int64_t *__restrict__ pix_cache,
+                             const double *__restrict__ z_cache, double ope,
+                             const double *__restrict__ minz,
+                             unsigned long long *__restrict__ accum) {
+    const int64_t n = prefix[nr];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pix = pix_cache[k];
+        if (pix < 0) continue;
+        if (!(z_cache[k] <= dmul(minz[pix], ope))) continue;
+        int64_t r = find_range(prefix, nr, k);
+        int64_t i = starts[r] + (k - prefix[r]);
+        unsigned long long *a = accum + 4 * pix;
+        atomicAdd(a + 0, (unsigned long long)col[3 * i + 0]);
+        atomicAdd(a + 1, (unsigned long long)col[3 * i + 1]);
+        atomicAdd(a + 2, (unsigned long long)col[3 * i + 2]);
+        atomicAdd(a + 3, 1ull);
+    }
+}
+
+__global__ void k_assemble_exact(const double *__restrict__ minz,
+                                 const unsigned long long *__restrict__ accum, int64_t npix,
+                                 float *__restrict__ rgb, float *__restrict__ depth,
+                                 uint8_t *__restrict__ alpha) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npix;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long *a = accum + 4 * p;
+        unsigned long long cnt = a[3];
+        if (cnt > 0) {
+            double denom = dmul((double)cnt, 255.0);
+            rgb[3 * p + 0] = __double2float_rn(ddiv((double)a[0], denom));
+            rgb[3 * p + 1] = __double2float_rn(ddiv((double)a[1], denom));
+            rgb[3 * p + 2] = __double2float_rn(ddiv((double)a[2], denom));
+            depth[p] = __double2float_rn(minz[p]);
+            alpha[p] = 1;
+        } else {
+            rgb[3 * p + 0] = rgb[3 * p + 1] = rgb[3 * p + 2] = 0.0f;
+            depth[p] = 0.0f;
+            alpha[p] = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (ii) fast path: warp tiles over the cell-major scan
+// ---------------------------------------------------------------------------
+
+struct SceneArgs {
+    const float *pos;
+    const uint8_t *col;
+    int64_t n;
+    const int64_t *occ_off;
+    const int32_t *tile_c0;
+    const int32_t *tile_c1;
+    int64_t n_tiles;
+};
+
+// 0 = tile fully culled, 1 = fully kept, 2 = mixed (per-point cell lookup)
+__device__ __forceinline__ int tile_status(const SceneArgs &s, const uint32_t *__restrict__ bits,
+                                           int64_t tile, int lane, int &c0, int &c1) {
+    c0 = __ldg(s.tile_c0 + tile);
+    c1 = __ldg(s.tile_c1 + tile);
+    bool any_keep = false, any_cull = false;
+    for (int j = c0 + lane; j <= c1; j += 32) {
+        bool k = (__ldg(bits + (j >> 5)) >> (j & 31)) & 1u;
+        any_keep |= k;
+        any_cull |= !k;
+    }
+    any_keep = __any_sync(0xffffffffu, any_keep);
+    any_cull = __any_sync(0xffffffffu, any_cull);
+    return any_keep ? (any_cull ? 2 : 1) : 0;
+}
+
+__device__ __forceinline__ bool point_kept(const SceneArgs &s, const uint32_t *__restrict__ bits,
+                                           int c0, int c1, int64_t i) {
+    int lo = c0, hi = c1;  // largest j in [c0,c1] with occ_off[j] <= i
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (__ldg(s.occ_off + mid) <= i) lo = mid; else hi = mid - 1;
+    }
+    return (__ldg(bits + (lo >> 5)) >> (lo & 31)) & 1u;
+}
+
+// Loads the lane's 4 points (xyz) -- vectorised when the group is complete.
+__device__ __forceinline__ int load_points(const SceneArgs &s, int64_t base, float (&P)[12]) {
+    if (base + 4 <= s.n) {
+        const float4 *p4 = reinterpret_cast<const float4 *>(s.pos + 3 * base);
+        float4 a = __ldg(p4), b = __ldg(p4 + 1), c = __ldg(p4 + 2);
+        P[0] = a.x; P[1] = a.y; P[2] = a.z; P[3] = a.w;
+        P[4] = b.x; P[5] = b.y; P[6] = b.z; P[7] = b.w;
+        P[8] = c.x; P[9] = c.y; P[10] = c.z; P[11] = c.w;
+        return 4;
+    }
+    int cnt = 0;
+    for (int k = 0; k < 4; ++k) {
+        if (base + k < s.n) {
+            P[3 * k] = __ldg(s.pos + 3 * (base + k));
+            P[3 * k + 1] = __ldg(s.pos + 3 * (base + k) + 1);
+            P[3 * k + 2] = __ldg(s.pos + 3 * (base + k) + 2);
+            cnt = k + 1;
+        }
+    }
+    return cnt;
+}
+
+__device__ __forceinline__ void load_colors(const SceneArgs &s, int64_t base, int cnt,
+                                            uint8_t (&C)[12]) {
+    if (cnt == 4) {
+        const uint32_t *c4 = reinterpret_cast<const uint32_t *>(s.col + 3 * base);
+        uint32_t w[3] = {__ldg(c4), __ldg(c4 + 1), __ldg(c4 + 2)};
+#pragma unroll
+        for (int b = 0; b < 12; ++b) C[b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+        return;
+    }
+    for (int b = 0; b < 3 * cnt; ++b) C[b] = __ldg(s.col + 3 * base + b);
+}
+
+__global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
+                                                     const uint32_t *__restrict__ bits,
+                                                     unsigned long long *__restrict__ minz) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t tile = w0; tile < s.n_tiles; tile += nw) {
+        int status = 1, c0 = 0, c1 = 0;
+        if (bits) {
+            status = tile_status(s, bits, tile, lane, c0, c1);
+            if (status == 0) continue;
+        }
+        const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
+        float P[12];
+        const int cnt = load_points(s, base, P);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= cnt) break;
+            if (status == 2 && !point_kept(s, bits, c0, c1, base + k)) continue;
+            double zc;
+            int64_t pix = project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc);
+            if (pix < 0) continue;
+            unsigned long long key = (unsigned long long)__double_as_longlong(zc);
+            if (key < __ldcg(minz + pix)) atomicMin(minz + pix, key);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
+                                                     const uint32_t *__restrict__ bits, double ope,
+                                                     const unsigned long long *__restrict__ minz,
+                                                     unsigned long long *__restrict__ acc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t tile = w0; tile < s.n_tiles; tile += nw) {
+        int status = 1, c0 = 0, c1 = 0;
+        if (bits) {
+            status = tile_status(s, bits, tile, lane, c0, c1);
+            if (status == 0) continue;
+        }
+        const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
+        float P[12];
+        uint8_t C[12];
+        const int cnt = load_points(s, base, P);
+        load_colors(s, base, cnt, C);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= cnt) break;
+            if (status == 2 && !point_kept(s, bits, c0, c1, base + k)) continue;
+            double zc;
+            int64_t pix = project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc);
+            if (pix < 0) continue;
+            const double m = __longlong_as_double((long long)__ldcg(minz + pix));
+            if (!(zc <= dmul(m, ope))) continue;
+            const unsigned long long w_rg =
+                (unsigned long long)C[3 * k] | ((unsigned long long)C[3 * k + 1] << 32);
+            const unsigned long long w_bn = (unsigned long long)C[3 * k + 2] | (1ull << 32);
+            atomicAdd(acc + 2 * pix, w_rg);
+            atomicAdd(acc + 2 * pix + 1, w_bn);
+        }
+    }
+}
+
+// Per-scan: occupied-cell span of every warp tile.
+__global__ void k_tile_index(const int64_t *__restrict__ occ_off, int64_t n_occ, int64_t n,
+                             int64_t n_tiles, int32_t *__restrict__ c0, int32_t *__restrict__ c1) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t first = t * LS_TILE_POINTS;
+        int64_t last = min(first + LS_TILE_POINTS, n) - 1;
+        int64_t res[2];
+        int64_t q[2] = {first, last};
+        for (int e = 0; e < 2; ++e) {
+            int64_t lo = 0, hi = n_occ - 1;
+            while (lo < hi) {
+                int64_t mid = (lo + hi + 1) >> 1;
+                if (occ_off[mid] <= q[e]) lo = mid; else hi = mid - 1;
+            }
+            res[e] = lo;
+        }
+        c0[t] = (int32_t)res[0];
+        c1[t] = (int32_t)res[1];
+    }
+}
+
+inline SceneArgs scene_args(const ls_scene &s) {
+    SceneArgs a;
+    a.pos = s.d_positions;
+    a.col = s.d_colors;
+    a.n = s.n_points;
+    a.occ_off = s.d_occ_offsets;
+    a.tile_c0 = s.d_tile_c0;
+    a.tile_c1 = s.d_tile_c1;
+    a.n_tiles = s.n_tiles;
+    return a;
+}
+
+inline bool camera_ok(const ls_camera *cam) {
+    return cam && cam->width > 0 && cam->height > 0 && cam->z_near > 0.0 &&
+           cam->width * cam->height < (int64_t(1) << 40);
+}
+
+// Frame passes: 256-thread CTAs, up to 8 resident per SM (8 warps x 8 = 64
+// warps = full occupancy), grid-stride over warp tiles.
+inline int frame_grid(int64_t n_tiles) { return grid_for(n_tiles * 32, 256, 8); }
+
+}  // namespace ls
+
+using namespace ls;
+
+extern "C" {
+
+size_t ls_ranges_workspace(int64_t n_ranges) { return sizeof(int64_t) * (size_t)(n_ranges + 1); }
+
+int ls_project_min_depth(const float *d_positions, const int64_t *d_starts, const int64_t *d_ends,
+                         int64_t n_ranges, const ls_camera *cam, double *d_minz,
+                         int64_t *d_pix_cache, double *d_z_cache, void *d_workspace,
+                         size_t workspace_bytes, void *stream) {
+    if (n_ranges < 0 || !camera_ok(cam) || workspace_bytes < ls_ranges_workspace(n_ranges))
+        return LS_EINVAL;
+    if (n_ranges == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t *prefix = (int64_t *)d_workspace;
+    k_range_prefix<<<1, 1024, 0, st>>>(d_starts, d_ends, n_ranges, prefix);
+    LS_LAUNCH_CHECK();
+    k_twin_pass1<<<kSmCount * 8, 256, 0, st>>>(d_positions, d_starts, prefix, n_ranges,
+                                              make_cam(*cam), (unsigned long long *)d_minz,
+                                              d_pix_cache, d_z_cache);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_project_accumulate(const uint8_t *d_colors, const int64_t *d_starts, const int64_t *d_ends,
+                          int64_t n_ranges, const int64_t *d_pix_cache, const double *d_z_cache,
+                          double eps_rel, const double *d_minz, uint64_t *d_accum,
+                          void *d_workspace, size_t workspace_bytes, void *stream) {
+    if (n_ranges < 0 || workspace_bytes < ls_ranges_workspace(n_ranges)) return LS_EINVAL;
+    if (n_ranges == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t *prefix = (int64_t *)d_workspace;
+    k_range_prefix<<<1, 1024, 0, st>>>(d_starts, d_ends, n_ranges, prefix);
+    LS_LAUNCH_CHECK();
+    const double ope = 1.0 + eps_rel;  // rounded once (_native.pyx:135)
+    k_twin_pass2<<<kSmCount * 8, 256, 0, st>>>(d_colors, d_starts, prefix, n_ranges, d_pix_cache,
+                                              d_z_cache, ope, d_minz,
+                                              (unsigned long long *)d_accum);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_assemble(const double *d_minz, const uint64_t *d_accum, int64_t n_pixels, float *d_rgb,
+                float *d_depth, uint8_t *d_alpha, void *stream) {
+    if (n_pixels < 0) return LS_EINVAL;
+    if (n_pixels == 0) return 0;
+    k_assemble_exact<<<grid_for(n_pixels, 256), 256, 0, (cudaStream_t)stream>>>(
+        d_minz, (const unsigned long long *)d_accum, n_pixels, d_rgb, d_depth, d_alpha);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_scene_tile_index(const int64_t *d_occ_offsets, int64_t n_occ, int64_t n_points,
+                        int32_t *d_tile_c0, int32_t *d_tile_c1, void *stream) {
+    if (n_occ <= 0 || n_points <= 0 || n_occ >= (int64_t(1) << 31)) return LS_EINVAL;
+    int64_t n_tiles = (n_points + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    k_tile_index<<<grid_for(n_tiles, 256), 256, 0, (cudaStream_t)stream>>>(
+        d_occ_offsets, n_occ, n_points, n_tiles, d_tile_c0, d_tile_c1);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
+                   uint64_t *d_minz_bits, void *stream) {
+    if (!scene || !camera_ok(cam) || scene->n_points < 0) return LS_EINVAL;
+    if (d_keep_bits && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets))
+        return LS_EINVAL;
+    if (scene->n_points == 0) return 0;
+    SceneArgs a = scene_args(*scene);
+    a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    k_frame_pass1<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
+        a, make_cam(*cam), d_keep_bits, (unsigned long long *)d_minz_bits);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
+                   double eps_rel, const uint64_t *d_minz_bits, uint64_t *d_accum2,
+                   void *stream) {
+    if (!scene || !camera_ok(cam) || scene->n_points < 0) return LS_EINVAL;
+    if (d_keep_bits && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets))
+        return LS_EINVAL;
+    if (scene->n_points == 0) return 0;
+    SceneArgs a = scene_args(*scene);
+    a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    const double ope = 1.0 + eps_rel;
+    k_frame_pass2<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
+        a, make_cam(*cam), d_keep_bits, ope, (const unsigned long long *)d_minz_bits,
+        (unsigned long long *)d_accum2);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
+                     double eps_rel, uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
+    int rc = ls_frame_pass1(scene, d_keep_bits, cam, d_minz_bits, stream);
+    if (rc) return rc;
+    return ls_frame_pass2(scene, d_keep_bits, cam, eps_rel, d_minz_bits, d_accum2, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+"""FrameRenderer: the device-resident per-frame pipeline.
+
+What the reference's render service / CLI do per frame (serve.py:55-79,
+cli.py:151-170, bench.py:85-99) -- cull, project, filter, reconstruct -- on a
+scan that stays resident in HBM.  Buffers are allocated once per resolution;
+a frame is a fixed sequence of launches on one stream with no host sync, so
+frames pipeline back to back.  ``render`` is the public end-to-end call (host
+result in pinned memory); ``enqueue`` is the device-only form used for the
+kernel-level throughput number.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .filtering import FilterParams
+from .frame import FrameRGBDA, RenderParams
+from .render import FrameBuffers, project_scene
+
+# kernel launches per frame of the fused path: cull, pass 1, pass 2,
+# assemble+pyramid, L filter steps (+ U-Net layers when attached)
+BASE_LAUNCHES = 4
+
+
+class FrameRenderer:
+    def __init__(self, grid, width: int, height: int, render_params: RenderParams | None = None,
+                 filter_params: FilterParams | None = None, unet=None):
+        import torch
+
+        self.device = _lib.device()
+        self.scene = grid.scene()
+        self.width, self.height = int(width), int(height)
+        self.rp = render_params or RenderParams()
+        self.fp = filter_params or FilterParams()
+        self.bufs = FrameBuffers(width, height, self.device)
+        h, w, dev = self.height, self.width, self.device
+        self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.fdepth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.falpha = torch.empty((h, w), dtype=torch.uint8, device=dev)
+        n = _lib.load().ls_pyramid_floats(h, w, self.fp.levels_n)
+        if n < 0:
+            raise ValueError(f"image {w}x{h} too small for {self.fp.levels_n} pyramid levels")
+        self.pyramid = torch.empty(int(n), dtype=torch.float32, device=dev)
+        self.unet = unet
+        self.unet_in = None
+        self.rgb_out = None
+        if unet is not None:
+            uh = (h + unet.divisor - 1) // unet.divisor * unet.divisor
+            uw = (w + unet.divisor - 1) // unet.divisor * unet.divisor
+            if uw != w:
+                raise ValueError("frame width must be divisible by 2^depth for the U-Net")
+            self.unet_in = torch.zeros((1, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
+            self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
+        self._pinned = None
+
+    @property
+    def launches_per_frame(self) -> int:
+        n = BASE_LAUNCHES + self.fp.levels_n
+        if self.unet is not None:
+            n += self.unet.launches
+        return n
+
+    def enqueue(self, camera, events=None) -> None:
+        """Enqueue one full frame on the current stream (no host sync).
+        ``events`` (optional list of 3 CUDA events) marks project / filter /
+        U-Net boundaries for per-stage timing."""
+        project_scene(self.scene, camera, self.rp.zbuffer_epsilon_rel, self.bufs, cull=True,
+                      filter_params=self.fp, filtered=(self.frgb, self.fdepth, self.falpha),
+                      unet_in=None if self.unet is None else self.unet_in[0],
+                      pyramid=self.pyramid, stage_events=events)
+        if self.unet is not None:
+            self.unet.forward(self.unet_in, self.rgb_out)
+        if events is not None:
+            events[-1].record()
+
+    def check_flags(self) -> None:
+        if int(self.bufs.flags.item()):
+            raise RuntimeError("packed accumulator bound exceeded; use project_points() for "
+                               "the exact path")
+
+    def render(self, camera):
+        """Public end-to-end call: one frame, result copied to pinned host
+        memory.  Returns the reconstructed RGB (H,W,3) f32 when a U-Net is
+        attached, else the filtered FrameRGBDA."""
+        import torch
+
+        self.enqueue(camera)
+        if self._pinned is None:
+            if self.unet is not None:
+                self._pinned = (torch.empty((self.height, self.width, 3), dtype=torch.float32,
+                                            pin_memory=True),)
+            else:
+                self._pinned = (torch.empty_like(self.frgb, device="cpu", pin_memory=True),
+                                torch.empty_like(self.fdepth, device="cpu", pin_memory=True),
+                                torch.empty_like(self.falpha, device="cpu", pin_memory=True))
+        if self.unet is not None:
+            self._pinned[0].copy_(self.rgb_out[0, : self.height], non_blocking=True)
+        else:
+            for dst, src in zip(self._pinned, (self.frgb, self.fdepth, self.falpha)):
+                dst.copy_(src, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if self.unet is not None:
+            return self._pinned[0].numpy()
+        return FrameRGBDA(*(t.numpy() for t in self._pinned))
+
+    @property
+    def d2h_bytes(self) -> int:
+        if self.unet is not None:
+            return self.height * self.width * 3 * 4
+        return self.height * self.width * (3 * 4 + 4 + 1)

@@ -1,0 +1,209 @@
+"""Deterministic point projection into an RGBDA frame (reference render.py).
+
+Two passes over the candidate points, on the GPU:
+  pass 1: per-pixel minimum camera depth (64-bit atomicMin on the f64 bits)
+  pass 2: integer colour sums of every point with zc <= minz*(1+eps)
+then the integer-mean assembly.  Min and integer add are order-free, so the
+frame is bit-identical to the reference for any point order and schedule.
+
+``project_points`` on a grid runs the device fast path: culling bits + warp
+tile passes over the resident cell-major scan + the fused assembly kernel.
+``project_candidates`` keeps the reference's range/cache interface (the
+backend-protocol twins).  Both return frames identical to the reference's.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._kernels import get_backend
+from .cloud import PointCloud
+from .frame import FrameRGBDA, RenderParams
+from .geometry import CameraModel, extract_frustum
+from .grid import DeviceScene, UniformGrid, cull_cells
+
+
+def worker_count(n_points: int) -> int:
+    """Kept for API compatibility: one GPU stream does the whole pass."""
+    return 1
+
+
+@dataclass
+class Candidates:
+    """Points surviving cell culling: ranges into position/colour arrays."""
+
+    positions: np.ndarray
+    colors: np.ndarray
+    starts: np.ndarray
+    ends: np.ndarray
+
+    @property
+    def count(self) -> int:
+        return int((self.ends - self.starts).sum())
+
+
+def candidates(cloud: PointCloud, grid: UniformGrid | None, camera: CameraModel) -> Candidates:
+    """Candidate set for a view: the whole cloud when ``grid`` is None, else the
+    merged ranges of the frustum-culled cells (culled on the GPU)."""
+    if grid is None:
+        return Candidates(cloud.positions, cloud.colors, np.zeros(1, np.int64),
+                          np.array([cloud.count], np.int64))
+    starts, ends = grid.cell_ranges(cull_cells(grid, extract_frustum(camera)))
+    return Candidates(grid.sorted_positions, grid.sorted_colors, starts, ends)
+
+
+def project_candidates(cands: Candidates, camera: CameraModel, params: RenderParams,
+                       backend=None, workers: int | None = None) -> FrameRGBDA:
+    """Rasterise candidate ranges with the reference's two-pass interface."""
+    import torch
+
+    kern = get_backend() if backend is None else backend
+    w, h = int(camera.width), int(camera.height)
+    rot = camera.world_to_camera.rotation
+    t = camera.world_to_camera.translation
+    n = cands.count
+    minz = np.full(h * w, np.inf)
+    pix = np.empty(n, np.int64)
+    z = np.empty(n, np.float64)
+    starts = np.ascontiguousarray(cands.starts, np.int64)
+    ends = np.ascontiguousarray(cands.ends, np.int64)
+    kern.project_min_depth(cands.positions, starts, ends, rot, t, float(camera.fx),
+                           float(camera.fy), float(camera.cx), float(camera.cy), w, h,
+                           float(camera.z_near), float(camera.z_far), minz, pix, z)
+    accum = np.zeros((h * w, 4), np.uint64)
+    kern.project_accumulate(cands.colors, starts, ends, pix, z,
+                            float(params.zbuffer_epsilon_rel), minz, accum)
+    return assemble_frame(minz, accum, w, h)
+
+
+def assemble_frame(minz: np.ndarray, accum: np.ndarray, width: int, height: int) -> FrameRGBDA:
+    """Fold pass buffers (f64 minz, u64 x4 accum) into a frame on the GPU."""
+    import torch
+
+    dev = _lib.device()
+    npix = width * height
+    d_minz = torch.from_numpy(np.ascontiguousarray(minz, np.float64)).to(dev)
+    d_acc = torch.from_numpy(np.ascontiguousarray(accum).view(np.int64)).to(dev)
+    rgb = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
+    depth = torch.empty((height, width), dtype=torch.float32, device=dev)
+    alpha = torch.empty((height, width), dtype=torch.uint8, device=dev)
+    _lib.check(_lib.load().ls_assemble(d_minz.data_ptr(), d_acc.data_ptr(), npix,
+                                       rgb.data_ptr(), depth.data_ptr(), alpha.data_ptr(),
+                                       _lib.stream_ptr()), "assemble")
+    return FrameRGBDA(rgb.cpu().numpy(), depth.cpu().numpy(), alpha.cpu().numpy())
+
+
+class FrameBuffers:
+    """Per-resolution device buffers of the fused frame path."""
+
+    def __init__(self, width: int, height: int, device):
+        import torch
+
+        self.width, self.height = int(width), int(height)
+        npix = self.width * self.height
+        self.minz = torch.full((npix,), _lib.INF_BITS, dtype=torch.int64, device=device)
+        self.accum = torch.zeros((npix, 2), dtype=torch.int64, device=device)
+        self.rgb = torch.empty((self.height, self.width, 3), dtype=torch.float32, device=device)
+        self.depth = torch.empty((self.height, self.width), dtype=torch.float32, device=device)
+        self.alpha = torch.empty((self.height, self.width), dtype=torch.uint8, device=device)
+        self.flags = torch.zeros(1, dtype=torch.int32, device=device)
+
+
+def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs: FrameBuffers,
+                  cull: bool = True, filter_params=None, filtered=None, keep=None,
+                  unet_in=None, unet_znear: float = 0.1, pyramid=None,
+                  stage_events=None) -> None:
+    """Enqueue one fused frame on the current stream (no host sync):
+    cull -> pass 1 -> pass 2 -> assemble (+ filter / U-Net input).
+    ``stage_events``: optional CUDA events recorded after cull, pass 1,
+    pass 2 and assemble/filter."""
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    cam = _lib.make_camera(camera)
+    ev = stage_events or [None] * 4
+    bits = None
+    if cull:
+        bits = scene.cull_bits(extract_frustum(camera).planes).data_ptr()
+    if ev[0] is not None:
+        ev[0].record()
+    _lib.check(lib.ls_frame_pass1(scene.struct, bits, cam, bufs.minz.data_ptr(), st),
+               "frame_pass1")
+    if ev[1] is not None:
+        ev[1].record()
+    _lib.check(lib.ls_frame_pass2(scene.struct, bits, cam, float(eps_rel), bufs.minz.data_ptr(),
+                                  bufs.accum.data_ptr(), st), "frame_pass2")
+    if ev[2] is not None:
+        ev[2].record()
+    fp = None if filter_params is None else _lib.make_filter(filter_params)
+    frgb = fdepth = falpha = None
+    if filtered is not None:
+        frgb, fdepth, falpha = (_lib.ptr(filtered[0]), _lib.ptr(filtered[1]),
+                                _lib.ptr(filtered[2]))
+    unet_h, unet_c = (0, 0) if unet_in is None else (int(unet_in.shape[-3]),
+                                                      int(unet_in.shape[-1]))
+    _lib.check(lib.ls_frame_finish(bufs.minz.data_ptr(), bufs.accum.data_ptr(), bufs.width,
+                                   bufs.height, fp, bufs.rgb.data_ptr(), bufs.depth.data_ptr(),
+                                   bufs.alpha.data_ptr(), frgb, fdepth, falpha, _lib.ptr(keep),
+                                   _lib.ptr(unet_in), unet_h, unet_c, float(unet_znear),
+                                   _lib.ptr(pyramid), bufs.flags.data_ptr(), st), "frame_finish")
+    if ev[3] is not None:
+        ev[3].record()
+
+
+def _exact_frame(cloud, grid, camera, params):
+    """Exact (u64 x 4) path, used if a pixel may exceed the packed bound."""
+    cands = candidates(cloud, grid, camera)
+    return project_candidates(cands, camera, params)
+
+
+def project_points(cloud: PointCloud, grid: UniformGrid | None, camera: CameraModel,
+                   params: RenderParams | None = None, backend=None,
+                   workers: int | None = None) -> FrameRGBDA:
+    """Render ``cloud`` through ``camera``.  With a grid the candidates come
+    from frustum-culled cells; with ``grid=None`` every point is considered.
+    Both yield bit-identical frames (reference render.py:164-178)."""
+    params = params or RenderParams()
+    if backend is not None and getattr(backend, "name", "cuda") != "cuda":
+        raise ValueError(f"unknown backend {backend!r}")
+    dev = _lib.device()
+    if grid is None:
+        pos, col = cloud.device_arrays()
+        scene = _brute_scene(cloud, pos, col)
+        cull = False
+    else:
+        scene = grid.scene()
+        cull = True
+    bufs = FrameBuffers(camera.width, camera.height, dev)
+    if scene.n_points:
+        project_scene(scene, camera, params.zbuffer_epsilon_rel, bufs, cull=cull)
+    else:
+        return FrameRGBDA.empty(camera.width, camera.height)
+    if int(bufs.flags.item()) & 1:
+        return _exact_frame(cloud, grid, camera, params)
+    return FrameRGBDA(bufs.rgb.cpu().numpy(), bufs.depth.cpu().numpy(),
+                      bufs.alpha.cpu().numpy())
+
+
+class _BruteScene:
+    """The whole cloud, input order, no culling (grid=None reference path)."""
+
+    def __init__(self, pos, col):
+        self.n_points = int(pos.shape[0])
+        s = _lib.LsScene()
+        s.d_positions, s.d_colors, s.n_points = pos.data_ptr(), col.data_ptr(), self.n_points
+        s.n_tiles = (self.n_points + _lib.LS_TILE_POINTS - 1) // _lib.LS_TILE_POINTS
+        s.cell_size = 1.0
+        self.struct = s
+        self._keep = (pos, col)
+
+
+def _brute_scene(cloud, pos, col):
+    key = "brute:" + str(pos.device)
+    sc = cloud._device.get(key)
+    if sc is None:
+        sc = _BruteScene(pos, col)
+        cloud._device[key] = sc
+    return sc

@@ -1,0 +1,204 @@
+"""Projection on the B200 vs the reference (ports of pkg/tests/test_projection.py
+and test_acceptance.py:85-112) -- bit-exact RGBDA."""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import (GOLDEN, golden, golden_camera, make_camera, plain_camera, random_cloud,
+                      random_view, two_plane_cloud)
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu(cuda_ready):
+    return cuda_ready
+
+
+def _eq(a, b):
+    return (np.array_equal(a.rgb, b.rgb) and np.array_equal(a.depth, b.depth)
+            and np.array_equal(a.alpha, b.alpha))
+
+
+def test_single_point_principal_pixel():
+    from lidarsplat import PointCloud, project_points
+
+    cam = make_camera()
+    z = 2 * cam.z_near
+    fr = project_points(PointCloud(np.array([[0.0, 0.0, z]], np.float32),
+                                   np.array([[255, 0, 0]], np.uint8)), None, cam)
+    px, py = int(math.floor(cam.cx)), int(math.floor(cam.cy))
+    assert fr.alpha.sum() == 1 and fr.alpha[py, px] == 1
+    assert fr.depth[py, px] == np.float32(z)
+    assert tuple(fr.rgb[py, px]) == (1.0, 0.0, 0.0)
+
+
+def test_soft_zbuffer_and_occlusion():
+    from lidarsplat import PointCloud, RenderParams, project_points
+
+    cam = make_camera()
+    px, py = int(cam.cx), int(cam.cy)
+    cols = np.array([[255, 0, 0], [0, 0, 255]], np.uint8)
+    soft = project_points(PointCloud(np.array([[0, 0, 1.0], [0, 0, 1.005]], np.float32), cols),
+                          None, cam, RenderParams(zbuffer_epsilon_rel=0.01))
+    assert soft.depth[py, px] == np.float32(1.0)
+    assert np.allclose(soft.rgb[py, px], [0.5, 0.0, 0.5])
+    occ = project_points(PointCloud(np.array([[0, 0, 1.0], [0, 0, 2.0]], np.float32), cols),
+                         None, cam, RenderParams(zbuffer_epsilon_rel=0.01))
+    assert tuple(occ.rgb[py, px]) == (1.0, 0.0, 0.0)
+
+
+def test_behind_and_out_of_range_skipped():
+    from lidarsplat import PointCloud, project_points
+
+    cam = make_camera()
+    pts = np.array([[0, 0, -1.0], [0, 0, 0.0], [0, 0, cam.z_near / 2], [0, 0, cam.z_far * 1.5]],
+                   np.float32)
+    fr = project_points(PointCloud(pts, np.full((4, 3), 255, np.uint8)), None, cam)
+    assert fr.alpha.sum() == 0
+    fr.validate()
+
+
+@pytest.mark.parametrize("s", range(5))
+def test_matches_reference_rasterizer_golden(s):
+    """Golden from reference.py:14-72 (pure-Python two-pass rasterizer)."""
+    from lidarsplat import PointCloud, RenderParams, project_points
+
+    d = golden("project.npz")
+    p = f"s{s}_"
+    fr = project_points(PointCloud(d[p + "pos"], d[p + "col"]), None, golden_camera(d, p),
+                        RenderParams(zbuffer_epsilon_rel=0.05))
+    assert np.array_equal(fr.alpha, d[p + "alpha"])
+    assert np.array_equal(fr.depth, d[p + "depth"])
+    assert np.array_equal(fr.rgb, d[p + "rgb"])
+
+
+def test_culled_equals_brute_force_and_oracle(rng, port):
+    from lidarsplat import build_grid, project_points
+
+    for _ in range(5):
+        cloud = random_cloud(rng, 50_000, extent=12.0, offset=-6.0)
+        cam = random_view(rng, cloud)
+        grid = build_grid(cloud, 1.0)
+        a = project_points(cloud, grid, cam)
+        b = project_points(cloud, None, cam)
+        assert _eq(a, b)
+        rgb, depth, alpha, _, _ = O.project(cloud.positions, cloud.colors, np.zeros(1, np.int64),
+                                            np.array([cloud.count], np.int64), cam, 0.01, port)
+        assert np.array_equal(a.rgb, rgb) and np.array_equal(a.depth, depth)
+        assert np.array_equal(a.alpha, alpha)
+
+
+def test_culling_transparency_acceptance():
+    """test_acceptance.py:85-98 (20 configs, up to 200k points)."""
+    from lidarsplat import build_grid, project_points
+
+    rng = np.random.default_rng(101)
+    for trial in range(20):
+        n = int(rng.integers(1_000, 200_001))
+        ext = float(rng.uniform(2.0, 25.0))
+        cloud = random_cloud(rng, n, extent=ext, offset=-ext / 2)
+        cam = random_view(rng, cloud)
+        grid = build_grid(cloud, float(rng.uniform(0.5, 2.0)))
+        assert _eq(project_points(cloud, grid, cam), project_points(cloud, None, cam)), trial
+
+
+def test_order_invariance():
+    from lidarsplat import build_grid, project_points
+
+    rng = np.random.default_rng(202)
+    for _ in range(10):
+        cloud = random_cloud(rng, int(rng.integers(500, 30_000)), extent=8.0)
+        cam = random_view(rng, cloud)
+        base = project_points(cloud, build_grid(cloud, 1.0), cam)
+        sh = cloud.permuted(rng.permutation(cloud.count))
+        assert _eq(base, project_points(sh, build_grid(sh, 1.0), cam))
+
+
+def test_depth_is_exact_per_pixel_minimum(rng):
+    from lidarsplat import project_points
+
+    cloud = random_cloud(rng, 5000, extent=4.0)
+    cam = random_view(rng, cloud)
+    fr = project_points(cloud, None, cam)
+    fr.validate()
+    u, v, z = cam.project(cloud.positions)
+    ok = ((z >= cam.z_near) & (z <= cam.z_far) & (u >= 0) & (u < cam.width) & (v >= 0)
+          & (v < cam.height))
+    best = {}
+    for ui, vi, zi in zip(u[ok], v[ok], z[ok]):
+        k = (int(math.floor(vi)), int(math.floor(ui)))
+        best[k] = min(best.get(k, np.inf), zi)
+    for (py, px), zmin in best.items():
+        assert fr.depth[py, px] == np.float32(zmin)
+
+
+def test_two_plane_scene():
+    from lidarsplat import project_points
+
+    cam = make_camera()
+    cloud, checker = two_plane_cloud(cam)
+    fr = project_points(cloud, None, cam)
+    assert fr.alpha.all()
+    assert np.array_equal(fr.depth, np.where(checker, np.float32(1.0), np.float32(5.0)))
+
+
+def test_pipeline_golden_culled():
+    from lidarsplat import FilterParams, PointCloud, RenderParams, build_grid, depth_filter
+    from lidarsplat import project_points
+
+    d = golden("pipeline.npz")
+    cloud = PointCloud(d["a_pos"], d["a_col"])
+    fr = project_points(cloud, build_grid(cloud, 1.0), golden_camera(d, "a_"), RenderParams())
+    assert np.array_equal(fr.rgb, d["a_rgb"]) and np.array_equal(fr.depth, d["a_depth"])
+    assert np.array_equal(fr.alpha, d["a_alpha"])
+    ft = depth_filter(fr, FilterParams())
+    assert np.array_equal(ft.rgb, d["a_frgb"]) and np.array_equal(ft.depth, d["a_fdepth"])
+    assert np.array_equal(ft.alpha, d["a_falpha"])
+
+
+def test_cull_cells_golden():
+    from lidarsplat import PointCloud, build_grid, cull_cells, extract_frustum
+
+    d = golden("cull.npz")
+    for s in range(6):
+        p = f"s{s}_"
+        grid = build_grid(PointCloud(d[p + "pos"], d[p + "col"]), float(d[p + "cell"]))
+        assert np.array_equal(grid.point_order, d[p + "order"])
+        assert np.array_equal(grid.cell_offsets, d[p + "offsets"])
+        fr = extract_frustum(golden_camera(d, p))
+        assert np.array_equal(fr.planes, d[p + "planes"])
+        assert np.array_equal(cull_cells(grid, fr), d[p + "culled"])
+
+
+def test_c1_reference_digest():
+    """C1 (1M uniform box, 512x512) through build_grid + project_points +
+    depth_filter equals the reference's own output (sha256 golden)."""
+    import hashlib
+
+    from lidarsplat import (CameraModel, FilterParams, PointCloud, RenderParams, build_grid,
+                            cull_cells, depth_filter, extract_frustum, project_points)
+    from test_oracle_golden import c1_scene
+
+    def dg(*arrs):
+        h = hashlib.sha256()
+        for a in arrs:
+            h.update(np.ascontiguousarray(a).tobytes())
+        return h.hexdigest()
+
+    info = json.load(open(os.path.join(GOLDEN, "c1.json")))
+    pts, cols = c1_scene()
+    cloud = PointCloud(pts, cols)
+    cam = CameraModel(fx=350.0, fy=350.0, cx=256.0, cy=256.0, width=512, height=512)
+    grid = build_grid(cloud, 1.0)
+    assert dg(grid.point_order) == info["grid_order"]
+    assert dg(cull_cells(grid, extract_frustum(cam))) == info["culled"]
+    fr = project_points(cloud, grid, cam, RenderParams())
+    assert dg(fr.rgb, fr.depth, fr.alpha) == info["frame"]
+    ft = depth_filter(fr, FilterParams())
+    assert dg(ft.rgb, ft.depth, ft.alpha) == info["filtered"]
