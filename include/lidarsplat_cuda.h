@@ -156,22 +156,34 @@ int ls_cull_compact(const uint32_t *d_keep_bits, const int64_t *d_occ_cells, int
                     int64_t *d_out_cells, int64_t *d_count, void *d_workspace,
                     size_t workspace_bytes, void *stream);
 
-/* Both projection passes over the culled scan (d_keep_bits NULL = no cull).
+/* Per-frame work list of the non-culled warp tiles (after ls_cull): d_list
+ * receives one u32 per tile that keeps any point (bit 31 = tile straddles a
+ * culled cell), d_count (1 u32, reset by this call) their number.  d_list
+ * must hold n_tiles entries. */
+int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
+                     uint32_t *d_count, void *stream);
+
+/* Both projection passes over the culled scan.  d_keep_bits NULL = no cull
+ * (every point is a candidate; d_list/d_count are then ignored), else the
+ * work list is built first (ls_tile_worklist).
  * d_minz_bits: (H*W) u64, the f64 bit pattern of the running minimum,
  *   must hold +inf (0x7FF0000000000000) on entry.
  * d_accum2: (H*W x 2) u64 packed accumulators {r | g<<32, b | count<<32},
  *   zero on entry.  Exact while no pixel keeps > LS_PACKED_COUNT_LIMIT points;
  *   ls_frame_finish flags a frame where that bound could be exceeded. */
-int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                     double eps_rel, uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream);
+int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
+                     uint32_t *d_count, const ls_camera *cam, double eps_rel,
+                     uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream);
 
-/* Pass 1 only / pass 2 only of ls_frame_project (multi-GPU: an all-reduce MIN
- * of d_minz_bits runs between them, a reduce SUM of d_accum2 after). */
-int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                   uint64_t *d_minz_bits, void *stream);
-int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                   double eps_rel, const uint64_t *d_minz_bits, uint64_t *d_accum2,
+/* Pass 1 only / pass 2 only of ls_frame_project over an existing work list
+ * (d_list NULL = all tiles).  Multi-GPU: an all-reduce MIN of d_minz_bits
+ * runs between them, a reduce SUM of d_accum2 after. */
+int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
+                   const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
                    void *stream);
+int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
+                   const uint32_t *d_count, const ls_camera *cam, double eps_rel,
+                   const uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream);
 
 /* Level sizes of the min pyramid (filtering.py:67-83); returns the float
  * count of the workspace ls_frame_finish needs for levels 0..L-1. */

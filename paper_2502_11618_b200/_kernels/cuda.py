@@ -35,6 +35,22 @@ def _need(arr, dtype, ndim, what, writable=False):
     return arr
 
 
+class _Stage:
+    """Host->device staging that keeps every uploaded tensor alive until the
+    call's results are read back (a bare ``tensor.data_ptr()`` would let the
+    caching allocator recycle the block while the kernel is still queued)."""
+
+    def __init__(self):
+        self.keep = []
+
+    def __call__(self, arr) -> int:
+        import torch
+
+        t = torch.from_numpy(np.array(arr, copy=True)).to(_lib.device())
+        self.keep.append(t)
+        return t.data_ptr()
+
+
 def _dev(arr):
     import torch
 
@@ -62,19 +78,21 @@ def _cam(rot, t, fx, fy, cx, cy, width, height, z_near, z_far):
 
 
 def assign_cells(positions, origin, cell_size, dims):
+    up = _Stage()
     _need(positions, np.float32, 2, "positions")
     origin = np.ascontiguousarray(_need(origin, np.float64, 1, "origin"))
     dims = np.ascontiguousarray(_need(dims, np.int64, 1, "dims"))
     n = positions.shape[0]
     ids = _empty((n,), __import__("torch").int64)
     lib = _lib.load()
-    _lib.check(lib.ls_assign_cells(_dev(positions).data_ptr(), n,
+    _lib.check(lib.ls_assign_cells(up(positions), n,
                                    origin.ctypes.data, float(cell_size), dims.ctypes.data,
                                    ids.data_ptr(), _lib.stream_ptr()), "assign_cells")
     return _host(ids)
 
 
 def counting_sort(ids, n_cells):
+    up = _Stage()
     import torch
 
     _need(ids, np.int64, 1, "ids")
@@ -89,7 +107,7 @@ def counting_sort(ids, n_cells):
     ws = _empty((ws_bytes,), torch.uint8)
     d_off = _empty((n_cells + 1,), torch.int64)
     d_order = _empty((n,), torch.int64)
-    _lib.check(lib.ls_counting_sort(_dev(ids).data_ptr(), n, n_cells, d_off.data_ptr(),
+    _lib.check(lib.ls_counting_sort(up(ids), n, n_cells, d_off.data_ptr(),
                                     d_order.data_ptr(), ws.data_ptr(), ws_bytes,
                                     _lib.stream_ptr()), "counting_sort")
     return _host(d_off), _host(d_order)
@@ -97,6 +115,7 @@ def counting_sort(ids, n_cells):
 
 def project_min_depth(positions, starts, ends, rot, t, fx, fy, cx, cy, width, height,
                       z_near, z_far, minz, pix_cache, z_cache):
+    up = _Stage()
     import torch
 
     _need(positions, np.float32, 2, "positions")
@@ -115,8 +134,8 @@ def project_min_depth(positions, starts, ends, rot, t, fx, fy, cx, cy, width, he
     d_z = _empty(z_cache.shape, torch.float64)
     ws_bytes = lib.ls_ranges_workspace(nr)
     ws = _empty((ws_bytes,), torch.uint8)
-    _lib.check(lib.ls_project_min_depth(_dev(positions).data_ptr(), _dev(starts).data_ptr(),
-                                        _dev(ends).data_ptr(), nr, cam, d_minz.data_ptr(),
+    _lib.check(lib.ls_project_min_depth(up(positions), up(starts),
+                                        up(ends), nr, cam, d_minz.data_ptr(),
                                         d_pix.data_ptr(), d_z.data_ptr(), ws.data_ptr(),
                                         ws_bytes, _lib.stream_ptr()), "project_min_depth")
     minz[:] = _host(d_minz)
@@ -126,6 +145,7 @@ def project_min_depth(positions, starts, ends, rot, t, fx, fy, cx, cy, width, he
 
 
 def project_accumulate(colors, starts, ends, pix_cache, z_cache, eps_rel, minz, accum):
+    up = _Stage()
     import torch
 
     _need(colors, np.uint8, 2, "colors")
@@ -142,39 +162,42 @@ def project_accumulate(colors, starts, ends, pix_cache, z_cache, eps_rel, minz, 
     d_acc = _dev(accum.view(np.int64))
     ws_bytes = lib.ls_ranges_workspace(nr)
     ws = _empty((ws_bytes,), torch.uint8)
-    _lib.check(lib.ls_project_accumulate(_dev(colors).data_ptr(), _dev(starts).data_ptr(),
-                                         _dev(ends).data_ptr(), nr, _dev(pix_cache).data_ptr(),
-                                         _dev(z_cache).data_ptr(), float(eps_rel),
-                                         _dev(minz).data_ptr(), d_acc.data_ptr(), ws.data_ptr(),
+    _lib.check(lib.ls_project_accumulate(up(colors), up(starts),
+                                         up(ends), nr, up(pix_cache),
+                                         up(z_cache), float(eps_rel),
+                                         up(minz), d_acc.data_ptr(), ws.data_ptr(),
                                          ws_bytes, _lib.stream_ptr()), "project_accumulate")
     accum[:] = _host(d_acc).view(np.uint64)
     return None
 
 
 def min_pool_2x2(img):
+    up = _Stage()
     import torch
 
     _need(img, np.float32, 2, "img")
     h, w = img.shape
     out = _empty(((h + 1) // 2, (w + 1) // 2), torch.float32)
-    _lib.check(_lib.load().ls_min_pool_2x2(_dev(img).data_ptr(), h, w, out.data_ptr(),
+    _lib.check(_lib.load().ls_min_pool_2x2(up(img), h, w, out.data_ptr(),
                                            _lib.stream_ptr()), "min_pool_2x2")
     return _host(out)
 
 
 def laplacian_edges(img, threshold):
+    up = _Stage()
     import torch
 
     _need(img, np.float32, 2, "img")
     h, w = img.shape
     out = _empty((h, w), torch.uint8)
-    _lib.check(_lib.load().ls_laplacian_edges(_dev(img).data_ptr(), h, w, float(threshold),
+    _lib.check(_lib.load().ls_laplacian_edges(up(img), h, w, float(threshold),
                                               out.data_ptr(), _lib.stream_ptr()),
                "laplacian_edges")
     return _host(out)
 
 
 def filter_keep(coarse, edges, fine, filter_strength):
+    up = _Stage()
     import torch
 
     _need(coarse, np.float32, 2, "coarse")
@@ -183,14 +206,15 @@ def filter_keep(coarse, edges, fine, filter_strength):
     ch, cw = coarse.shape
     fh, fw = fine.shape
     out = _empty((fh, fw), torch.float32)
-    _lib.check(_lib.load().ls_filter_keep(_dev(coarse).data_ptr(), ch, cw,
-                                          _dev(edges).data_ptr(), _dev(fine).data_ptr(), fh, fw,
+    _lib.check(_lib.load().ls_filter_keep(up(coarse), ch, cw,
+                                          up(edges), up(fine), fh, fw,
                                           float(filter_strength), out.data_ptr(),
                                           _lib.stream_ptr()), "filter_keep")
     return _host(out)
 
 
 def bilinear_fill(coarse, fine):
+    up = _Stage()
     import torch
 
     _need(coarse, np.float32, 2, "coarse")
@@ -198,7 +222,7 @@ def bilinear_fill(coarse, fine):
     ch, cw = coarse.shape
     fh, fw = fine.shape
     out = _empty((fh, fw), torch.float32)
-    _lib.check(_lib.load().ls_bilinear_fill(_dev(coarse).data_ptr(), ch, cw,
-                                            _dev(fine).data_ptr(), fh, fw, out.data_ptr(),
+    _lib.check(_lib.load().ls_bilinear_fill(up(coarse), ch, cw,
+                                            up(fine), fh, fw, out.data_ptr(),
                                             _lib.stream_ptr()), "bilinear_fill")
     return _host(out)

@@ -13,6 +13,8 @@
 // lane owns 4 consecutive points = 48 contiguous bytes (3 x LDG.128) of xyz and
 // 12 bytes (3 x LDG.32) of rgb.  Per-tile occupied-cell spans (built once per
 // scan) let a warp skip a fully culled tile without touching its points.
+#include <stdlib.h>
+
 #include "ls_common.cuh"
 
 namespace ls {
@@ -150,22 +152,6 @@ struct SceneArgs {
     int64_t n_tiles;
 };
 
-// 0 = tile fully culled, 1 = fully kept, 2 = mixed (per-point cell lookup)
-__device__ __forceinline__ int tile_status(const SceneArgs &s, const uint32_t *__restrict__ bits,
-                                           int64_t tile, int lane, int &c0, int &c1) {
-    c0 = __ldg(s.tile_c0 + tile);
-    c1 = __ldg(s.tile_c1 + tile);
-    bool any_keep = false, any_cull = false;
-    for (int j = c0 + lane; j <= c1; j += 32) {
-        bool k = (__ldg(bits + (j >> 5)) >> (j & 31)) & 1u;
-        any_keep |= k;
-        any_cull |= !k;
-    }
-    any_keep = __any_sync(0xffffffffu, any_keep);
-    any_cull = __any_sync(0xffffffffu, any_cull);
-    return any_keep ? (any_cull ? 2 : 1) : 0;
-}
-
 __device__ __forceinline__ bool point_kept(const SceneArgs &s, const uint32_t *__restrict__ bits,
                                            int c0, int c1, int64_t i) {
     int lo = c0, hi = c1;  // largest j in [c0,c1] with occ_off[j] <= i
@@ -174,6 +160,39 @@ __device__ __forceinline__ bool point_kept(const SceneArgs &s, const uint32_t *_
         if (__ldg(s.occ_off + mid) <= i) lo = mid; else hi = mid - 1;
     }
     return (__ldg(bits + (lo >> 5)) >> (lo & 31)) & 1u;
+}
+
+// Work list of the frame: one u32 per non-culled warp tile, bit 31 = mixed
+// (some of its cells culled).  One thread per tile, warp-aggregated append;
+// list order is irrelevant (both passes are order-free reductions).
+constexpr uint32_t kMixed = 0x80000000u;
+
+__global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *__restrict__ bits,
+                                                   uint32_t *__restrict__ list,
+                                                   uint32_t *__restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31);
+         base < s.n_tiles;
+         base += stride) {
+        const int64_t t = base + lane;
+        bool keep_any = false, cull_any = false;
+        if (t < s.n_tiles) {
+            const int c0 = __ldg(s.tile_c0 + t), c1 = __ldg(s.tile_c1 + t);
+            for (int j = c0; j <= c1; ++j) {
+                const bool k = (__ldg(bits + (j >> 5)) >> (j & 31)) & 1u;
+                keep_any |= k;
+                cull_any |= !k;
+            }
+        }
+        const uint32_t vote = __ballot_sync(0xffffffffu, keep_any);
+        if (vote == 0u) continue;
+        uint32_t off = 0;
+        if (lane == 0) off = atomicAdd(count, (uint32_t)__popc(vote));
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (keep_any)
+            list[off + __popc(vote & ((1u << lane) - 1u))] = (uint32_t)t | (cull_any ? kMixed : 0u);
+    }
 }
 
 // Loads the lane's 4 points (xyz) -- vectorised when the group is complete.
@@ -187,91 +206,157 @@ __device__ __forceinline__ int load_points(const SceneArgs &s, int64_t base, flo
         return 4;
     }
     int cnt = 0;
+#pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (base + k < s.n) {
             P[3 * k] = __ldg(s.pos + 3 * (base + k));
             P[3 * k + 1] = __ldg(s.pos + 3 * (base + k) + 1);
             P[3 * k + 2] = __ldg(s.pos + 3 * (base + k) + 2);
             cnt = k + 1;
+        } else {
+            P[3 * k] = P[3 * k + 1] = P[3 * k + 2] = 0.0f;
         }
     }
     return cnt;
 }
 
 __device__ __forceinline__ void load_colors(const SceneArgs &s, int64_t base, int cnt,
-                                            uint8_t (&C)[12]) {
+                                            uint32_t (&W)[3]) {
     if (cnt == 4) {
         const uint32_t *c4 = reinterpret_cast<const uint32_t *>(s.col + 3 * base);
-        uint32_t w[3] = {__ldg(c4), __ldg(c4 + 1), __ldg(c4 + 2)};
-#pragma unroll
-        for (int b = 0; b < 12; ++b) C[b] = (uint8_t)(w[b >> 2] >> (8 * (b & 3)));
+        W[0] = __ldg(c4);
+        W[1] = __ldg(c4 + 1);
+        W[2] = __ldg(c4 + 2);
         return;
     }
-    for (int b = 0; b < 3 * cnt; ++b) C[b] = __ldg(s.col + 3 * base + b);
+    W[0] = W[1] = W[2] = 0u;
+    for (int b = 0; b < 3 * cnt; ++b) W[b >> 2] |= (uint32_t)__ldg(s.col + 3 * base + b) << (8 * (b & 3));
 }
 
-__global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
-                                                     const uint32_t *__restrict__ bits,
-                                                     unsigned long long *__restrict__ minz) {
+__device__ __forceinline__ uint32_t color_byte(const uint32_t (&W)[3], int b) {
+    return (W[b >> 2] >> (8 * (b & 3))) & 0xffu;
+}
+
+__device__ __forceinline__ void red_min_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Iterates the frame's tiles: the work list when culling, every tile otherwise.
+// The next tile's list entry and points are loaded before the current tile is
+// processed, so each warp always has two tiles of loads in flight.
+template <typename F>
+__device__ __forceinline__ void for_each_tile(const SceneArgs &s, const uint32_t *__restrict__ list,
+                                              const uint32_t *__restrict__ count, F &&body) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t tile = w0; tile < s.n_tiles; tile += nw) {
-        int status = 1, c0 = 0, c1 = 0;
-        if (bits) {
-            status = tile_status(s, bits, tile, lane, c0, c1);
-            if (status == 0) continue;
+    const int64_t n_items = list ? (int64_t)__ldg(count) : s.n_tiles;
+    int64_t i = w0;
+    if (i >= n_items) return;
+    uint32_t e = list ? __ldg(list + i) : (uint32_t)i;
+    float P[12];
+    int cnt = load_points(s, (int64_t)(e & ~kMixed) * LS_TILE_POINTS + 4 * lane, P);
+    for (;;) {
+        const int64_t inext = i + nw;
+        const bool more = inext < n_items;
+        uint32_t en = 0;
+        float Pn[12];
+        int cntn = 0;
+        if (more) {
+            en = list ? __ldg(list + inext) : (uint32_t)inext;
+            cntn = load_points(s, (int64_t)(en & ~kMixed) * LS_TILE_POINTS + 4 * lane, Pn);
         }
+        body(e, cnt, P);
+        if (!more) break;
+        i = inext;
+        e = en;
+        cnt = cntn;
+#pragma unroll
+        for (int q = 0; q < 12; ++q) P[q] = Pn[q];
+    }
+}
+
+template <bool PRECHECK>
+__global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
+                                                     const uint32_t *__restrict__ bits,
+                                                     const uint32_t *__restrict__ list,
+                                                     const uint32_t *__restrict__ count,
+                                                     unsigned long long *__restrict__ minz) {
+    const int lane = threadIdx.x & 31;
+    for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
+        const int64_t tile = e & ~kMixed;
         const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
-        float P[12];
-        const int cnt = load_points(s, base, P);
+        int c0 = 0, c1 = 0;
+        if (e & kMixed) {
+            c0 = __ldg(s.tile_c0 + tile);
+            c1 = __ldg(s.tile_c1 + tile);
+        }
+        int64_t pix[4];
+        unsigned long long key[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (k >= cnt) break;
-            if (status == 2 && !point_kept(s, bits, c0, c1, base + k)) continue;
             double zc;
-            int64_t pix = project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc);
-            if (pix < 0) continue;
-            unsigned long long key = (unsigned long long)__double_as_longlong(zc);
-            if (key < __ldcg(minz + pix)) atomicMin(minz + pix, key);
+            pix[k] = k < cnt ? project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc) : -1;
+            if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
+            key[k] = (unsigned long long)__double_as_longlong(zc);
         }
-    }
+        if (PRECHECK) {
+            unsigned long long cur[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldcg(minz + pix[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pix[k] >= 0) red_min_u64(minz + pix[k], key[k]);
+        }
+    });
 }
 
 __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
-                                                     const uint32_t *__restrict__ bits, double ope,
+                                                     const uint32_t *__restrict__ bits,
+                                                     const uint32_t *__restrict__ list,
+                                                     const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
                                                      unsigned long long *__restrict__ acc) {
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t tile = w0; tile < s.n_tiles; tile += nw) {
-        int status = 1, c0 = 0, c1 = 0;
-        if (bits) {
-            status = tile_status(s, bits, tile, lane, c0, c1);
-            if (status == 0) continue;
-        }
+    for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
+        const int64_t tile = e & ~kMixed;
         const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
-        float P[12];
-        uint8_t C[12];
-        const int cnt = load_points(s, base, P);
-        load_colors(s, base, cnt, C);
+        uint32_t W[3];
+        load_colors(s, base, cnt, W);
+        int c0 = 0, c1 = 0;
+        if (e & kMixed) {
+            c0 = __ldg(s.tile_c0 + tile);
+            c1 = __ldg(s.tile_c1 + tile);
+        }
+        int64_t pix[4];
+        double zc[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (k >= cnt) break;
-            if (status == 2 && !point_kept(s, bits, c0, c1, base + k)) continue;
-            double zc;
-            int64_t pix = project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc);
-            if (pix < 0) continue;
-            const double m = __longlong_as_double((long long)__ldcg(minz + pix));
-            if (!(zc <= dmul(m, ope))) continue;
-            const unsigned long long w_rg =
-                (unsigned long long)C[3 * k] | ((unsigned long long)C[3 * k + 1] << 32);
-            const unsigned long long w_bn = (unsigned long long)C[3 * k + 2] | (1ull << 32);
-            atomicAdd(acc + 2 * pix, w_rg);
-            atomicAdd(acc + 2 * pix + 1, w_bn);
+            pix[k] = k < cnt ? project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc[k]) : -1;
+            if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
         }
-    }
+        unsigned long long m[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldcg(minz + pix[k]) : 0ull;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (pix[k] < 0) continue;
+            if (!(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope))) continue;
+            const unsigned long long w_rg = (unsigned long long)color_byte(W, 3 * k) |
+                                            ((unsigned long long)color_byte(W, 3 * k + 1) << 32);
+            const unsigned long long w_bn = (unsigned long long)color_byte(W, 3 * k + 2) | (1ull << 32);
+            red_add_u64(acc + 2 * pix[k], w_rg);
+            red_add_u64(acc + 2 * pix[k] + 1, w_bn);
+        }
+    });
 }
 
 // Per-scan: occupied-cell span of every warp tile.
@@ -381,42 +466,85 @@ int ls_scene_tile_index(const int64_t *d_occ_offsets, int64_t n_occ, int64_t n_p
     return 0;
 }
 
-int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                   uint64_t *d_minz_bits, void *stream) {
-    if (!scene || !camera_ok(cam) || scene->n_points < 0) return LS_EINVAL;
-    if (d_keep_bits && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets))
-        return LS_EINVAL;
+static bool scene_ok(const ls_scene *scene, const uint32_t *d_list) {
+    if (!scene || scene->n_points < 0 || scene->n_points >= (int64_t(1) << 38)) return false;
+    if (d_list && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets)) return false;
+    return true;
+}
+
+static int g_precheck = -1;  // pass-1 read-before-atomic (LS_PASS1_PRECHECK=0/1, default 1)
+
+static bool use_precheck() {
+    if (g_precheck < 0) {
+        const char *e = getenv("LS_PASS1_PRECHECK");
+        g_precheck = (e && e[0] == '0') ? 0 : 1;
+    }
+    return g_precheck == 1;
+}
+
+int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
+                     uint32_t *d_count, void *stream) {
+    if (!scene_ok(scene, d_list) || !d_keep_bits || !d_list || !d_count) return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return (int)e;
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    k_frame_pass1<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-        a, make_cam(*cam), d_keep_bits, (unsigned long long *)d_minz_bits);
+    k_tile_list<<<grid_for(a.n_tiles, 256, 8), 256, 0, st>>>(a, d_keep_bits, d_list, d_count);
     LS_LAUNCH_CHECK();
     return 0;
 }
 
-int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                   double eps_rel, const uint64_t *d_minz_bits, uint64_t *d_accum2,
+int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
+                   const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
                    void *stream) {
-    if (!scene || !camera_ok(cam) || scene->n_points < 0) return LS_EINVAL;
-    if (d_keep_bits && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets))
+    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)))
+        return LS_EINVAL;
+    if (scene->n_points == 0) return 0;
+    SceneArgs a = scene_args(*scene);
+    a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    if (use_precheck())
+        k_frame_pass1<true><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
+            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits);
+    else
+        k_frame_pass1<false><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
+            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits);
+    LS_LAUNCH_CHECK();
+    return 0;
+}
+
+int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
+                   const uint32_t *d_count, const ls_camera *cam, double eps_rel,
+                   const uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
+    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)))
         return LS_EINVAL;
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
     const double ope = 1.0 + eps_rel;
     k_frame_pass2<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-        a, make_cam(*cam), d_keep_bits, ope, (const unsigned long long *)d_minz_bits,
-        (unsigned long long *)d_accum2);
+        a, make_cam(*cam), d_keep_bits, d_list, d_count, ope,
+        (const unsigned long long *)d_minz_bits, (unsigned long long *)d_accum2);
     LS_LAUNCH_CHECK();
     return 0;
 }
 
-int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, const ls_camera *cam,
-                     double eps_rel, uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
-    int rc = ls_frame_pass1(scene, d_keep_bits, cam, d_minz_bits, stream);
+int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
+                     uint32_t *d_count, const ls_camera *cam, double eps_rel,
+                     uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
+    int rc = 0;
+    if (d_keep_bits) {
+        rc = ls_tile_worklist(scene, d_keep_bits, d_list, d_count, stream);
+        if (rc) return rc;
+    } else {
+        d_list = nullptr;
+        d_count = nullptr;
+    }
+    rc = ls_frame_pass1(scene, d_keep_bits, d_list, d_count, cam, d_minz_bits, stream);
     if (rc) return rc;
-    return ls_frame_pass2(scene, d_keep_bits, cam, eps_rel, d_minz_bits, d_accum2, stream);
+    return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits,
+                          d_accum2, stream);
 }
 
 }  // extern "C"

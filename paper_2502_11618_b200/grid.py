@@ -55,6 +55,8 @@ class DeviceScene:
                                                self.n_points, self.tile_c0.data_ptr(),
                                                self.tile_c1.data_ptr(), st), "scene_tile_index")
         self.keep_bits = torch.empty(max((n_occ + 31) // 32, 1), dtype=torch.int32, device=dev)
+        self.tile_list = torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev)
+        self.tile_count = torch.zeros(1, dtype=torch.int32, device=dev)
         s = _lib.LsScene()
         s.d_positions, s.d_colors, s.n_points = (positions.data_ptr(), colors.data_ptr(),
                                                  self.n_points)
@@ -74,6 +76,14 @@ class DeviceScene:
         _lib.check(_lib.load().ls_cull(self.struct, pl.ctypes.data, CULL_SLACK, bits.data_ptr(),
                                        _lib.stream_ptr()), "cull")
         return bits
+
+    def worklist(self):
+        """Frame work list of non-culled tiles from the current keep bits."""
+        _lib.check(_lib.load().ls_tile_worklist(self.struct, self.keep_bits.data_ptr(),
+                                                self.tile_list.data_ptr(),
+                                                self.tile_count.data_ptr(), _lib.stream_ptr()),
+                   "tile_worklist")
+        return self.tile_list, self.tile_count
 
 
 class UniformGrid:

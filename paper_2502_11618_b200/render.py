@@ -124,17 +124,20 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
     st = _lib.stream_ptr()
     cam = _lib.make_camera(camera)
     ev = stage_events or [None] * 4
-    bits = None
+    bits = lst = cnt = None
     if cull:
         bits = scene.cull_bits(extract_frustum(camera).planes).data_ptr()
+        tl, tc = scene.worklist()
+        lst, cnt = tl.data_ptr(), tc.data_ptr()
     if ev[0] is not None:
         ev[0].record()
-    _lib.check(lib.ls_frame_pass1(scene.struct, bits, cam, bufs.minz.data_ptr(), st),
+    _lib.check(lib.ls_frame_pass1(scene.struct, bits, lst, cnt, cam, bufs.minz.data_ptr(), st),
                "frame_pass1")
     if ev[1] is not None:
         ev[1].record()
-    _lib.check(lib.ls_frame_pass2(scene.struct, bits, cam, float(eps_rel), bufs.minz.data_ptr(),
-                                  bufs.accum.data_ptr(), st), "frame_pass2")
+    _lib.check(lib.ls_frame_pass2(scene.struct, bits, lst, cnt, cam, float(eps_rel),
+                                  bufs.minz.data_ptr(), bufs.accum.data_ptr(), st),
+               "frame_pass2")
     if ev[2] is not None:
         ev[2].record()
     fp = None if filter_params is None else _lib.make_filter(filter_params)
