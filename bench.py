@@ -23,6 +23,7 @@ restatement of the reference host code, on this box's host cores.
 from __future__ import annotations
 
 import argparse
+import faulthandler
 import json
 import os
 import statistics
@@ -78,13 +79,20 @@ class ClockSampler:
         self.error = None
 
     def _handle(self, nv):
+        """NVML handle of the CUDA device (matched by UUID; index fallback)."""
         try:
             import torch
 
-            bus = torch.cuda.get_device_properties(self.cuda_index).pci_bus_id
-            return nv.nvmlDeviceGetHandleByPciBusId(bus)
-        except Exception:
-            return nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
+            want = str(torch.cuda.get_device_properties(self.cuda_index).uuid)
+            for i in range(nv.nvmlDeviceGetCount()):
+                h = nv.nvmlDeviceGetHandleByIndex(i)
+                uuid = nv.nvmlDeviceGetUUID(h)
+                uuid = uuid.decode() if isinstance(uuid, bytes) else uuid
+                if want in uuid:
+                    return h
+        except Exception:  # noqa: BLE001
+            pass
+        return nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
 
     def start(self):
         try:
@@ -346,6 +354,7 @@ def run_b200(args):
 
 
 def main():
+    faulthandler.enable()
     args = parse()
     if args.impl == "reference":
         return run_reference(args)

@@ -174,36 +174,81 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     const int64_t by = blockIdx.y, bx = blockIdx.x;
     float m = INFINITY;
     bool overflow = false;
+    const int64_t x = bx * 32 + 2 * gx;
+    // Issue every load of the thread's 2x2 pixels before any use (4 independent
+    // 16 B minz/accum pairs in flight), then compute, then vector stores.
+    unsigned long long key[2][2], wrg[2][2], wbn[2][2];
+    bool ok[2][2];
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
         const int64_t y = by * 32 + 2 * gy + dy;
+        const int64_t p = y * W + x;
+        ok[dy][0] = y < H && x < W;
+        ok[dy][1] = y < H && x + 1 < W;
+        if (ok[dy][1] && (W & 1) == 0) {
+            const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2 *>(minz + p));
+            const ulonglong4 a4 = *reinterpret_cast<const ulonglong4 *>(acc + 2 * p);
+            key[dy][0] = k2.x; key[dy][1] = k2.y;
+            wrg[dy][0] = a4.x; wbn[dy][0] = a4.y; wrg[dy][1] = a4.z; wbn[dy][1] = a4.w;
+        } else {
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                key[dy][dx] = ok[dy][dx] ? minz[p + dx] : kInfBits;
+                wrg[dy][dx] = ok[dy][dx] ? acc[2 * (p + dx)] : 0ull;
+                wbn[dy][dx] = ok[dy][dx] ? acc[2 * (p + dx) + 1] : 0ull;
+            }
+        }
+    }
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+        const int64_t y = by * 32 + 2 * gy + dy;
+        const int64_t p = y * W + x;
+        float c[2][3], d[2];
+        uint8_t al[2];
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
-            const int64_t x = bx * 32 + 2 * gx + dx;
-            if (y >= H || x >= W) continue;
-            const int64_t p = y * W + x;
-            const unsigned long long key = minz[p];
-            const unsigned long long w_rg = acc[2 * p], w_bn = acc[2 * p + 1];
-            minz[p] = kInfBits;
-            acc[2 * p] = 0ull;
-            acc[2 * p + 1] = 0ull;
-            const unsigned long long cnt = w_bn >> 32;
-            float d = 0.0f;
+            const unsigned long long cnt = wbn[dy][dx] >> 32;
+            d[dx] = 0.0f;
+            c[dx][0] = c[dx][1] = c[dx][2] = 0.0f;
+            al[dx] = 0;
             if (cnt > 0) {
                 overflow |= cnt > LS_PACKED_COUNT_LIMIT;
                 const double denom = dmul((double)cnt, 255.0);
-                rgb[3 * p + 0] = __double2float_rn(ddiv((double)(w_rg & 0xffffffffull), denom));
-                rgb[3 * p + 1] = __double2float_rn(ddiv((double)(w_rg >> 32), denom));
-                rgb[3 * p + 2] = __double2float_rn(ddiv((double)(w_bn & 0xffffffffull), denom));
-                d = __double2float_rn(__longlong_as_double((long long)key));
-                alpha[p] = 1;
-            } else {
-                rgb[3 * p + 0] = rgb[3 * p + 1] = rgb[3 * p + 2] = 0.0f;
-                alpha[p] = 0;
+                c[dx][0] = __double2float_rn(ddiv((double)(wrg[dy][dx] & 0xffffffffull), denom));
+                c[dx][1] = __double2float_rn(ddiv((double)(wrg[dy][dx] >> 32), denom));
+                c[dx][2] = __double2float_rn(ddiv((double)(wbn[dy][dx] & 0xffffffffull), denom));
+                d[dx] = __double2float_rn(__longlong_as_double((long long)key[dy][dx]));
+                al[dx] = 1;
             }
-            depth[p] = d;
-            const float sv = sentinel(d);
-            m = sv < m ? sv : m;
+            if (ok[dy][dx]) {
+                const float sv = sentinel(d[dx]);
+                m = sv < m ? sv : m;
+            }
+        }
+        if (ok[dy][1] && (W & 1) == 0) {
+            float2 *r2 = reinterpret_cast<float2 *>(rgb + 3 * p);
+            r2[0] = make_float2(c[0][0], c[0][1]);
+            r2[1] = make_float2(c[0][2], c[1][0]);
+            r2[2] = make_float2(c[1][1], c[1][2]);
+            *reinterpret_cast<float2 *>(depth + p) = make_float2(d[0], d[1]);
+            *reinterpret_cast<uchar2 *>(alpha + p) = make_uchar2(al[0], al[1]);
+            // consume-and-reset for the next frame
+            *reinterpret_cast<ulonglong2 *>(minz + p) = make_ulonglong2(kInfBits, kInfBits);
+            *reinterpret_cast<ulonglong4 *>(acc + 2 * p) = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+        } else {
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                if (!ok[dy][dx]) continue;
+                const int64_t q = p + dx;
+                rgb[3 * q] = c[dx][0];
+                rgb[3 * q + 1] = c[dx][1];
+                rgb[3 * q + 2] = c[dx][2];
+                depth[q] = d[dx];
+                alpha[q] = al[dx];
+                minz[q] = kInfBits;
+                acc[2 * q] = 0ull;
+                acc[2 * q + 1] = 0ull;
+            }
         }
     }
     if (overflow) atomicOr(flags, 1);

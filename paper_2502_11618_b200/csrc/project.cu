@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
         if (PRECHECK) {
             unsigned long long cur[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldcg(minz + pix[k]) : 0ull;
+            for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldca(minz + pix[k]) : 0ull;  // stale L1 is safe: min only decreases
 #pragma unroll
             for (int k = 0; k < 4; ++k)
                 if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
         }
         unsigned long long m[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldcg(minz + pix[k]) : 0ull;
+        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;  // read-only in pass 2
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (pix[k] < 0) continue;

@@ -1,0 +1,35 @@
+"""Run a few pipeline frames for ncu captures (no timing printed here).
+
+    python scripts/profile_frame.py [--points N] [--frames F] [--unet none|default]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+from paper_2502_11618_b200 import PointCloud, build_grid
+from paper_2502_11618_b200.engine import FrameRenderer
+from paper_2502_11618_b200.scenes import hall_cameras, multi_station_hall
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--points", type=int, default=20_000_000)
+ap.add_argument("--frames", type=int, default=3)
+ap.add_argument("--unet", default="none")
+a = ap.parse_args()
+pos, col, _ = multi_station_hall(a.points)
+grid = build_grid(PointCloud(pos, col), 1.0)
+unet = None
+if a.unet != "none":
+    from paper_2502_11618_b200.unet import UNet
+
+    unet = UNet.from_config(a.unet, seed=7, device=torch.device("cuda"))
+cams = hall_cameras(8)
+r = FrameRenderer(grid, 1920, 1080, unet=unet)
+for i in range(a.frames):
+    r.enqueue(cams[i % len(cams)])
+torch.cuda.synchronize()
+r.check_flags()
+print("done")
