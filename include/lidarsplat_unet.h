@@ -1,0 +1,74 @@
+/*
+ * lidarsplat_unet.h -- C ABI of the U-Net reconstruction stage on sm_100a
+ * tensor cores (tcgen05.mma + TMEM accumulators, TMA-fed implicit GEMM).
+ *
+ * Replaces the bridge's neural model (reference FE:src/bridge.ts:31-53 ->
+ * FE:src/model/tfjsExec.ts:121-134 TfjsUNet.forward, graph of
+ * FE:src/model/unet.ts:148-184).  Activations are bf16 NHWC, accumulation f32.
+ * Same conventions as lidarsplat_cuda.h (caller-owned device memory, async on
+ * `stream`, 0 / LS_EINVAL / cudaError_t).
+ */
+#ifndef LIDARSPLAT_UNET_H
+#define LIDARSPLAT_UNET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Activations of the fused epilogue. */
+#define LS_ACT_NONE 0
+#define LS_ACT_RELU 1
+#define LS_ACT_LEAKY 2
+
+/* A pre-planned convolution layer: tensor maps encoded once, launched per
+ * frame with no host work beyond the launch. */
+typedef struct ls_conv_plan ls_conv_plan;
+
+/* Plan one convolution (grad64.ts:65-141 conv2d "same", or 146-201
+ * convTranspose2x2 when transposed != 0):
+ *
+ *   conv      y[n,y,x,o] = act(scale[o] * sum_{ky,kx,c} X[n,y+ky-1,x+kx-1,c] W[o][ky*3+kx][c]
+ *                              + shift[o])                (ksize 3; ksize 1 = no shift)
+ *   transposed y[n,2i+dy,2j+dx,o] = act(scale[q] * sum_c X[n,i,j,c] W[q][c] + shift[q]),
+ *              q = (dy*2+dx)*cout + o                     (scale/shift have 4*cout entries)
+ *
+ * X is the channel concatenation [x0 (c0 ch), x1 (c1 ch)] (unet.ts:179 concat
+ * order [up, skip]); x1 may be NULL with c1 = 0.  W is bf16, K-major:
+ * [n][taps][c0+c1] with n = output column (cout, or 4*cout transposed).
+ * Outputs (any subset, NULL = skip):
+ *   y       bf16 NHWC (batch, H', W', cout)
+ *   y_f32   f32  NHWC
+ *   pool    bf16 NHWC 2x2 max pool of y (maxPool2, grad64.ts:203-238)
+ *   head    f32 NHWC (batch,H,W,head_c) = sigmoid(head_w[head_c][cout] . y + head_b)
+ *           (the final 1x1 conv + sigmoid, unet.ts:183), head_c <= 4
+ * Requirements: c0, c1 in {16, 32} or multiples of 64; cout multiple of 16;
+ * columns (cout or 4*cout) <= 4096; h, w even when pooling.
+ * *status receives 0 or LS_EINVAL / a CUDA error; returns NULL on failure. */
+ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1,
+                                  int32_t c1, int32_t batch, int32_t h, int32_t w,
+                                  const uint16_t *d_w, int32_t ksize, int32_t cout,
+                                  int32_t transposed, const float *d_scale, const float *d_shift,
+                                  int32_t act, float alpha, uint16_t *d_y, float *d_y_f32,
+                                  uint16_t *d_pool, const float *d_head_w, const float *d_head_b,
+                                  int32_t head_c, float *d_head_out, int32_t *status);
+int ls_conv_plan_launch(const ls_conv_plan *plan, void *stream);
+void ls_conv_plan_destroy(ls_conv_plan *plan);
+
+/* One-shot convenience: plan, launch, destroy. */
+int ls_conv2d(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1, int32_t c1, int32_t batch,
+              int32_t h, int32_t w, const uint16_t *d_w, int32_t ksize, int32_t cout,
+              const float *d_scale, const float *d_shift, int32_t act, float alpha,
+              uint16_t *d_y, float *d_y_f32, uint16_t *d_pool, const float *d_head_w,
+              const float *d_head_b, int32_t head_c, float *d_head_out, void *stream);
+
+int ls_conv_transpose2x2(const uint16_t *d_x, int32_t cin, int32_t batch, int32_t h, int32_t w,
+                         const uint16_t *d_w, int32_t cout, const float *d_scale,
+                         const float *d_shift, uint16_t *d_y, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIDARSPLAT_UNET_H */

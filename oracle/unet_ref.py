@@ -1,0 +1,137 @@
+"""CPU restatement of the reference U-Net -- TEST INFRASTRUCTURE ONLY.
+
+Follows the reference's float64 engine op by op (FE = /root/reference/pkg/frontend/src):
+  conv2d             FE:model/grad64.ts:65-141   NHWC, kernel [kh,kw,ci,co], zero "same" pad
+  convTranspose2x2   FE:model/grad64.ts:146-201  kernel [2,2,co,ci], y[2i+dy,2j+dx,o] = b + sum_c x W
+  maxPool2           FE:model/grad64.ts:203-238
+  batchNorm (infer)  FE:model/grad64.ts:250-313  eps 1e-3 (:247)
+  relu / leakyRelu / sigmoid  FE:model/grad64.ts:315-354
+  concatC            FE:model/grad64.ts:357-379  [up, skip]
+  graph              FE:model/unet.ts:148-184
+  input prep         FE:model/weights.ts:90-95 normalizeDepth + FE:bridge.ts:31-53 NHWC pack
+
+Runs in torch on the CPU (float64 = the reference engine, float32 = the tfjs
+executor's precision).  U-Net parity is UNPINNED: the reference executors
+need node + @tensorflow/tfjs (not installed), so there are no golden vectors;
+correctness rests on this restatement plus the reference's relative
+properties (shape, [0,1] range, translation covariance, FE:tests/unet.test.ts).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+BN_EPSILON = 1e-3
+DECODER_LEAK = 0.1
+
+
+def _t(a, dtype):
+    import torch
+
+    return torch.as_tensor(np.asarray(a), dtype=dtype)
+
+
+def conv2d(x, k, b):
+    """x NHWC, k [kh,kw,ci,co] -> NHWC (zero 'same' padding for odd k)."""
+    import torch.nn.functional as F
+
+    w = k.permute(3, 2, 0, 1)  # [co, ci, kh, kw]
+    y = F.conv2d(x.permute(0, 3, 1, 2), w, b, padding=k.shape[0] // 2)
+    return y.permute(0, 2, 3, 1)
+
+
+def conv_transpose2x2(x, k, b):
+    """k [2,2,co,ci] -> torch weight [ci, co, 2, 2]."""
+    import torch.nn.functional as F
+
+    w = k.permute(3, 2, 0, 1)
+    y = F.conv_transpose2d(x.permute(0, 3, 1, 2), w, b, stride=2)
+    return y.permute(0, 2, 3, 1)
+
+
+def max_pool2(x):
+    import torch.nn.functional as F
+
+    return F.max_pool2d(x.permute(0, 3, 1, 2), 2).permute(0, 2, 3, 1)
+
+
+def batch_norm(x, p, name):
+    inv = 1.0 / (p[name + ".moving_var"] + BN_EPSILON).sqrt()
+    return (x - p[name + ".moving_mean"]) * inv * p[name + ".gamma"] + p[name + ".beta"]
+
+
+def forward(cfg, params, x, dtype=None, collect=None):
+    """x: (B,H,W,inChannels) NHWC -> (B,H,W,outChannels) in [0,1].
+    ``collect`` (dict) receives intermediate tensors by layer name."""
+    import torch
+
+    dtype = dtype or torch.float64
+    p = {k: _t(v, dtype) for k, v in params.items()}
+    x = _t(x, dtype)
+    h, w = x.shape[1], x.shape[2]
+    div = 2 ** cfg.depth
+    if h % div or w % div:
+        raise ValueError(f"input {w}x{h} not divisible by 2^depth = {div}")
+
+    def keep(name, t):
+        if collect is not None:
+            collect[name] = t
+        return t
+
+    relu = torch.relu
+    skips = []
+    cur = x
+    for s in range(cfg.depth):
+        cur = keep(f"enc{s}_1", relu(batch_norm(conv2d(cur, p[f"enc{s}_conv1.kernel"],
+                                                       p[f"enc{s}_conv1.bias"]), p, f"enc{s}_bn1")))
+        cur = keep(f"enc{s}_2", relu(batch_norm(conv2d(cur, p[f"enc{s}_conv2.kernel"],
+                                                       p[f"enc{s}_conv2.bias"]), p, f"enc{s}_bn2")))
+        skips.append(cur)
+        cur = max_pool2(cur)
+    cur = keep("bott_1", relu(batch_norm(conv2d(cur, p["bott_conv1.kernel"], p["bott_conv1.bias"]),
+                                         p, "bott_bn1")))
+    cur = keep("bott_2", relu(batch_norm(conv2d(cur, p["bott_conv2.kernel"], p["bott_conv2.bias"]),
+                                         p, "bott_bn2")))
+    leaky = lambda t: torch.where(t > 0, t, DECODER_LEAK * t)  # noqa: E731
+    for s in range(cfg.depth - 1, -1, -1):
+        cur = keep(f"dec{s}_up", conv_transpose2x2(cur, p[f"dec{s}_up.kernel"], p[f"dec{s}_up.bias"]))
+        cur = torch.cat([cur, skips[s]], dim=-1)
+        cur = keep(f"dec{s}_1", leaky(conv2d(cur, p[f"dec{s}_conv1.kernel"], p[f"dec{s}_conv1.bias"])))
+        cur = keep(f"dec{s}_2", leaky(conv2d(cur, p[f"dec{s}_conv2.kernel"], p[f"dec{s}_conv2.bias"])))
+    return torch.sigmoid(conv2d(cur, p["final_conv.kernel"], p["final_conv.bias"]))
+
+
+def pack_input(rgb, depth, alpha, z_near=0.1, pad_rows_to=16):
+    """bridge.ts:31-53 + weights.ts:90-95: NHWC [r,g,b,d',a], d' = zNear/max(d,zNear)
+    in f64 stored as f32; zero rows appended to a multiple of 2^depth."""
+    h, w = depth.shape
+    dn = np.where(depth > 0, (z_near / np.maximum(depth.astype(np.float64), z_near)), 0.0)
+    x = np.concatenate([rgb.astype(np.float32), dn.astype(np.float32)[..., None],
+                        alpha.astype(np.float32)[..., None]], axis=-1)
+    hp = (h + pad_rows_to - 1) // pad_rows_to * pad_rows_to
+    out = np.zeros((1, hp, w, 5), np.float32)
+    out[0, :h] = x
+    return out
+
+
+class CpuUNet:
+    """The CPU U-Net leg of the reference arm: f32 torch (tfjs precision) on
+    all host threads, same random-init weights as the device network."""
+
+    def __init__(self, name="default", threads=None, seed=7):
+        import torch
+
+        from paper_2502_11618_b200.unet import DEFAULT_CONFIG, REDUCED_CONFIG, init_params
+
+        if threads:
+            torch.set_num_threads(threads)
+        self.cfg = {"default": DEFAULT_CONFIG, "reduced": REDUCED_CONFIG}[name]
+        self.params = init_params(self.cfg, seed)
+
+    def reconstruct(self, rgb, depth, alpha):
+        import torch
+
+        x = pack_input(rgb, depth, alpha, self.cfg.depthZNear, 2 ** self.cfg.depth)
+        with torch.no_grad():
+            y = forward(self.cfg, self.params, x, dtype=torch.float32)
+        return y[0, : depth.shape[0]].numpy()

@@ -99,6 +99,16 @@ SIGNATURES = {
     "ls_depth_filter_frame": (ctypes.c_int, [_P, _P, _P, _I64, _I64,
                                              ctypes.POINTER(LsFilterParams), _P, _P, _P, _P, _P,
                                              _P]),
+    # lidarsplat_unet.h
+    "ls_conv_plan_create": (ctypes.c_void_p, [_P, _I32, _P, _I32, _I32, _I32, _I32, _P, _I32,
+                                              _I32, _I32, _P, _P, _I32, _F, _P, _P, _P, _P, _P,
+                                              _I32, _P, ctypes.POINTER(ctypes.c_int32)]),
+    "ls_conv_plan_launch": (ctypes.c_int, [_P, _P]),
+    "ls_conv_plan_destroy": (None, [_P]),
+    "ls_conv2d": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _P,
+                                 _I32, _F, _P, _P, _P, _P, _P, _I32, _P, _P]),
+    "ls_conv_transpose2x2": (ctypes.c_int, [_P, _I32, _I32, _I32, _I32, _P, _I32, _P, _P, _P,
+                                            _P]),
 }
 
 _lock = threading.Lock()

@@ -34,6 +34,7 @@ SOURCES = [
     ("filter.cu", EXACT),
     ("cull.cu", EXACT),
     ("grid.cu", EXACT),
+    ("unet.cu", []),
 ]
 HEADERS = ["ls_common.cuh", "umma.cuh"]
 
