@@ -25,10 +25,12 @@ BN_EPSILON = 1e-3
 DECODER_LEAK = 0.1
 
 
-def _t(a, dtype):
+def _t(a, dtype, device=None):
     import torch
 
-    return torch.as_tensor(np.asarray(a), dtype=dtype)
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device or a.device, dtype=dtype)
+    return torch.as_tensor(np.asarray(a), dtype=dtype, device=device)
 
 
 def conv2d(x, k, b):
@@ -60,14 +62,16 @@ def batch_norm(x, p, name):
     return (x - p[name + ".moving_mean"]) * inv * p[name + ".gamma"] + p[name + ".beta"]
 
 
-def forward(cfg, params, x, dtype=None, collect=None):
+def forward(cfg, params, x, dtype=None, collect=None, device=None):
     """x: (B,H,W,inChannels) NHWC -> (B,H,W,outChannels) in [0,1].
-    ``collect`` (dict) receives intermediate tensors by layer name."""
+    ``collect`` (dict) receives intermediate tensors by layer name.  ``device``
+    lets the same restatement run as a plain-PyTorch GPU forward (used only to
+    measure the bf16 error floor)."""
     import torch
 
     dtype = dtype or torch.float64
-    p = {k: _t(v, dtype) for k, v in params.items()}
-    x = _t(x, dtype)
+    p = {k: _t(v, dtype, device) for k, v in params.items()}
+    x = _t(x, dtype, device)
     h, w = x.shape[1], x.shape[2]
     div = 2 ** cfg.depth
     if h % div or w % div:
