@@ -120,8 +120,8 @@ def test_divisibility_rejected():
     from paper_2502_11618_b200.unet import UNet
 
     net = UNet.from_config("reduced", seed=1)
-    xin = torch.zeros((1, 100, 100, 16), dtype=torch.bfloat16, device="cuda")
-    out = torch.empty((1, 100, 100, 3), dtype=torch.float32, device="cuda")
+    xin = torch.zeros((1, 102, 100, 16), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty((1, 102, 100, 3), dtype=torch.float32, device="cuda")
     with pytest.raises(ValueError, match="divisible"):
         net.forward(xin, out)
 
