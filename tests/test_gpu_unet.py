@@ -160,3 +160,35 @@ def test_weights_file_roundtrip(tmp_path):
     a = _run_device(UNet(cfg, q), x)
     b = _run_device(UNet.from_weights(path), x)
     assert np.array_equal(a, b)
+
+
+def test_full_frame_with_unet_vs_oracle(port):
+    """FrameRenderer (cull -> project -> filter -> pack -> U-Net on device)
+    vs the CPU oracle pipeline + f64 U-Net restatement, 320x256 frame."""
+    import torch
+
+    from oracle import oracle as O
+    from oracle.unet_ref import forward, pack_input
+    from paper_2502_11618_b200 import CameraModel, PointCloud, RigidTransform, build_grid
+    from paper_2502_11618_b200.engine import FrameRenderer
+    from paper_2502_11618_b200.unet import UNet
+
+    rng = np.random.default_rng(17)
+    n = 300_000
+    pos = rng.random((n, 3)) * np.array([8.0, 6.0, 3.0]) + np.array([-4.0, -3.0, 4.0])
+    cloud = PointCloud(pos.astype(np.float32), rng.integers(0, 256, (n, 3), dtype=np.uint8))
+    cam = CameraModel(fx=300.0, fy=300.0, cx=160.0, cy=120.0, width=320, height=240,
+                      world_to_camera=RigidTransform.identity())
+    net = UNet.from_config("default", seed=3)
+    r = FrameRenderer(build_grid(cloud, 1.0), 320, 240, unet=net)
+    got = r.render(cam)
+    r.check_flags()
+    og = O.OracleGrid(cloud.positions, cloud.colors, 1.0, port)
+    rgb, depth, alpha, _ = O.render_frame(og, cam, 0.01, 4, 0.1, 0.25, port, port)
+    # the device path's filtered frame is bit-exact; the U-Net within tolerance
+    assert np.array_equal(r.frgb.cpu().numpy(), rgb)
+    ref = forward(net.cfg, net.params, pack_input(rgb, depth, alpha, 0.1, 16)).numpy()[0, :240]
+    assert got.shape == (240, 320, 3)
+    err = float(np.abs(got - ref).max())
+    print(f"frame+unet max-abs {err:.3e} PSNR {_psnr(got, ref):.1f} dB")
+    assert err <= 1.5e-2 and _psnr(got, ref) >= 40.0
