@@ -30,14 +30,16 @@ typedef struct ls_conv_plan ls_conv_plan;
 /* Plan one convolution (grad64.ts:65-141 conv2d "same", or 146-201
  * convTranspose2x2 when transposed != 0):
  *
- *   conv      y[n,y,x,o] = act(scale[o] * sum_{ky,kx,c} X[n,y+ky-1,x+kx-1,c] W[o][ky*3+kx][c]
+ *   conv      y[n,y,x,o] = act(scale[o] * sum_{ky,kx,c} X[n,y+ky-1,x+kx-1,c] W[kx*3+ky][o][c]
  *                              + shift[o])                (ksize 3; ksize 1 = no shift)
- *   transposed y[n,2i+dy,2j+dx,o] = act(scale[q] * sum_c X[n,i,j,c] W[q][c] + shift[q]),
+ *   transposed y[n,2i+dy,2j+dx,o] = act(scale[q] * sum_c X[n,i,j,c] W[0][q][c] + shift[q]),
  *              q = (dy*2+dx)*cout + o                     (scale/shift have 4*cout entries)
  *
  * X is the channel concatenation [x0 (c0 ch), x1 (c1 ch)] (unet.ts:179 concat
- * order [up, skip]); x1 may be NULL with c1 = 0.  W is bf16, K-major:
- * [n][taps][c0+c1] with n = output column (cout, or 4*cout transposed).
+ * order [up, skip]); x1 may be NULL with c1 = 0.  W is bf16, tap-major then
+ * K-major: [tap][n][c0+c1], tap = kx*3+ky (kx-major, so one weight box per kx
+ * covers the three ky taps that share an input box), n = output column
+ * (cout, or 4*cout transposed).
  * Outputs (any subset, NULL = skip):
  *   y       bf16 NHWC (batch, H', W', cout)
  *   y_f32   f32  NHWC

@@ -300,11 +300,12 @@ class UNet:
             co = k.shape[3]
             co_p = _pad16(co)
             ci_p = sum(_pad16(c) for c in srcs)
-            wd = np.zeros((co_p, 9, ci_p))
+            # device layout [tap = kx*3+ky][co_p][ci_p] (lidarsplat_unet.h)
+            wd = np.zeros((9, co_p, ci_p))
             off_r, off_p = 0, 0
             for c in srcs:
-                blk = k[:, :, off_r:off_r + c, :]  # [3,3,c,co]
-                wd[:co, :, off_p:off_p + c] = blk.reshape(9, c, co).transpose(2, 0, 1)
+                blk = k[:, :, off_r:off_r + c, :]  # [ky,kx,c,co]
+                wd[:, :co, off_p:off_p + c] = blk.transpose(1, 0, 3, 2).reshape(9, co, c)
                 off_r += c
                 off_p += _pad16(c)
             scale = np.zeros(co_p)
@@ -317,7 +318,7 @@ class UNet:
             else:
                 scale[:co] = 1.0
                 shift[:co] = b
-            layers[name] = dict(w=bf16(wd.reshape(co_p, 9 * ci_p)), scale=f32(scale),
+            layers[name] = dict(w=bf16(wd), scale=f32(scale),
                                 shift=f32(shift), cout=co_p)
 
         def up(name):

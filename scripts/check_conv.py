@@ -24,8 +24,9 @@ def conv_case(c0, c1, cout, h, w, act, pool=False, head=False, batch=1, seed=0):
     hw = (torch.randn(3, cout, generator=g) * 0.2).to(dev) if head else None
     hb = (torch.randn(3, generator=g) * 0.1).to(dev) if head else None
     ho = torch.empty(batch, h, w, 3, dtype=torch.float32, device=dev) if head else None
+    wdev = wt.reshape(cout, 3, 3, cin).permute(2, 1, 0, 3).contiguous()  # [kx][ky][o][c]
     rc = lib.ls_conv2d(x0.data_ptr(), c0, None if x1 is None else x1.data_ptr(), c1, batch, h, w,
-                       wt.data_ptr(), 3, cout, scale.data_ptr(), shift.data_ptr(), act, 0.1,
+                       wdev.data_ptr(), 3, cout, scale.data_ptr(), shift.data_ptr(), act, 0.1,
                        y.data_ptr(), yf.data_ptr(), _lib.ptr(pl), _lib.ptr(hw), _lib.ptr(hb),
                        3 if head else 0, _lib.ptr(ho), 0)
     torch.cuda.synchronize()
