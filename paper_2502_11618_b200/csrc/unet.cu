@@ -35,10 +35,11 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-// ====================================================================== v2 ==
-// Persistent, warp-specialised variant (the production path):
-//   * 192 threads: warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue;
-//     one CTA per SM loops over (pixel tile, column tile) work items.
+// ============================================================ conv kernel ==
+// Persistent, warp-specialised implicit-GEMM convolution:
+//   * 320 threads: warp 0 TMA producer, warp 1 MMA issuer, warps 2-9 epilogue
+//     (two warps per TMEM lane quarter, splitting the column groups); one CTA
+//     per SM loops over (pixel tile, column tile) work items.
 //   * TMEM holds TWO accumulators (2 x BN columns): the epilogue drains tile i
 //     while the MMA warp already accumulates tile i+1.
 //   * Halo reuse: the pixel tile is 8 rows x 16 columns (m = row*16 + col) and
@@ -49,18 +50,23 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 //   * Weights of small layers (<= kResidentMax bytes, one column tile) are
 //     loaded into shared memory ONCE per CTA and stay resident; otherwise a
 //     (kys x BN x chunk) weight box streams with every A box.
-//   Weight layout for v2: [tap][n][c] with tap = kx*kys + ky (kx-major).
-constexpr int kThreadsP = 192;
+//   * Epilogue constants (folded-BN scale/shift, head weights) are staged in
+//     shared memory once per CTA.
+//   Weight layout: [tap][n][c] with tap = kx*kys + ky (kx-major).
+constexpr int kEpiWarps = 8;
+constexpr int kThreadsP = 64 + 32 * kEpiWarps;
 constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
-constexpr size_t kSmemBudget = 225 * 1024;
+constexpr size_t kSmemBudget = 222 * 1024;
+
+enum EpiMode { kPlain = 0, kPool = 1, kHead = 2, kTransposed = 3 };
 
 struct ConvParamsP {
     int batch, h, w;
     int tiles_x, tiles_y, n_tiles_m, n_tiles_n, n_items;
     int c0, c1, ctot, nq0, nq;
     int kxs, kys, pad;
-    int n_total, cout, transposed, act;
+    int n_total, cout, act;
     float alpha;
     const float *scale, *shift;
     __nv_bfloat16 *y;
@@ -74,9 +80,10 @@ struct ConvParamsP {
     uint32_t a_bytes;      // A stage footprint (1024-aligned)
     uint32_t a_tx;         // TMA bytes of one A box
     uint32_t b_blk;        // bytes of one (kys x BN x chunk) weight block
-    uint32_t off_b;        // resident weights offset
-    uint32_t off_pool;     // pool staging offset
-    uint32_t off_bar;      // barriers offset
+    uint32_t off_b;        // resident weights
+    uint32_t off_const;    // scale[n_total], shift[n_total], head_w, head_b (f32)
+    uint32_t off_pool;     // pool / head staging
+    uint32_t off_bar;      // barriers
 };
 
 template <int BN, int CHUNK>
@@ -85,21 +92,49 @@ struct CfgP {
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
     static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int kGroups = BN / 16;
 };
 
-template <int BN, int CHUNK>
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint32_t hmax4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162 *>(&a);
+    __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162 *>(&b);
+    __nv_bfloat162 z = *reinterpret_cast<__nv_bfloat162 *>(&c);
+    __nv_bfloat162 w = *reinterpret_cast<__nv_bfloat162 *>(&d);
+    __nv_bfloat162 m = __hmax2(__hmax2(x, y), __hmax2(z, w));
+    return *reinterpret_cast<uint32_t *>(&m);
+}
+
+template <int BN, int CHUNK, int MODE>
 __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__ CUtensorMap mA0,
                                                          const __grid_constant__ CUtensorMap mA1,
                                                          const __grid_constant__ CUtensorMap mB,
                                                          const ConvParamsP p) {
     using C = CfgP<BN, CHUNK>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-align inside the shared window (keeps the shared address space visible)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
     const int S = p.stages;
     const uint32_t stage_bytes = p.a_bytes + (p.resident ? 0u : p.b_blk);
-    uint8_t *sB_res = smem + p.off_b;
-    __nv_bfloat16 *spool = reinterpret_cast<__nv_bfloat16 *>(smem + p.off_pool);
+    float *sconst = reinterpret_cast<float *>(smem + p.off_const);
+    const float *s_scale = sconst;
+    const float *s_shift = sconst + p.n_total;
+    const float *s_hw = sconst + 2 * p.n_total;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
@@ -116,7 +151,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
             }
             for (int a = 0; a < 2; ++a) {
                 mbar_init(tfull + a, 1);
-                mbar_init(tempty + a, 4);
+                mbar_init(tempty + a, kEpiWarps);
             }
             mbar_init(bres, 1);
             fence_barrier_init();
@@ -126,29 +161,39 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
         }
         __syncwarp();
         tmem_alloc(tslot, C::kTmemCols);
+    } else if (warp >= 2) {
+        // stage the epilogue constants (visible after the __syncthreads below)
+        const int t = threadIdx.x - 64;
+        for (int i = t; i < p.n_total; i += 32 * kEpiWarps) {
+            sconst[i] = p.scale[i];
+            sconst[p.n_total + i] = p.shift[i];
+        }
+        if (MODE == kHead)
+            for (int i = t; i < p.head_c * p.cout; i += 32 * kEpiWarps)
+                sconst[2 * p.n_total + i] = p.head_w[i];
     }
     fence_before_sync();
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tslot;
-    const int nk = p.kxs * p.nq;  // K stages per work item
 
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (p.resident) {
-                mbar_expect_tx(bres, (uint32_t)nk * p.b_blk);
+                mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk);
                 for (int kx = 0; kx < p.kxs; ++kx)
                     for (int q = 0; q < p.nq; ++q) {
                         const bool second = q >= p.nq0;
-                        const int kc = (second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK);
-                        tma_load_3d(sB_res + (kx * p.nq + q) * p.b_blk, &mB, kc, 0, kx * p.kys, bres);
+                        const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
+                        tma_load_3d(smem + p.off_b + (kx * p.nq + q) * p.b_blk, &mB, kc, 0,
+                                    kx * p.kys, bres);
                     }
             }
             uint32_t it = 0;
+            const int tpi = p.tiles_x * p.tiles_y;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
                 const int mt = item / p.n_tiles_n, nt = item - mt * p.n_tiles_n;
-                const int tpi = p.tiles_x * p.tiles_y;
                 const int img = mt / tpi, r = mt - img * tpi;
                 const int y0 = (r / p.tiles_x) * kTH, x0 = (r % p.tiles_x) * kTW;
                 for (int kx = 0; kx < p.kxs; ++kx) {
@@ -186,10 +231,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                         const uint32_t ph = (it / (uint32_t)S) & 1u;
                         mbar_wait(full + s, ph);
                         fence_after_sync();
-                        const uint32_t a0 = smem_u32(smem + (size_t)s * stage_bytes);
-                        const uint32_t b0 = p.resident
-                                                ? smem_u32(sB_res + (kx * p.nq + q) * p.b_blk)
-                                                : a0 + p.a_bytes;
+                        const uint32_t a0 = sbase + (uint32_t)s * stage_bytes;
+                        const uint32_t b0 = p.resident ? sbase + p.off_b + (kx * p.nq + q) * p.b_blk
+                                                       : a0 + p.a_bytes;
                         for (int ky = 0; ky < p.kys; ++ky) {
 #pragma unroll
                             for (int j = 0; j < CHUNK / 16; ++j) {
@@ -210,13 +254,16 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
         }
     } else {
         // --------------------------------- epilogue ---------------------------------
-        const int quarter = warp & 3;          // TMEM lane quarter this warp may access
-        const int m = quarter * 32 + lane;     // pixel row of the tile
+        const int e = warp - 2;                  // 0..7
+        const int quarter = warp & 3;            // TMEM lane quarter this warp may access
+        const int half = e >> 2;                 // column-group parity handled by this warp
+        const int m = quarter * 32 + lane;       // pixel row of the tile
         const int tx = m % kTW, ty = m / kTW;
+        const uint32_t spool = sbase + p.off_pool + (uint32_t)half * (128u * 32u);
+        const int tpi = p.tiles_x * p.tiles_y;
         uint32_t acc = 0;
         for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
             const int mt = item / p.n_tiles_n, nt = item - mt * p.n_tiles_n;
-            const int tpi = p.tiles_x * p.tiles_y;
             const int img = mt / tpi, r = mt - img * tpi;
             const int gy = (r / p.tiles_x) * kTH + ty, gx = (r % p.tiles_x) * kTW + tx;
             const bool valid = gx < p.w && gy < p.h;
@@ -225,25 +272,24 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
             fence_after_sync();
             const uint32_t trow = tmem + ab * BN + ((uint32_t)(quarter * 32) << 16);
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 1
-            for (int g = 0; g < BN / 16; ++g) {
+#pragma unroll
+            for (int g = half; g < C::kGroups; g += 2) {
                 const int n = nt * BN + g * 16;
                 if (n >= p.n_total) break;  // uniform
                 uint32_t rr[16];
                 tmem_ld16(trow + (uint32_t)(g * 16), rr);
                 float v[16];
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float a = __uint_as_float(rr[i]);
-                    v[i] = apply_act(fmaf(a, __ldg(p.scale + n + i), __ldg(p.shift + n + i)), p.act,
-                                     p.alpha);
-                }
-                if (p.head_w) {
+                for (int i = 0; i < 16; ++i)
+                    v[i] = apply_act(fmaf(__uint_as_float(rr[i]), s_scale[n + i], s_shift[n + i]),
+                                     p.act, p.alpha);
+                if (MODE == kHead) {
                     for (int j2 = 0; j2 < p.head_c; ++j2) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i)
-                            hacc[j2] = fmaf(__ldg(p.head_w + j2 * p.cout + n + i), v[i], hacc[j2]);
+                            hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
                     }
+                    continue;  // the head's input activation is never stored
                 }
                 uint4 lo, hi;
                 lo.x = pack_bf16(v[0], v[1]);
@@ -257,7 +303,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                 if (valid) {
                     int64_t pix;
                     int o = n;
-                    if (p.transposed) {
+                    if (MODE == kTransposed) {
                         const int dd = n / p.cout;
                         o = n - dd * p.cout;
                         pix = ((int64_t)img * (2 * p.h) + 2 * gy + (dd >> 1)) * (2 * p.w) + 2 * gx +
@@ -278,44 +324,49 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                         dst[3] = make_float4(v[12], v[13], v[14], v[15]);
                     }
                 }
-                if (p.pool) {
-                    uint4 *srow = reinterpret_cast<uint4 *>(spool + m * 16);
-                    srow[0] = lo;
-                    srow[1] = hi;
-                    named_bar_sync(1, 128);
+                if (MODE == kPool) {
+                    st_shared_v4(spool + m * 32, lo);
+                    st_shared_v4(spool + m * 32 + 16, hi);
+                    named_bar_sync(1 + half, 128);
                     if (valid && !(tx & 1) && !(ty & 1)) {
-                        const __nv_bfloat162 *r0 =
-                            reinterpret_cast<const __nv_bfloat162 *>(spool + m * 16);
-                        const __nv_bfloat162 *r1 =
-                            reinterpret_cast<const __nv_bfloat162 *>(spool + (m + 1) * 16);
-                        const __nv_bfloat162 *r2 =
-                            reinterpret_cast<const __nv_bfloat162 *>(spool + (m + kTW) * 16);
-                        const __nv_bfloat162 *r3 =
-                            reinterpret_cast<const __nv_bfloat162 *>(spool + (m + kTW + 1) * 16);
-                        uint32_t ow[8];
+                        uint4 o2[2];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            __nv_bfloat162 mx = __hmax2(__hmax2(r0[i], r1[i]), __hmax2(r2[i], r3[i]));
-                            ow[i] = *reinterpret_cast<uint32_t *>(&mx);
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const uint4 a0 = ld_shared_v4(spool + m * 32 + hh * 16);
+                            const uint4 a1 = ld_shared_v4(spool + (m + 1) * 32 + hh * 16);
+                            const uint4 a2 = ld_shared_v4(spool + (m + kTW) * 32 + hh * 16);
+                            const uint4 a3 = ld_shared_v4(spool + (m + kTW + 1) * 32 + hh * 16);
+                            o2[hh] = make_uint4(hmax4(a0.x, a1.x, a2.x, a3.x),
+                                                hmax4(a0.y, a1.y, a2.y, a3.y),
+                                                hmax4(a0.z, a1.z, a2.z, a3.z),
+                                                hmax4(a0.w, a1.w, a2.w, a3.w));
                         }
                         const int64_t pp = ((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
                         uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
-                        dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-                        dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+                        dst[0] = o2[0];
+                        dst[1] = o2[1];
                     }
-                    named_bar_sync(1, 128);
+                    named_bar_sync(1 + half, 128);
                 }
             }
             // accumulator drained -> hand the TMEM buffer back to the MMA warp
             fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + ab);
-            if (p.head_w && valid) {
-                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
-                for (int j2 = 0; j2 < p.head_c; ++j2) {
-                    const float z = hacc[j2] + __ldg(p.head_b + j2);
-                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+            if (MODE == kHead) {
+                // combine the two column halves' partial dot products
+                float *hst = reinterpret_cast<float *>(smem + p.off_pool);
+                if (half == 1)
+                    for (int j2 = 0; j2 < 4; ++j2) hst[m * 4 + j2] = hacc[j2];
+                named_bar_sync(3, 32 * kEpiWarps);
+                if (half == 0 && valid) {
+                    const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
+                    for (int j2 = 0; j2 < p.head_c; ++j2) {
+                        const float z = hacc[j2] + hst[m * 4 + j2] + __ldg(p.head_b + j2);
+                        p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                    }
                 }
+                named_bar_sync(3, 32 * kEpiWarps);
             }
         }
     }
@@ -357,7 +408,7 @@ using namespace ls::unet;
 struct ls_conv_plan {
     CUtensorMap a0, a1, b;
     ConvParamsP p;
-    int bn, chunk, grid;
+    int bn, chunk, grid, mode;
     size_t smem;
 };
 
@@ -393,18 +444,29 @@ static bool encode_wts_p(CUtensorMap *map, const void *base, int ctot, int n_tot
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int CHUNK>
-static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
+template <int BN, int CHUNK, int MODE>
+static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;  // idempotent: racing threads set the same value
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK>,
+        cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
         attr_done = 1;
     }
-    k_conv_p<BN, CHUNK><<<pl->grid, kThreadsP, pl->smem, st>>>(pl->a0, pl->a1, pl->b, pl->p);
+    k_conv_p<BN, CHUNK, MODE><<<pl->grid, kThreadsP, pl->smem, st>>>(pl->a0, pl->a1, pl->b,
+                                                                      pl->p);
     return (int)cudaGetLastError();
+}
+
+template <int BN, int CHUNK>
+static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
+    switch (pl->mode) {
+        case kPlain: return launch_m<BN, CHUNK, kPlain>(pl, st);
+        case kPool: return launch_m<BN, CHUNK, kPool>(pl, st);
+        case kHead: return launch_m<BN, CHUNK, kHead>(pl, st);
+        default: return launch_m<BN, CHUNK, kTransposed>(pl, st);
+    }
 }
 
 }  // namespace unet
@@ -459,7 +521,6 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.pad = ksize == 3 ? 1 : 0;
     p.n_total = n_total;
     p.cout = cout;
-    p.transposed = transposed ? 1 : 0;
     p.act = act;
     p.alpha = alpha;
     p.scale = d_scale;
@@ -480,7 +541,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
     const size_t res_bytes = p.resident ? nk * p.b_blk : 0;
     const size_t stage_bytes = p.a_bytes + (p.resident ? 0 : p.b_blk);
-    const size_t fixed = res_bytes + 4096 + 256;
+    const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
+                               ~size_t(1023);
+    const size_t fixed = res_bytes + const_bytes + 8192 + 256;
     int stages = (int)((kSmemBudget - fixed) / stage_bytes);
     if (stages > 8) stages = 8;
     if (stages < 2) {
@@ -489,11 +552,13 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     p.stages = stages;
     p.off_b = (uint32_t)(stages * stage_bytes);
-    p.off_pool = (uint32_t)(p.off_b + res_bytes);
-    p.off_bar = p.off_pool + 4096;
+    p.off_const = (uint32_t)(p.off_b + res_bytes);
+    p.off_pool = (uint32_t)(p.off_const + const_bytes);
+    p.off_bar = p.off_pool + 8192;
     pl->smem = 1024 + p.off_bar + 256;
     pl->bn = bn;
     pl->chunk = chunk;
+    pl->mode = transposed ? kTransposed : (d_head_w ? kHead : (d_pool ? kPool : kPlain));
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
