@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                         for (int i = 0; i < 16; ++i)
                             hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
                     }
-                    continue;  // the head's input activation is never stored
+                    if (!p.y && !p.y_f32) continue;  // head input not materialised
                 }
                 uint4 lo, hi;
                 lo.x = pack_bf16(v[0], v[1]);
