@@ -53,8 +53,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 //   * Epilogue constants (folded-BN scale/shift, head weights) are staged in
 //     shared memory once per CTA.
 //   Weight layout: [tap][n][c] with tap = kx*kys + ky (kx-major).
-constexpr int kEpiWarps = 8;
-constexpr int kThreadsP = 64 + 32 * kEpiWarps;
 constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
 constexpr size_t kSmemBudget = 222 * 1024;
@@ -84,6 +82,7 @@ struct ConvParamsP {
     uint32_t off_const;    // scale[n_total], shift[n_total], head_w, head_b (f32)
     uint32_t off_pool;     // pool / head staging
     uint32_t off_bar;      // barriers
+    int dbg;               // experiments: bit0 skip MMA, bit1 skip stores, bit2 skip TMA A
 };
 
 template <int BN, int CHUNK>
@@ -91,9 +90,20 @@ struct CfgP {
     static constexpr uint32_t kRow = CHUNK * 2;  // bytes per operand row
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
-    static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    // epilogue warpgroups (4 warps = the 4 TMEM lane quarters) working on
+    // different tiles concurrently, and TMEM accumulator buffers so the MMA
+    // warp can run ahead of all of them
+    static constexpr int kEpiGroups = BN >= 256 ? 1 : (BN >= 128 ? 2 : (BN >= 64 ? 3 : 4));
+    static constexpr int kAcc = (512 / BN) < 2 * kEpiGroups ? (512 / BN) : 2 * kEpiGroups;
+    static constexpr int kThreads = 64 + 128 * kEpiGroups;
+    static constexpr int kTmemColsRaw = kAcc * BN;
+    static constexpr int kTmemCols = kTmemColsRaw <= 32 ? 32 : (kTmemColsRaw <= 64 ? 64 :
+                                     (kTmemColsRaw <= 128 ? 128 : (kTmemColsRaw <= 256 ? 256 : 512)));
     static constexpr int kGroups = BN / 16;
 };
+
+template <int BN, int CHUNK>
+constexpr int threads_for() { return CfgP<BN, CHUNK>::kThreads; }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
@@ -120,7 +130,7 @@ __device__ __forceinline__ uint32_t hmax4(uint32_t a, uint32_t b, uint32_t c, ui
 }
 
 template <int BN, int CHUNK, int MODE>
-__global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__ CUtensorMap mA0,
+__global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __grid_constant__ CUtensorMap mA0,
                                                          const __grid_constant__ CUtensorMap mA1,
                                                          const __grid_constant__ CUtensorMap mB,
                                                          const ConvParamsP p) {
@@ -138,8 +148,8 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
-    uint64_t *tempty = tfull + 2;
-    uint64_t *bres = tempty + 2;
+    uint64_t *tempty = tfull + C::kAcc;
+    uint64_t *bres = tempty + C::kAcc;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,9 +159,9 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                 mbar_init(full + s, 1);
                 mbar_init(empty + s, 1);
             }
-            for (int a = 0; a < 2; ++a) {
+            for (int a = 0; a < C::kAcc; ++a) {
                 mbar_init(tfull + a, 1);
-                mbar_init(tempty + a, kEpiWarps);
+                mbar_init(tempty + a, 4);
             }
             mbar_init(bres, 1);
             fence_barrier_init();
@@ -164,12 +174,13 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
     } else if (warp >= 2) {
         // stage the epilogue constants (visible after the __syncthreads below)
         const int t = threadIdx.x - 64;
-        for (int i = t; i < p.n_total; i += 32 * kEpiWarps) {
+        constexpr int kEpiThreads = 128 * C::kEpiGroups;
+        for (int i = t; i < p.n_total; i += kEpiThreads) {
             sconst[i] = p.scale[i];
             sconst[p.n_total + i] = p.shift[i];
         }
         if (MODE == kHead)
-            for (int i = t; i < p.head_c * p.cout; i += 32 * kEpiWarps)
+            for (int i = t; i < p.head_c * p.cout; i += kEpiThreads)
                 sconst[2 * p.n_total + i] = p.head_w[i];
     }
     fence_before_sync();
@@ -204,6 +215,10 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                         uint8_t *st = smem + (size_t)s * stage_bytes;
                         const bool second = q >= p.nq0;
                         const int c = (second ? q - p.nq0 : q) * CHUNK;
+                        if (p.dbg & 4) {
+                            mbar_arrive(full + s);
+                            continue;
+                        }
                         mbar_expect_tx(full + s, p.a_tx + (p.resident ? 0u : p.b_blk));
                         tma_load_4d(st, second ? &mA1 : &mA0, c, x0 + kx - p.pad, y0 - p.pad, img,
                                     full + s);
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
             if (p.resident) mbar_wait(bres, 0);
             uint32_t it = 0, acc = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
-                const uint32_t ab = acc & 1u, aph = (acc >> 1) & 1u;
+                const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
                 mbar_wait(tempty + ab, aph ^ 1u);
                 fence_after_sync();
                 const uint32_t d = tmem + ab * BN;
@@ -238,6 +253,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
 #pragma unroll
                             for (int j = 0; j < CHUNK / 16; ++j) {
                                 const uint32_t accum = (kx | q | ky | j) != 0;
+                                if (p.dbg & 1) continue;
                                 mma_bf16(d,
                                          smem_desc(a0 + (uint32_t)(ky * kTW) * C::kRow + 32u * j,
                                                    C::kRow, C::kLayout),
@@ -254,30 +270,38 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
         }
     } else {
         // --------------------------------- epilogue ---------------------------------
-        const int e = warp - 2;                  // 0..7
+        // warpgroup eg (4 warps, one per TMEM lane quarter) drains every
+        // kEpiGroups-th tile of this CTA, all column groups of it
+        const int eg = (warp - 2) >> 2;
         const int quarter = warp & 3;            // TMEM lane quarter this warp may access
-        const int half = e >> 2;                 // column-group parity handled by this warp
         const int m = quarter * 32 + lane;       // pixel row of the tile
         const int tx = m % kTW, ty = m / kTW;
-        const uint32_t spool = sbase + p.off_pool + (uint32_t)half * (128u * 32u);
+        const uint32_t spool = sbase + p.off_pool + (uint32_t)eg * (128u * 32u);
         const int tpi = p.tiles_x * p.tiles_y;
-        uint32_t acc = 0;
-        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
+        uint32_t acc = (uint32_t)eg;
+        for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
+             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
             const int mt = item / p.n_tiles_n, nt = item - mt * p.n_tiles_n;
             const int img = mt / tpi, r = mt - img * tpi;
             const int gy = (r / p.tiles_x) * kTH + ty, gx = (r % p.tiles_x) * kTW + tx;
             const bool valid = gx < p.w && gy < p.h;
-            const uint32_t ab = acc & 1u, aph = (acc >> 1) & 1u;
+            const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             const uint32_t trow = tmem + ab * BN + ((uint32_t)(quarter * 32) << 16);
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-            for (int g = half; g < C::kGroups; g += 2) {
+#pragma unroll 1
+            for (int g = 0; g < C::kGroups; ++g) {
                 const int n = nt * BN + g * 16;
                 if (n >= p.n_total) break;  // uniform
                 uint32_t rr[16];
                 tmem_ld16(trow + (uint32_t)(g * 16), rr);
+                if (g + 1 == C::kGroups || n + 16 >= p.n_total) {
+                    // accumulator fully read -> hand the TMEM buffer back early
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty + ab);
+                }
                 float v[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i)
@@ -300,7 +324,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                 hi.y = pack_bf16(v[10], v[11]);
                 hi.z = pack_bf16(v[12], v[13]);
                 hi.w = pack_bf16(v[14], v[15]);
-                if (valid) {
+                if (valid && !(p.dbg & 2)) {
                     int64_t pix;
                     int o = n;
                     if (MODE == kTransposed) {
@@ -327,7 +351,7 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                 if (MODE == kPool) {
                     st_shared_v4(spool + m * 32, lo);
                     st_shared_v4(spool + m * 32 + 16, hi);
-                    named_bar_sync(1 + half, 128);
+                    named_bar_sync(1 + eg, 128);
                     if (valid && !(tx & 1) && !(ty & 1)) {
                         uint4 o2[2];
 #pragma unroll
@@ -346,27 +370,15 @@ __global__ void __launch_bounds__(kThreadsP, 1) k_conv_p(const __grid_constant__
                         dst[0] = o2[0];
                         dst[1] = o2[1];
                     }
-                    named_bar_sync(1 + half, 128);
+                    named_bar_sync(1 + eg, 128);
                 }
             }
-            // accumulator drained -> hand the TMEM buffer back to the MMA warp
-            fence_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + ab);
-            if (MODE == kHead) {
-                // combine the two column halves' partial dot products
-                float *hst = reinterpret_cast<float *>(smem + p.off_pool);
-                if (half == 1)
-                    for (int j2 = 0; j2 < 4; ++j2) hst[m * 4 + j2] = hacc[j2];
-                named_bar_sync(3, 32 * kEpiWarps);
-                if (half == 0 && valid) {
-                    const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
-                    for (int j2 = 0; j2 < p.head_c; ++j2) {
-                        const float z = hacc[j2] + hst[m * 4 + j2] + __ldg(p.head_b + j2);
-                        p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
-                    }
+            if (MODE == kHead && valid) {
+                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
+                for (int j2 = 0; j2 < p.head_c; ++j2) {
+                    const float z = hacc[j2] + __ldg(p.head_b + j2);
+                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
                 }
-                named_bar_sync(3, 32 * kEpiWarps);
             }
         }
     }
@@ -454,8 +466,8 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = 1;
     }
-    k_conv_p<BN, CHUNK, MODE><<<pl->grid, kThreadsP, pl->smem, st>>>(pl->a0, pl->a1, pl->b,
-                                                                      pl->p);
+    k_conv_p<BN, CHUNK, MODE><<<pl->grid, CfgP<BN, CHUNK>::kThreads, pl->smem, st>>>(
+        pl->a0, pl->a1, pl->b, pl->p);
     return (int)cudaGetLastError();
 }
 
@@ -543,9 +555,19 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     const size_t stage_bytes = p.a_bytes + (p.resident ? 0 : p.b_blk);
     const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
                                ~size_t(1023);
-    const size_t fixed = res_bytes + const_bytes + 8192 + 256;
-    int stages = (int)((kSmemBudget - fixed) / stage_bytes);
-    if (stages > 8) stages = 8;
+    const size_t fixed = res_bytes + const_bytes + 16384 + 512;
+    // tuning knobs (experiments only): LS_CONV_MAX_STAGES, LS_CONV_CTAS_PER_SM
+    const char *env_st = getenv("LS_CONV_MAX_STAGES");
+    const char *env_cps = getenv("LS_CONV_CTAS_PER_SM");
+    const int max_stages = env_st ? atoi(env_st) : 8;
+    const int ctas_per_sm = env_cps ? atoi(env_cps) : 1;
+    const size_t budget = kSmemBudget / (ctas_per_sm > 1 ? ctas_per_sm : 1);
+    if (budget <= fixed + 2 * stage_bytes) {
+        delete pl;
+        return fail(LS_EINVAL);
+    }
+    int stages = (int)((budget - fixed) / stage_bytes);
+    if (stages > max_stages) stages = max_stages;
     if (stages < 2) {
         delete pl;
         return fail(LS_EINVAL);
@@ -554,14 +576,17 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.off_b = (uint32_t)(stages * stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
-    p.off_bar = p.off_pool + 8192;
-    pl->smem = 1024 + p.off_bar + 256;
+    p.off_bar = p.off_pool + 16384;
+    pl->smem = 1024 + p.off_bar + 512;
     pl->bn = bn;
     pl->chunk = chunk;
     pl->mode = transposed ? kTransposed : (d_head_w ? kHead : (d_pool ? kPool : kPlain));
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    const char *env_dbg = getenv("LS_CONV_DBG");
+    p.dbg = env_dbg ? atoi(env_dbg) : 0;
+    const int max_ctas = n_sm * (ctas_per_sm > 1 ? ctas_per_sm : 1);
+    pl->grid = p.n_items < max_ctas ? p.n_items : max_ctas;
     bool ok = encode_act_p(&pl->a0, d_x0, c0, w, h, batch, chunk, box_h);
     ok = ok && encode_act_p(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0, w, h, batch, chunk,
                             box_h);
