@@ -83,7 +83,14 @@ struct ConvParamsP {
     uint32_t off_pool;     // pool / head staging
     uint32_t off_bar;      // barriers
     int dbg;               // experiments: bit0 skip MMA, bit1 skip stores, bit2 skip TMA A
+    unsigned long long *dbg_ts;  // bit3: per-CTA event timestamps (globaltimer)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 template <int BN, int CHUNK>
 struct CfgP {
@@ -135,12 +142,14 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __gri
                                                          const __grid_constant__ CUtensorMap mB,
                                                          const ConvParamsP p) {
     using C = CfgP<BN, CHUNK>;
+    constexpr int KXS = MODE == kTransposed ? 1 : 3;
+    constexpr int KYS = KXS;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align inside the shared window (keeps the shared address space visible)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     const int S = p.stages;
-    const uint32_t stage_bytes = p.a_bytes + (p.resident ? 0u : p.b_blk);
+    const uint32_t stage_bytes = KXS * (p.a_bytes + (p.resident ? 0u : p.b_blk));
     float *sconst = reinterpret_cast<float *>(smem + p.off_const);
     const float *s_scale = sconst;
     const float *s_shift = sconst + p.n_total;
@@ -192,13 +201,13 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __gri
         if (lane == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (p.resident) {
-                mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk);
-                for (int kx = 0; kx < p.kxs; ++kx)
-                    for (int q = 0; q < p.nq; ++q) {
+                mbar_expect_tx(bres, (uint32_t)(KXS * p.nq) * p.b_blk);
+                for (int q = 0; q < p.nq; ++q)
+                    for (int kx = 0; kx < KXS; ++kx) {
                         const bool second = q >= p.nq0;
                         const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
-                        tma_load_3d(smem + p.off_b + (kx * p.nq + q) * p.b_blk, &mB, kc, 0,
-                                    kx * p.kys, bres);
+                        tma_load_3d(smem + p.off_b + (q * KXS + kx) * p.b_blk, &mB, kc, 0, kx * KYS,
+                                    bres);
                     }
             }
             uint32_t it = 0;
@@ -207,24 +216,29 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __gri
                 const int mt = item / p.n_tiles_n, nt = item - mt * p.n_tiles_n;
                 const int img = mt / tpi, r = mt - img * tpi;
                 const int y0 = (r / p.tiles_x) * kTH, x0 = (r % p.tiles_x) * kTW;
-                for (int kx = 0; kx < p.kxs; ++kx) {
-                    for (int q = 0; q < p.nq; ++q, ++it) {
-                        const int s = (int)(it % (uint32_t)S);
-                        const uint32_t ph = (it / (uint32_t)S) & 1u;
-                        mbar_wait(empty + s, ph ^ 1u);
-                        uint8_t *st = smem + (size_t)s * stage_bytes;
-                        const bool second = q >= p.nq0;
-                        const int c = (second ? q - p.nq0 : q) * CHUNK;
-                        if (p.dbg & 4) {
-                            mbar_arrive(full + s);
-                            continue;
-                        }
-                        mbar_expect_tx(full + s, p.a_tx + (p.resident ? 0u : p.b_blk));
-                        tma_load_4d(st, second ? &mA1 : &mA0, c, x0 + kx - p.pad, y0 - p.pad, img,
-                                    full + s);
+                const uint32_t tl = (uint32_t)((item - (int)blockIdx.x) / (int)gridDim.x);
+                if ((p.dbg & 8) && !(p.dbg & 16) && tl < 64)
+                    p.dbg_ts[(blockIdx.x * 4 + 2) * 64 + tl] = gtimer();
+                // one stage = one channel chunk, all KXS input boxes (+ weight blocks)
+                for (int q = 0; q < p.nq; ++q, ++it) {
+                    const int s = (int)(it % (uint32_t)S);
+                    const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    mbar_wait(empty + s, ph ^ 1u);
+                    uint8_t *st = smem + (size_t)s * stage_bytes;
+                    const bool second = q >= p.nq0;
+                    const int c = (second ? q - p.nq0 : q) * CHUNK;
+                    if (p.dbg & 4) {
+                        mbar_arrive(full + s);
+                        continue;
+                    }
+                    mbar_expect_tx(full + s, KXS * (p.a_tx + (p.resident ? 0u : p.b_blk)));
+#pragma unroll
+                    for (int kx = 0; kx < KXS; ++kx) {
+                        tma_load_4d(st + kx * p.a_bytes, second ? &mA1 : &mA0, c, x0 + kx - p.pad,
+                                    y0 - p.pad, img, full + s);
                         if (!p.resident)
-                            tma_load_3d(st + p.a_bytes, &mB, (second ? p.c0 : 0) + c, nt * BN,
-                                        kx * p.kys, full + s);
+                            tma_load_3d(st + KXS * p.a_bytes + kx * p.b_blk, &mB,
+                                        (second ? p.c0 : 0) + c, nt * BN, kx * KYS, full + s);
                     }
                 }
             }
@@ -232,38 +246,53 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __gri
     } else if (warp == 1) {
         if (lane == 0) {
             // ------------------------------- MMA issuer -------------------------------
+            // Descriptors are built once: per MMA only the 14-bit start-address
+            // field (low word) moves, by compile-time offsets.
             const uint32_t idesc = idesc_bf16(128, BN);
+            const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
+            const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
             if (p.resident) mbar_wait(bres, 0);
+            const uint32_t a_box16 = p.a_bytes >> 4, b_blk16 = p.b_blk >> 4;
             uint32_t it = 0, acc = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
                 const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
+                if ((p.dbg & 8) && acc < 64) p.dbg_ts[(blockIdx.x * 4 + 0) * 64 + acc] = gtimer();
                 mbar_wait(tempty + ab, aph ^ 1u);
+                if ((p.dbg & 8) && acc < 64) p.dbg_ts[(blockIdx.x * 4 + 1) * 64 + acc] = gtimer();
                 fence_after_sync();
                 const uint32_t d = tmem + ab * BN;
-                for (int kx = 0; kx < p.kxs; ++kx) {
-                    for (int q = 0; q < p.nq; ++q, ++it) {
-                        const int s = (int)(it % (uint32_t)S);
-                        const uint32_t ph = (it / (uint32_t)S) & 1u;
-                        mbar_wait(full + s, ph);
-                        fence_after_sync();
-                        const uint32_t a0 = sbase + (uint32_t)s * stage_bytes;
-                        const uint32_t b0 = p.resident ? sbase + p.off_b + (kx * p.nq + q) * p.b_blk
-                                                       : a0 + p.a_bytes;
-                        for (int ky = 0; ky < p.kys; ++ky) {
+                for (int q = 0; q < p.nq; ++q, ++it) {
+                    const int s = (int)(it % (uint32_t)S);
+                    const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    mbar_wait(full + s, ph);
+                    if ((p.dbg & 16) && q == 0 && acc < 64)
+                        p.dbg_ts[(blockIdx.x * 4 + 2) * 64 + acc] = gtimer();
+                    fence_after_sync();
+                    const uint32_t a_lo = dlo + ((sbase + (uint32_t)s * stage_bytes) >> 4);
+                    const uint32_t b_lo =
+                        dlo + ((p.resident ? sbase + p.off_b + (uint32_t)(q * KXS) * p.b_blk
+                                           : sbase + (uint32_t)s * stage_bytes + KXS * p.a_bytes) >>
+                               4);
+                    if (!(p.dbg & 1)) {
 #pragma unroll
-                            for (int j = 0; j < CHUNK / 16; ++j) {
-                                const uint32_t accum = (kx | q | ky | j) != 0;
-                                if (p.dbg & 1) continue;
-                                mma_bf16(d,
-                                         smem_desc(a0 + (uint32_t)(ky * kTW) * C::kRow + 32u * j,
-                                                   C::kRow, C::kLayout),
-                                         smem_desc(b0 + (uint32_t)(ky * BN) * C::kRow + 32u * j,
-                                                   C::kRow, C::kLayout),
-                                         idesc, accum);
+                        for (int kx = 0; kx < KXS; ++kx) {
+#pragma unroll
+                            for (int ky = 0; ky < KYS; ++ky) {
+#pragma unroll
+                                for (int j = 0; j < CHUNK / 16; ++j) {
+                                    const uint32_t ao = kx * a_box16 + (ky * kTW * C::kRow + 32 * j) / 16;
+                                    const uint32_t bo = kx * b_blk16 + (ky * BN * C::kRow + 32 * j) / 16;
+                                    const uint64_t adesc = ((uint64_t)dhi << 32) | (a_lo + ao);
+                                    const uint64_t bdesc = ((uint64_t)dhi << 32) | (b_lo + bo);
+                                    mma_bf16(d, adesc, bdesc, idesc,
+                                             (q | kx | ky | j) != 0 ? 1u : 0u);
+                                }
                             }
                         }
-                        mma_commit(empty + s);
                     }
+                    mma_commit(empty + s);
+                    if ((p.dbg & 16) && q == 0 && acc < 64)
+                        p.dbg_ts[(blockIdx.x * 4 + 3) * 64 + acc] = gtimer();
                 }
                 mma_commit(tfull + ab);
             }
@@ -287,6 +316,8 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(const __gri
             const bool valid = gx < p.w && gy < p.h;
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
+            if ((p.dbg & 8) && !(p.dbg & 16) && acc < 64 && quarter == 0 && lane == 0)
+                p.dbg_ts[(blockIdx.x * 4 + 3) * 64 + acc] = gtimer();
             fence_after_sync();
             const uint32_t trow = tmem + ab * BN + ((uint32_t)(quarter * 32) << 16);
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -521,13 +552,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.tiles_x = (w + kTW - 1) / kTW;
     p.tiles_y = (h + kTH - 1) / kTH;
     p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
-    p.n_tiles_n = (n_total + bn - 1) / bn;
-    p.n_items = p.n_tiles_m * p.n_tiles_n;
     p.c0 = c0;
     p.c1 = c1;
     p.ctot = c0 + c1;
-    p.nq0 = c0 / chunk;
-    p.nq = (c0 + c1) / chunk;
     p.kxs = ksize == 3 ? 3 : 1;
     p.kys = ksize == 3 ? 3 : 1;
     p.pad = ksize == 3 ? 1 : 0;
@@ -544,34 +571,40 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.head_b = d_head_b;
     p.head_c = head_c;
     p.head_out = d_head_out;
-    const uint32_t row = (uint32_t)chunk * 2;
+    const char *env_st = getenv("LS_CONV_MAX_STAGES");  // tuning experiments only
+    const int max_stages = env_st ? atoi(env_st) : 8;
     const int box_h = kTH + 2 * p.pad;
-    p.a_tx = (uint32_t)(kTW * box_h) * row;
-    p.a_bytes = (p.a_tx + 1023u) & ~1023u;
-    p.b_blk = (uint32_t)(p.kys * bn) * row;
-    const size_t nk = (size_t)p.kxs * p.nq;
-    p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
-    const size_t res_bytes = p.resident ? nk * p.b_blk : 0;
-    const size_t stage_bytes = p.a_bytes + (p.resident ? 0 : p.b_blk);
     const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
                                ~size_t(1023);
-    const size_t fixed = res_bytes + const_bytes + 16384 + 512;
-    // tuning knobs (experiments only): LS_CONV_MAX_STAGES, LS_CONV_CTAS_PER_SM
-    const char *env_st = getenv("LS_CONV_MAX_STAGES");
-    const char *env_cps = getenv("LS_CONV_CTAS_PER_SM");
-    const int max_stages = env_st ? atoi(env_st) : 8;
-    const int ctas_per_sm = env_cps ? atoi(env_cps) : 1;
-    const size_t budget = kSmemBudget / (ctas_per_sm > 1 ? ctas_per_sm : 1);
-    if (budget <= fixed + 2 * stage_bytes) {
-        delete pl;
-        return fail(LS_EINVAL);
+    size_t res_bytes = 0, stage_bytes = 0;
+    int stages = 0;
+    // shrink the K chunk, then the column tile, until >= 2 pipeline stages fit
+    for (;;) {
+        const uint32_t row = (uint32_t)chunk * 2;
+        p.nq0 = c0 / chunk;
+        p.nq = (c0 + c1) / chunk;
+        p.a_tx = (uint32_t)(kTW * box_h) * row;
+        p.a_bytes = (p.a_tx + 1023u) & ~1023u;
+        p.n_tiles_n = (n_total + bn - 1) / bn;
+        p.n_items = p.n_tiles_m * p.n_tiles_n;
+        p.b_blk = (uint32_t)(p.kys * bn) * row;
+        const size_t nk = (size_t)p.kxs * p.nq;
+        p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
+        res_bytes = p.resident ? nk * p.b_blk : 0;
+        stage_bytes = (size_t)p.kxs * (p.a_bytes + (p.resident ? 0 : p.b_blk));
+        const size_t fixed = res_bytes + const_bytes + 16384 + 512;
+        stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
+        if (stages >= 2) break;
+        if (chunk > 16 && (c0 % (chunk / 2)) == 0 && (c1 % (chunk / 2)) == 0) {
+            chunk >>= 1;
+        } else if (bn > 32 && !d_head_w) {
+            bn >>= 1;
+        } else {
+            delete pl;
+            return fail(LS_EINVAL);
+        }
     }
-    int stages = (int)((budget - fixed) / stage_bytes);
     if (stages > max_stages) stages = max_stages;
-    if (stages < 2) {
-        delete pl;
-        return fail(LS_EINVAL);
-    }
     p.stages = stages;
     p.off_b = (uint32_t)(stages * stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
@@ -585,8 +618,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     const char *env_dbg = getenv("LS_CONV_DBG");
     p.dbg = env_dbg ? atoi(env_dbg) : 0;
-    const int max_ctas = n_sm * (ctas_per_sm > 1 ? ctas_per_sm : 1);
-    pl->grid = p.n_items < max_ctas ? p.n_items : max_ctas;
+    p.dbg_ts = nullptr;
+    if (p.dbg & 8) cudaMalloc(&p.dbg_ts, 148 * 4 * 64 * sizeof(unsigned long long));
+    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     bool ok = encode_act_p(&pl->a0, d_x0, c0, w, h, batch, chunk, box_h);
     ok = ok && encode_act_p(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0, w, h, batch, chunk,
                             box_h);
@@ -612,7 +646,16 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     return LS_EINVAL;
 }
 
-void ls_conv_plan_destroy(ls_conv_plan *pl) { delete pl; }
+void ls_conv_plan_destroy(ls_conv_plan *pl) {
+    if (pl && pl->p.dbg_ts) cudaFree(pl->p.dbg_ts);
+    delete pl;
+}
+
+/* experiments only: copy the per-CTA event timestamps (LS_CONV_DBG bit 3) */
+int ls_conv_plan_debug_ts(const ls_conv_plan *pl, unsigned long long *host, int n) {
+    if (!pl || !pl->p.dbg_ts || n > 148 * 4 * 64) return LS_EINVAL;
+    return (int)cudaMemcpy(host, pl->p.dbg_ts, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
 
 int ls_conv2d(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1, int32_t c1, int32_t batch,
               int32_t h, int32_t w, const uint16_t *d_w, int32_t ksize, int32_t cout,
