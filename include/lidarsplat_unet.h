@@ -31,7 +31,7 @@ typedef struct ls_conv_plan ls_conv_plan;
  * convTranspose2x2 when transposed != 0):
  *
  *   conv      y[n,y,x,o] = act(scale[o] * sum_{ky,kx,c} X[n,y+ky-1,x+kx-1,c] W[kx*3+ky][o][c]
- *                              + shift[o])                (ksize 3; ksize 1 = no shift)
+ *                              + shift[o])                (ksize 3)
  *   transposed y[n,2i+dy,2j+dx,o] = act(scale[q] * sum_c X[n,i,j,c] W[0][q][c] + shift[q]),
  *              q = (dy*2+dx)*cout + o                     (scale/shift have 4*cout entries)
  *
