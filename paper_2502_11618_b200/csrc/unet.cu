@@ -68,7 +68,7 @@ struct ConvParamsP {
     uint32_t stage_bytes;
     uint32_t off_b;         // resident weights
     uint32_t off_const;     // scale[n_total], shift[n_total], head_w (f32)
-    uint32_t off_pool;      // pool staging
+    uint32_t off_pool;      // (unused: pooling is done with warp shuffles)
     uint32_t off_bar;       // barriers
 };
 
@@ -309,11 +309,13 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
         }
     } else {
         // --------------------------------- epilogue ---------------------------------
+        // Pixel m = quarter*32 + lane of a sub-tile is (row m/16, col m%16): the
+        // 2x2 max-pool partners of a lane are lanes ^1 and ^16 of the SAME warp,
+        // so pooling is two shuffle-max steps (no shared memory, no barriers).
         const int eg = (warp - 2) >> 2;          // warpgroup -> every kEpiGroups-th item
         const int quarter = warp & 3;            // TMEM lane quarter this warp may access
-        const int m = quarter * 32 + lane;       // pixel row of a sub-tile
+        const int m = quarter * 32 + lane;
         const int tx = m % kTW, ty = m / kTW;
-        const uint32_t spool = sbase + p.off_pool + (uint32_t)eg * (128u * 32u);
         uint32_t acc = (uint32_t)eg;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
@@ -329,87 +331,77 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                 const bool valid = gx < p.w && gy < p.h;
                 float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 1
-                for (int g = 0; g < C::kGroups; ++g) {
-                    const int n = ip.nt * BN + g * 16;
-                    if (n >= p.n_total) break;  // uniform
-                    uint32_t rr[16];
-                    tmem_ld16(tbase + (uint32_t)(u * BN + g * 16), rr);
-                    if (u + 1 == MT && (g + 1 == C::kGroups || n + 16 >= p.n_total)) {
+                for (int g = 0; g < BN / 32; ++g) {
+                    const int n0 = ip.nt * BN + g * 32;
+                    if (n0 >= p.n_total) break;  // uniform
+                    uint32_t rr[32];
+                    tmem_ld32(tbase + (uint32_t)(u * BN + g * 32), rr);
+                    if (u + 1 == MT && (g + 1 == BN / 32 || n0 + 32 >= p.n_total)) {
                         // item fully read -> hand the TMEM buffer back early
                         fence_before_sync();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(tempty + ab);
                     }
-                    float v[16];
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        v[i] = apply_act(fmaf(__uint_as_float(rr[i]), s_scale[n + i], s_shift[n + i]),
-                                         p.act, p.alpha);
-                    if (MODE == kHead) {
-                        for (int j2 = 0; j2 < p.head_c; ++j2) {
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int n = n0 + h2 * 16;
+                        float v[16];
 #pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
-                        }
-                        if (!p.y && !p.y_f32) continue;  // head input not materialised
-                    }
-                    uint4 lo, hi;
-                    lo.x = pack_bf16(v[0], v[1]);
-                    lo.y = pack_bf16(v[2], v[3]);
-                    lo.z = pack_bf16(v[4], v[5]);
-                    lo.w = pack_bf16(v[6], v[7]);
-                    hi.x = pack_bf16(v[8], v[9]);
-                    hi.y = pack_bf16(v[10], v[11]);
-                    hi.z = pack_bf16(v[12], v[13]);
-                    hi.w = pack_bf16(v[14], v[15]);
-                    if (valid) {
-                        int64_t pix;
-                        int o = n;
-                        if (MODE == kTransposed) {
-                            const int dd = n / p.cout;
-                            o = n - dd * p.cout;
-                            pix = ((int64_t)ip.img * (2 * p.h) + 2 * gy + (dd >> 1)) * (2 * p.w) +
-                                  2 * gx + (dd & 1);
-                        } else {
-                            pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
-                        }
-                        if (p.y) {
-                            uint4 *dst = reinterpret_cast<uint4 *>(p.y + pix * p.cout + o);
-                            dst[0] = lo;
-                            dst[1] = hi;
-                        }
-                        if (p.y_f32) {
-                            float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + o);
-                            dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-                            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-                            dst[2] = make_float4(v[8], v[9], v[10], v[11]);
-                            dst[3] = make_float4(v[12], v[13], v[14], v[15]);
-                        }
-                    }
-                    if (MODE == kPool) {
-                        st_shared_v4(spool + m * 32, lo);
-                        st_shared_v4(spool + m * 32 + 16, hi);
-                        named_bar_sync(1 + eg, 128);
-                        if (valid && !(tx & 1) && !(ty & 1)) {
-                            uint4 o2[2];
+                        for (int i = 0; i < 16; ++i)
+                            v[i] = apply_act(fmaf(__uint_as_float(rr[h2 * 16 + i]), s_scale[n + i],
+                                                  s_shift[n + i]),
+                                             p.act, p.alpha);
+                        if (MODE == kHead) {
+                            for (int j2 = 0; j2 < p.head_c; ++j2) {
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const uint4 a0 = ld_shared_v4(spool + m * 32 + hh * 16);
-                                const uint4 a1 = ld_shared_v4(spool + (m + 1) * 32 + hh * 16);
-                                const uint4 a2 = ld_shared_v4(spool + (m + kTW) * 32 + hh * 16);
-                                const uint4 a3 = ld_shared_v4(spool + (m + kTW + 1) * 32 + hh * 16);
-                                o2[hh] = make_uint4(hmax4(a0.x, a1.x, a2.x, a3.x),
-                                                    hmax4(a0.y, a1.y, a2.y, a3.y),
-                                                    hmax4(a0.z, a1.z, a2.z, a3.z),
-                                                    hmax4(a0.w, a1.w, a2.w, a3.w));
+                                for (int i = 0; i < 16; ++i)
+                                    hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
                             }
-                            const int64_t pp =
-                                ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
-                            uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
-                            dst[0] = o2[0];
-                            dst[1] = o2[1];
+                            if (!p.y && !p.y_f32) continue;  // head input not materialised
                         }
-                        named_bar_sync(1 + eg, 128);
+                        uint32_t pk[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                        if (valid) {
+                            int64_t pix;
+                            int o = n;
+                            if (MODE == kTransposed) {
+                                const int dd = n / p.cout;
+                                o = n - dd * p.cout;
+                                pix = ((int64_t)ip.img * (2 * p.h) + 2 * gy + (dd >> 1)) * (2 * p.w) +
+                                      2 * gx + (dd & 1);
+                            } else {
+                                pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
+                            }
+                            if (p.y) {
+                                uint4 *dst = reinterpret_cast<uint4 *>(p.y + pix * p.cout + o);
+                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            }
+                            if (p.y_f32) {
+                                float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + o);
+                                dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                                dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                                dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+                                dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+                            }
+                        }
+                        if (MODE == kPool) {
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const uint32_t a1 = __shfl_xor_sync(0xffffffffu, pk[i], 1);
+                                const uint32_t a2 = __shfl_xor_sync(0xffffffffu, pk[i], 16);
+                                const uint32_t a3 = __shfl_xor_sync(0xffffffffu, pk[i], 17);
+                                pk[i] = hmax4(pk[i], a1, a2, a3);
+                            }
+                            if (valid && (lane & 17) == 0) {
+                                const int64_t pp =
+                                    ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
+                                uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
+                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            }
+                        }
                     }
                 }
                 if (MODE == kHead && valid) {
@@ -605,7 +597,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         const size_t nk = (size_t)p.kxs * p.nq;
         p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
         res_bytes = p.resident ? nk * p.b_blk : 0;
-        const size_t fixed = res_bytes + const_bytes + 16384 + 512;
+        const size_t fixed = res_bytes + const_bytes + 512;
         bool fit = false;
         for (int kxps = p.kxs; kxps >= 1 && !fit; kxps = kxps == 1 ? 0 : 1) {
             const size_t stage_bytes = (size_t)kxps * (p.a_bytes + (p.resident ? 0 : p.b_blk));
@@ -631,7 +623,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.off_b = (uint32_t)(stages * p.stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
-    p.off_bar = p.off_pool + 16384;
+    p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = bn;
     pl->chunk = chunk;
