@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
 #pragma unroll
                     for (int h2 = 0; h2 < 2; ++h2) {
                         const int n = n0 + h2 * 16;
+                        if (n >= p.n_total) break;  // uniform (n_total may be 16 mod 32)
                         float v[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i)
