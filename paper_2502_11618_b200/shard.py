@@ -1,0 +1,155 @@
+"""Point-sharded multi-GPU rendering.
+
+The cell-major scan is split into contiguous, point-balanced shards, one per
+rank (the reference's worker split, render.py:69-81, across GPUs instead of
+threads).  Per frame:
+
+  every rank : cull its shard (its own occupied cells), build the tile work
+               list, pass 1 into a local minz
+  collective : all-reduce MIN of minz -- u64 bit patterns of positive f64
+               depths order like the doubles, and like int64 (< 2^63)
+  every rank : pass 2 against the GLOBAL minz into local packed accumulators
+  collective : reduce SUM of the accumulators to the frame's root
+               (root = frame index mod world size, so consecutive frames'
+               filter + U-Net run on different GPUs)
+  root       : assemble + depth filter + U-Net input + U-Net
+  others     : reset their pass buffers for the next frame
+
+Min and integer addition are order-free, so the frame is bit-identical to the
+single-GPU frame for any shard count.  The collectives are torch.distributed
+(NCCL over NVLink on the GPU box; gloo in the CPU tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .filtering import FilterParams
+from .frame import RenderParams
+from .geometry import extract_frustum
+from .grid import DeviceScene
+
+
+def shard_bounds(n_points: int, rank: int, world: int):
+    """[start, end) of rank's contiguous, point-balanced share."""
+    start = (n_points * rank) // world
+    end = (n_points * (rank + 1)) // world
+    return start, end
+
+
+def shard_cell_offsets(cell_offsets, start: int, end: int):
+    """Cell offsets of the sub-array [start, end) (same cell ids, clamped)."""
+    return (cell_offsets.clamp(min=start, max=end) - start).contiguous()
+
+
+def merge_minz(minz_bits, group=None):
+    """All-reduce MIN of per-shard pass-1 minima (int64 view of the f64 bits)."""
+    import torch.distributed as dist
+
+    dist.all_reduce(minz_bits, op=dist.ReduceOp.MIN, group=group)
+    return minz_bits
+
+
+def merge_accum(accum, root: int, group=None):
+    """Reduce SUM of the packed accumulators to ``root`` (two's complement int64
+    addition == u64 addition, so the packed {r | g<<32, b | count<<32} halves
+    add exactly while the packed bound holds)."""
+    import torch.distributed as dist
+
+    dist.reduce(accum, dst=root, op=dist.ReduceOp.SUM, group=group)
+    return accum
+
+
+class ShardedRenderer:
+    """FrameRenderer over one shard of the scan, merged across ranks."""
+
+    def __init__(self, grid, width: int, height: int, rank: int, world: int,
+                 render_params: RenderParams | None = None,
+                 filter_params: FilterParams | None = None, unet=None, group=None):
+        import torch
+
+        from .render import FrameBuffers
+
+        self.rank, self.world, self.group = rank, world, group
+        self.device = _lib.device()
+        self.rp = render_params or RenderParams()
+        self.fp = filter_params or FilterParams()
+        self.width, self.height = int(width), int(height)
+        full = grid.scene()
+        start, end = shard_bounds(full.n_points, rank, world)
+        offs = shard_cell_offsets(grid._device_field("cell_offsets", np.int64), start, end)
+        self.scene = DeviceScene(full.positions[start:end], full.colors[start:end], offs,
+                                 grid.origin, grid.cell_size, grid.dims)
+        self.bufs = FrameBuffers(width, height, self.device)
+        h, w, dev = self.height, self.width, self.device
+        self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
+        self.fdepth = torch.empty((h, w), dtype=torch.float32, device=dev)
+        self.falpha = torch.empty((h, w), dtype=torch.uint8, device=dev)
+        self.pyramid = torch.empty(int(_lib.load().ls_pyramid_floats(h, w, self.fp.levels_n)),
+                                   dtype=torch.float32, device=dev)
+        self.unet = unet
+        self.unet_in = self.rgb_out = None
+        if unet is not None:
+            uh = (h + unet.divisor - 1) // unet.divisor * unet.divisor
+            self.unet_in = torch.zeros((1, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
+            self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
+        self.frame_index = 0
+
+    @property
+    def launches_per_frame(self) -> int:
+        # cull, work list, pass 1, pass 2 on every rank; finish + filter + U-Net
+        # on the root (1/world of the frames)
+        n = 4 + (1 + self.fp.levels_n + (self.unet.launches if self.unet else 0)) / self.world
+        return int(round(n))
+
+    def enqueue(self, camera, events=None) -> None:
+        """Enqueue one frame (this rank's share) on the current stream."""
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        ev = events or [None] * 5
+        root = self.frame_index % self.world
+        self.frame_index += 1
+        cam = _lib.make_camera(camera)
+        sc = self.scene
+        bits = sc.cull_bits(extract_frustum(camera).planes).data_ptr()
+        tl, tc = sc.worklist()
+        if ev[0] is not None:
+            ev[0].record()
+        _lib.check(lib.ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
+                                      self.bufs.minz.data_ptr(), st), "frame_pass1")
+        merge_minz(self.bufs.minz, self.group)
+        if ev[1] is not None:
+            ev[1].record()
+        _lib.check(lib.ls_frame_pass2(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
+                                      float(self.rp.zbuffer_epsilon_rel), self.bufs.minz.data_ptr(),
+                                      self.bufs.accum.data_ptr(), st), "frame_pass2")
+        merge_accum(self.bufs.accum, root, self.group)
+        if ev[2] is not None:
+            ev[2].record()
+        if self.rank == root:
+            b = self.bufs
+            _lib.check(lib.ls_frame_finish(
+                b.minz.data_ptr(), b.accum.data_ptr(), b.width, b.height,
+                _lib.make_filter(self.fp), b.rgb.data_ptr(), b.depth.data_ptr(),
+                b.alpha.data_ptr(), self.frgb.data_ptr(), self.fdepth.data_ptr(),
+                self.falpha.data_ptr(), None, _lib.ptr(None if self.unet_in is None
+                                                       else self.unet_in[0]),
+                0 if self.unet_in is None else int(self.unet_in.shape[1]),
+                0 if self.unet_in is None else int(self.unet_in.shape[3]), 0.1,
+                self.pyramid.data_ptr(), b.flags.data_ptr(), st), "frame_finish")
+            if ev[3] is not None:
+                ev[3].record()
+            if self.unet is not None:
+                self.unet.forward(self.unet_in, self.rgb_out)
+        else:
+            self.bufs.minz.fill_(_lib.INF_BITS)
+            self.bufs.accum.zero_()
+            if ev[3] is not None:
+                ev[3].record()
+        if events is not None:
+            events[-1].record()
+
+    def check_flags(self) -> None:
+        if int(self.bufs.flags.item()):
+            raise RuntimeError("packed accumulator bound exceeded")

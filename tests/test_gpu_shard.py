@@ -1,0 +1,111 @@
+"""Sharded rendering on the GPU (one device): every shard's cull + passes run
+through the real kernels and are merged on-device; the merged frame must be
+bit-identical to the unsharded frame for any shard count.
+The multi-rank collectives themselves are covered by tests/test_shard_gloo.py."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import random_cloud, random_view
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _gpu(cuda_ready):
+    return cuda_ready
+
+
+def _frame_setup(n=400_000, seed=3):
+    from lidarsplat import CameraModel, build_grid
+
+    rng = np.random.default_rng(seed)
+    cloud = random_cloud(rng, n, extent=10.0, offset=-5.0)
+    cam0 = random_view(rng, cloud)
+    cam = CameraModel.unchecked(300.0, 300.0, 160.0, 120.0, 320, 240, cam0.world_to_camera)
+    return cloud, cam, build_grid(cloud, 1.0)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_virtual_shards_bit_identical(world):
+    import torch
+
+    from lidarsplat import _lib
+    from lidarsplat.geometry import extract_frustum
+    from lidarsplat.grid import DeviceScene
+    from lidarsplat.render import FrameBuffers, project_scene
+    from lidarsplat.shard import shard_bounds, shard_cell_offsets
+
+    cloud, cam, grid = _frame_setup()
+    dev = torch.device("cuda")
+    full = grid.scene()
+    ref = FrameBuffers(cam.width, cam.height, dev)
+    project_scene(full, cam, 0.01, ref)
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    c = _lib.make_camera(cam)
+    scenes, bufs = [], []
+    for r in range(world):
+        s, e = shard_bounds(full.n_points, r, world)
+        offs = shard_cell_offsets(grid._device_field("cell_offsets", np.int64), s, e)
+        sc = DeviceScene(full.positions[s:e], full.colors[s:e], offs, grid.origin,
+                         grid.cell_size, grid.dims)
+        scenes.append(sc)
+        b = FrameBuffers(cam.width, cam.height, dev)
+        bufs.append(b)
+        sc.cull_bits(extract_frustum(cam).planes)
+        tl, tc = sc.worklist()
+        _lib.check(lib.ls_frame_pass1(sc.struct, sc.keep_bits.data_ptr(), tl.data_ptr(),
+                                      tc.data_ptr(), c, b.minz.data_ptr(), st), "pass1")
+    gmin = torch.stack([b.minz for b in bufs]).min(0).values
+    for sc, b in zip(scenes, bufs):
+        b.minz.copy_(gmin)
+        sc.cull_bits(extract_frustum(cam).planes)
+        tl, tc = sc.worklist()
+        _lib.check(lib.ls_frame_pass2(sc.struct, sc.keep_bits.data_ptr(), tl.data_ptr(),
+                                      tc.data_ptr(), c, 0.01, b.minz.data_ptr(),
+                                      b.accum.data_ptr(), st), "pass2")
+    root = bufs[world - 1]
+    root.accum.copy_(torch.stack([b.accum for b in bufs]).sum(0))
+    _lib.check(lib.ls_frame_finish(root.minz.data_ptr(), root.accum.data_ptr(), cam.width,
+                                   cam.height, None, root.rgb.data_ptr(), root.depth.data_ptr(),
+                                   root.alpha.data_ptr(), None, None, None, None, None, 0, 0, 0.1,
+                                   None, root.flags.data_ptr(), st), "finish")
+    torch.cuda.synchronize()
+    assert torch.equal(root.rgb, ref.rgb)
+    assert torch.equal(root.depth, ref.depth)
+    assert torch.equal(root.alpha, ref.alpha)
+
+
+def test_sharded_renderer_single_rank_group():
+    """ShardedRenderer wiring (cull -> pass 1 -> all-reduce -> pass 2 -> reduce
+    -> finish) in a 1-rank NCCL group matches FrameRenderer."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from lidarsplat.engine import FrameRenderer
+    from lidarsplat.shard import ShardedRenderer
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        cloud, cam, grid = _frame_setup(seed=5)
+        a = ShardedRenderer(grid, cam.width, cam.height, 0, 1)
+        b = FrameRenderer(grid, cam.width, cam.height)
+        for _ in range(2):
+            a.enqueue(cam)
+            b.enqueue(cam)
+        torch.cuda.synchronize()
+        assert torch.equal(a.frgb, b.frgb) and torch.equal(a.falpha, b.falpha)
+        assert torch.equal(a.fdepth, b.fdepth)
+    finally:
+        dist.destroy_process_group()
