@@ -43,8 +43,8 @@ typedef struct ls_camera {
 /* Device-resident scan: the grid's cell-major arrays (grid.py:25-41) plus the
  * per-scan tile index that lets the frame passes skip culled cells. */
 typedef struct ls_scene {
-    const float *d_positions;    /* (n_points,3) f32, cell-major (sorted_positions) */
-    const uint8_t *d_colors;     /* (n_points,3) u8, cell-major (sorted_colors)    */
+    const float *d_positions;    /* (n_points,3) f32, cell-major, 16 B aligned       */
+    const uint8_t *d_colors;     /* (n_points,3) u8, cell-major, 4 B aligned         */
     int64_t n_points;
     const int64_t *d_occ_cells;  /* (n_occ,) ascending occupied cell ids             */
     const int64_t *d_occ_offsets;/* (n_occ+1,) point offset of each occupied cell    */

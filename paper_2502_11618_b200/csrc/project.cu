@@ -468,6 +468,10 @@ int ls_scene_tile_index(const int64_t *d_occ_offsets, int64_t n_occ, int64_t n_p
 
 static bool scene_ok(const ls_scene *scene, const uint32_t *d_list) {
     if (!scene || scene->n_points < 0 || scene->n_points >= (int64_t(1) << 38)) return false;
+    // the warp-tile passes load xyz as 3 x 16 B and rgb as 3 x 4 B per 4 points
+    if ((reinterpret_cast<uintptr_t>(scene->d_positions) & 15) ||
+        (reinterpret_cast<uintptr_t>(scene->d_colors) & 3))
+        return false;
     if (d_list && (!scene->d_tile_c0 || !scene->d_tile_c1 || !scene->d_occ_offsets)) return false;
     return true;
 }

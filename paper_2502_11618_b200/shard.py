@@ -32,10 +32,20 @@ from .grid import DeviceScene
 
 
 def shard_bounds(n_points: int, rank: int, world: int):
-    """[start, end) of rank's contiguous, point-balanced share."""
-    start = (n_points * rank) // world
-    end = (n_points * (rank + 1)) // world
-    return start, end
+    """[start, end) of rank's contiguous, point-balanced share; interior
+    boundaries fall on multiples of LS_TILE_POINTS, so every shard's arrays
+    keep the 16 B (xyz) / 4 B (rgb) alignment of the vectorised frame passes
+    and its warp tiles coincide with the global ones."""
+    t = _lib.LS_TILE_POINTS
+
+    def cut(r):
+        if r <= 0:
+            return 0
+        if r >= world:
+            return n_points
+        return min(n_points, ((n_points * r) // world + t // 2) // t * t)
+
+    return cut(rank), cut(rank + 1)
 
 
 def shard_cell_offsets(cell_offsets, start: int, end: int):
