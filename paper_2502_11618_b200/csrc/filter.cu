@@ -347,16 +347,25 @@ __global__ void __launch_bounds__(256) k_filter_step(
                         const float dn =
                             dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear)))
                                       : 0.0f;
-                        __nv_bfloat16 *o = unet_in + p * unet_c;
                         __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
                         __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
                         __nv_bfloat162 v45 = __floats2bfloat162_rn((float)a, 0.0f);
-                        __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
-                        __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(o);
-                        o2[0] = v01;
-                        o2[1] = v23;
-                        o2[2] = v45;
-                        for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
+                        const uint4 q0 = make_uint4(*reinterpret_cast<uint32_t *>(&v01),
+                                                    *reinterpret_cast<uint32_t *>(&v23),
+                                                    *reinterpret_cast<uint32_t *>(&v45), 0u);
+                        if ((unet_c & 7) == 0) {
+                            // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
+                            uint4 *o4 = reinterpret_cast<uint4 *>(unet_in + p * unet_c);
+                            o4[0] = q0;
+                            for (int c = 1; c < unet_c / 8; ++c) o4[c] = make_uint4(0u, 0u, 0u, 0u);
+                        } else {
+                            __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(unet_in + p * unet_c);
+                            const __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
+                            o2[0] = v01;
+                            o2[1] = v23;
+                            o2[2] = v45;
+                            for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
+                        }
                     }
                 }
             }
