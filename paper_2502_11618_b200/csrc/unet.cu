@@ -5,30 +5,24 @@
 // transposed conv).
 //
 // GEMM view of one layer:  D[M = pixels][N = out channels] = A[M][K] * B[N][K]^T
-//   A : im2col of the NHWC bf16 input, never materialised; the decoder's
-//       [up, skip] concat is two tensor maps walked in K order.
+//   A : im2col of the NHWC bf16 input, never materialised: TMA boxes of the
+//       input whose out-of-bounds zero fill is the conv's "same" padding; the
+//       decoder's [up, skip] concat is two tensor maps walked in K order.
 //   B : the weights, K-major, layout [tap][n][c] with tap = kx*3 + ky.
-//
-// Halo tiles with a padded row pitch.  A work item is R image rows x 16
-// columns.  For every channel chunk ONE TMA box of (R+2) rows x 18 columns of
-// the input (TMA's out-of-bounds zero fill = the conv's zero padding) lands in
-// shared memory as a K-major swizzled tile whose smem row r is the input pixel
-// (r / 18, r % 18) of the halo window.  The GEMM rows use the same indexing
-// (output pixel (r / 18, r % 18); columns 16 and 17 are junk and discarded), so
-// tap (ky, kx) is just the descriptor start moved by ky*18 + kx rows -- all 9
-// taps read one box.  This relies on the tensor core applying the swizzle on
-// absolute shared-memory address bits (measured: scripts/umma_shift_test.cu --
-// every row shift 0..8 is exact with base_offset 0, for 32/64/128 B swizzle).
-// R = 7*MT rows, so the item is MT blocks of 128 GEMM rows (126 used).
-// The 2x2 transposed conv has no halo: pitch 16, R = 8*MT, one tap.
 //
 // Kernel structure (persistent, warp-specialised, one CTA per SM):
 //   warp 0 lane 0 : TMA producer over a STAGES-deep shared-memory ring
 //   warp 1 lane 0 : tcgen05.mma issuer (descriptors precomputed: per MMA only
-//                   the 14-bit start-address field moves)
-//   warps 2..     : kEpiGroups epilogue warpgroups, each draining a different
+//                   the 14-bit start-address field moves, by constant offsets)
+//   warps 2..     : kEpiGroups epilogue warpgroups; each drains a different
 //                   work item (4 warps = the 4 TMEM lane quarters)
-// TMEM holds kAcc items' worth of accumulators, so the MMA warp runs ahead.
+// A work item is MT x 128 output pixels (MT sub-tiles of 8 rows x 16 columns
+// stacked vertically) times BN output columns; TMEM holds kAcc items' worth of
+// accumulators so the MMA warp runs ahead of the epilogues.
+// Halo reuse: for each channel chunk one TMA box of (8*MT + 2) rows x 16
+// columns per kx serves all three ky taps and all MT sub-tiles -- tap ky /
+// sub-tile u is the same smem box offset by (u*8 + ky)*16 rows, i.e. whole
+// 8-row swizzle atoms, so only the descriptor start moves.
 // Small weight tensors (<= kResidentMax, one column tile) stay resident in
 // shared memory for the whole CTA; otherwise weight boxes stream with A.
 #include <cuda.h>
@@ -46,7 +40,7 @@ namespace unet {
 
 using namespace ls::umma;
 
-constexpr int kTW = 16;  // output columns per item
+constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
 constexpr size_t kSmemBudget = 222 * 1024;
 
@@ -56,7 +50,7 @@ struct ConvParamsP {
     int batch, h, w;
     int tiles_x, tiles_y, n_tiles_m, n_tiles_n, n_items;
     int c0, c1, ctot, nq0, nq;
-    int kxps;               // kx taps per pipeline stage (1 or 3; 1 for transposed)
+    int kxs, kxps, pad;     // kx taps, kx taps per pipeline stage (1 or kxs)
     int n_total, cout, act;
     float alpha;
     const float *scale, *shift;
@@ -68,31 +62,23 @@ struct ConvParamsP {
     float *head_out;
     int resident;           // weights resident in smem
     int stages;
-    uint32_t a_bytes;       // A box footprint (1024-aligned)
+    uint32_t a_bytes;       // one A box footprint (1024-aligned)
     uint32_t a_tx;          // TMA bytes of one A box
-    uint32_t b_tap;         // bytes of one tap's (BN x chunk) weight block
+    uint32_t b_blk;         // bytes of one (3 x BN x chunk) weight block
     uint32_t stage_bytes;
     uint32_t off_b;         // resident weights
     uint32_t off_const;     // scale[n_total], shift[n_total], head_w (f32)
-    uint32_t off_stage;     // pool staging (per epilogue group)
-    uint32_t stage_grp;     // bytes of one group's pool staging
+    uint32_t off_pool;      // (unused: pooling is done with warp shuffles)
     uint32_t off_bar;       // barriers
 };
 
-template <int BN, int CHUNK, int MODE>
+template <int BN, int CHUNK>
 struct CfgP {
     static constexpr uint32_t kRow = CHUNK * 2;  // bytes per operand row
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
-    static constexpr bool kConv3 = MODE != kTransposed;
-    static constexpr int kTaps = kConv3 ? 9 : 1;
-    static constexpr int kKys = kConv3 ? 3 : 1;
-    static constexpr int kPitch = kConv3 ? 18 : 16;              // smem rows per image row
-    static constexpr int kMT = BN <= 32 ? 4 : (BN <= 64 ? 2 : 1);  // 128-row blocks per item
-    // image rows per item (even when pooling so 2x2 windows never straddle items)
-    static constexpr int kR = kConv3 ? ((MODE == kPool && (7 * kMT) % 2) ? 7 * kMT - 1 : 7 * kMT)
-                                     : 8 * kMT;
-    static constexpr int kItemCols = kMT * BN;                   // TMEM columns per item
+    static constexpr int kMT = BN <= 32 ? 4 : (BN <= 64 ? 2 : 1);      // sub-tiles per item
+    static constexpr int kItemCols = kMT * BN;                          // TMEM columns per item
     static constexpr int kAcc = 512 / kItemCols >= 4 ? 4 : 512 / kItemCols;
     static constexpr int kEpiGroups = kAcc >= 4 ? 3 : (kAcc >= 3 ? 2 : 1);
     static constexpr int kThreads = 64 + 128 * kEpiGroups;
@@ -100,10 +86,11 @@ struct CfgP {
                                      (kAcc * kItemCols <= 64 ? 64 :
                                      (kAcc * kItemCols <= 128 ? 128 :
                                      (kAcc * kItemCols <= 256 ? 256 : 512)));
+    static constexpr int kGroups = BN / 16;
 };
 
-template <int BN, int CHUNK, int MODE>
-constexpr int threads_for() { return CfgP<BN, CHUNK, MODE>::kThreads; }
+template <int BN, int CHUNK>
+constexpr int threads_for() { return CfgP<BN, CHUNK>::kThreads; }
 
 __device__ __forceinline__ float apply_act(float v, int act, float alpha) {
     if (act == LS_ACT_RELU) return v > 0.0f ? v : 0.0f;
@@ -155,7 +142,7 @@ struct ItemPos {
 };
 
 __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, float r_nt, float r_tpi,
-                                            float r_tx, int rows) {
+                                            float r_tx, int tile_h) {
     ItemPos ip;
     const int mt = fdiv(item, p.n_tiles_n, r_nt);
     ip.nt = item - mt * p.n_tiles_n;
@@ -163,17 +150,19 @@ __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, floa
     ip.img = fdiv(mt, tpi, r_tpi);
     const int r = mt - ip.img * tpi;
     const int ty = fdiv(r, p.tiles_x, r_tx);
-    ip.y0 = ty * rows;
+    ip.y0 = ty * tile_h;
     ip.x0 = (r - ty * p.tiles_x) * kTW;
     return ip;
 }
 
 template <int BN, int CHUNK, int MODE>
-__global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
+__global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
-    using C = CfgP<BN, CHUNK, MODE>;
-    constexpr int MT = C::kMT, KYS = C::kKys, P = C::kPitch, R = C::kR;
+    using C = CfgP<BN, CHUNK>;
+    constexpr int KYS = MODE == kTransposed ? 1 : 3;
+    constexpr int MT = C::kMT;
+    constexpr int kTileH = kTH * MT;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align inside the shared window (keeps the shared address space visible)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -192,8 +181,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
     const float r_nt = 1.0f / (float)p.n_tiles_n;
     const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
     const float r_tx = 1.0f / (float)p.tiles_x;
-    const int kxs = C::kTaps / KYS;
-    const int n_kg = kxs / p.kxps;  // stages per channel chunk
+    const int n_kg = p.kxs / p.kxps;  // stages per channel chunk
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0) {
@@ -235,17 +223,18 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
         if (lane == 0) {
             // ------------------------------ TMA producer ------------------------------
             if (p.resident) {
-                // per chunk q: one box {chunk, BN, taps} -> [tap][BN][chunk]
-                mbar_expect_tx(bres, (uint32_t)(p.nq * C::kTaps) * p.b_tap);
-                for (int q = 0; q < p.nq; ++q) {
-                    const bool second = q >= p.nq0;
-                    const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
-                    tma_load_3d(smem + p.off_b + q * C::kTaps * p.b_tap, &mB, kc, 0, 0, bres);
-                }
+                mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk);
+                for (int q = 0; q < p.nq; ++q)
+                    for (int kx = 0; kx < p.kxs; ++kx) {
+                        const bool second = q >= p.nq0;
+                        const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
+                        tma_load_3d(smem + p.off_b + (q * p.kxs + kx) * p.b_blk, &mB, kc, 0,
+                                    kx * KYS, bres);
+                    }
             }
             uint32_t it = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-                const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, R);
+                const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
                 for (int q = 0; q < p.nq; ++q) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
@@ -255,13 +244,15 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
                         const uint32_t ph = (it / (uint32_t)S) & 1u;
                         mbar_wait(empty + s, ph ^ 1u);
                         uint8_t *st = smem + (size_t)s * p.stage_bytes;
-                        const uint32_t btx = p.resident ? 0u : (uint32_t)(p.kxps * KYS) * p.b_tap;
-                        mbar_expect_tx(full + s, p.a_tx + btx);
-                        tma_load_4d(st, ma, c, ip.x0 - (C::kConv3 ? 1 : 0),
-                                    ip.y0 - (C::kConv3 ? 1 : 0), ip.img, full + s);
-                        if (!p.resident)
-                            tma_load_3d(st + p.a_bytes, &mB, (second ? p.c0 : 0) + c, ip.nt * BN,
-                                        kg * p.kxps * KYS, full + s);
+                        mbar_expect_tx(full + s, p.kxps * (p.a_tx + (p.resident ? 0u : p.b_blk)));
+                        for (int k = 0; k < p.kxps; ++k) {
+                            const int kx = kg * p.kxps + k;
+                            tma_load_4d(st + k * p.a_bytes, ma, c, ip.x0 + kx - p.pad,
+                                        ip.y0 - p.pad, ip.img, full + s);
+                            if (!p.resident)
+                                tma_load_3d(st + p.kxps * p.a_bytes + k * p.b_blk, &mB,
+                                            (second ? p.c0 : 0) + c, ip.nt * BN, kx * KYS, full + s);
+                        }
                     }
                 }
             }
@@ -273,7 +264,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
             const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
             const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
             if (p.resident) mbar_wait(bres, 0);
-            const uint32_t b_tap16 = p.b_tap >> 4;
+            const uint32_t a_box16 = p.a_bytes >> 4, b_blk16 = p.b_blk >> 4;
             uint32_t it = 0, acc = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
                 const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
@@ -288,14 +279,12 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
                         fence_after_sync();
                         const uint32_t st = sbase + (uint32_t)s * p.stage_bytes;
                         const uint32_t a_lo = dlo + (st >> 4);
-                        // B row block of (kx, ky): resident [q][tap][BN], streamed [tap_in_stage][BN]
                         const uint32_t b_lo =
-                            dlo + ((p.resident ? sbase + p.off_b + (uint32_t)(q * C::kTaps) * p.b_tap +
-                                                     (uint32_t)(kg * p.kxps * KYS) * p.b_tap
-                                               : st + p.a_bytes) >>
+                            dlo + ((p.resident
+                                        ? sbase + p.off_b + (uint32_t)(q * p.kxs + kg * p.kxps) * p.b_blk
+                                        : st + p.kxps * p.a_bytes) >>
                                    4);
                         for (int k = 0; k < p.kxps; ++k) {
-                            const int kx = kg * p.kxps + k;
 #pragma unroll
                             for (int u = 0; u < MT; ++u) {
 #pragma unroll
@@ -303,9 +292,8 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
 #pragma unroll
                                     for (int j = 0; j < CHUNK / 16; ++j) {
                                         const uint32_t ao =
-                                            ((u * 128 + ky * P + kx) * C::kRow + 32 * j) / 16;
-                                        const uint32_t bo =
-                                            (uint32_t)(k * KYS + ky) * b_tap16 + (32 * j) / 16;
+                                            k * a_box16 + ((u * kTH + ky) * kTW * C::kRow + 32 * j) / 16;
+                                        const uint32_t bo = k * b_blk16 + (ky * BN * C::kRow + 32 * j) / 16;
                                         mma_bf16(d0 + u * BN, ((uint64_t)dhi << 32) | (a_lo + ao),
                                                  ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
                                                  (q | kg | k | ky | j) != 0 ? 1u : 0u);
@@ -321,60 +309,54 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
         }
     } else {
         // --------------------------------- epilogue ---------------------------------
-        // GEMM row r = u*128 + m of an item is output pixel (r / P, r % P);
-        // columns >= 16 and rows >= R are junk and discarded.
+        // Pixel m = quarter*32 + lane of a sub-tile is (row m/16, col m%16): the
+        // 2x2 max-pool partners of a lane are lanes ^1 and ^16 of the SAME warp,
+        // so pooling is two shuffle-max steps (no shared memory, no barriers).
         const int eg = (warp - 2) >> 2;          // warpgroup -> every kEpiGroups-th item
         const int quarter = warp & 3;            // TMEM lane quarter this warp may access
         const int m = quarter * 32 + lane;
-        const int et = threadIdx.x - 64 - 128 * eg;  // 0..127 within the warpgroup
-        const uint32_t sstage = sbase + p.off_stage + (uint32_t)eg * p.stage_grp;
+        const int tx = m % kTW, ty = m / kTW;
         uint32_t acc = (uint32_t)eg;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
-            const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, R);
+            const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             const uint32_t tbase = tmem + ab * C::kItemCols + ((uint32_t)(quarter * 32) << 16);
-            float hacc[MT][4];
-#pragma unroll
-            for (int u = 0; u < MT; ++u)
-#pragma unroll
-                for (int j2 = 0; j2 < 4; ++j2) hacc[u][j2] = 0.0f;
+            const int gx = ip.x0 + tx;
 #pragma unroll 1
-            for (int g = 0; g < BN / 32; ++g) {
-                const int n0 = ip.nt * BN + g * 32;
-                if (n0 >= p.n_total) break;  // uniform
+            for (int u = 0; u < MT; ++u) {
+                const int gy = ip.y0 + u * kTH + ty;
+                const bool valid = gx < p.w && gy < p.h;
+                float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll 1
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    const int n = n0 + h2 * 16;
-                    if (n >= p.n_total) break;  // uniform (n_total may be 16 mod 32)
+                for (int g = 0; g < BN / 32; ++g) {
+                    const int n0 = ip.nt * BN + g * 32;
+                    if (n0 >= p.n_total) break;  // uniform
+                    uint32_t rr[32];
+                    tmem_ld32(tbase + (uint32_t)(u * BN + g * 32), rr);
+                    if (u + 1 == MT && (g + 1 == BN / 32 || n0 + 32 >= p.n_total)) {
+                        // item fully read -> hand the TMEM buffer back early
+                        fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(tempty + ab);
+                    }
 #pragma unroll
-                    for (int u = 0; u < MT; ++u) {
-                        const int r = u * 128 + m;
-                        const int yy = r / P, xx = r - yy * P;
-                        const int gy = ip.y0 + yy, gx = ip.x0 + xx;
-                        const bool valid = xx < kTW && yy < R && gx < p.w && gy < p.h;
-                        uint32_t rr[16];
-                        tmem_ld16(tbase + (uint32_t)(u * BN + g * 32 + h2 * 16), rr);
-                        if (u + 1 == MT && (h2 == 1 || n + 16 >= p.n_total) &&
-                            (g + 1 == BN / 32 || n0 + 32 >= p.n_total)) {
-                            // item fully read -> hand the TMEM buffer back early
-                            fence_before_sync();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive(tempty + ab);
-                        }
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int n = n0 + h2 * 16;
+                        if (n >= p.n_total) break;  // uniform (n_total may be 16 mod 32)
                         float v[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i)
-                            v[i] = apply_act(fmaf(__uint_as_float(rr[i]), s_scale[n + i],
+                            v[i] = apply_act(fmaf(__uint_as_float(rr[h2 * 16 + i]), s_scale[n + i],
                                                   s_shift[n + i]),
                                              p.act, p.alpha);
                         if (MODE == kHead) {
                             for (int j2 = 0; j2 < p.head_c; ++j2) {
 #pragma unroll
                                 for (int i = 0; i < 16; ++i)
-                                    hacc[u][j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[u][j2]);
+                                    hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
                             }
                             if (!p.y && !p.y_f32) continue;  // head input not materialised
                         }
@@ -406,52 +388,27 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MODE>()) k_conv_p(
                             }
                         }
                         if (MODE == kPool) {
-                            // stage this 16-channel slice of every GEMM row of the item
-                            st_shared_v4(sstage + (uint32_t)r * 32u, make_uint4(pk[0], pk[1], pk[2], pk[3]));
-                            st_shared_v4(sstage + (uint32_t)r * 32u + 16u,
-                                         make_uint4(pk[4], pk[5], pk[6], pk[7]));
-                        }
-                    }
-                    if (MODE == kPool) {
-                        named_bar_sync(1 + eg, 128);
-                        // (R/2) x 8 pooled outputs per item
-                        for (int o = et; o < (R / 2) * (kTW / 2); o += 128) {
-                            const int py = o >> 3, px = o & 7;
-                            const int r00 = (2 * py) * P + 2 * px;
-                            const int gy = ip.y0 + 2 * py, gx = ip.x0 + 2 * px;
-                            if (gx >= p.w || gy >= p.h) continue;
-                            uint4 o2[2];
 #pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const uint4 a0 = ld_shared_v4(sstage + (uint32_t)r00 * 32u + hh * 16);
-                                const uint4 a1 = ld_shared_v4(sstage + (uint32_t)(r00 + 1) * 32u + hh * 16);
-                                const uint4 a2 = ld_shared_v4(sstage + (uint32_t)(r00 + P) * 32u + hh * 16);
-                                const uint4 a3 = ld_shared_v4(sstage + (uint32_t)(r00 + P + 1) * 32u + hh * 16);
-                                o2[hh] = make_uint4(hmax4(a0.x, a1.x, a2.x, a3.x),
-                                                    hmax4(a0.y, a1.y, a2.y, a3.y),
-                                                    hmax4(a0.z, a1.z, a2.z, a3.z),
-                                                    hmax4(a0.w, a1.w, a2.w, a3.w));
+                            for (int i = 0; i < 8; ++i) {
+                                const uint32_t a1 = __shfl_xor_sync(0xffffffffu, pk[i], 1);
+                                const uint32_t a2 = __shfl_xor_sync(0xffffffffu, pk[i], 16);
+                                const uint32_t a3 = __shfl_xor_sync(0xffffffffu, pk[i], 17);
+                                pk[i] = hmax4(pk[i], a1, a2, a3);
                             }
-                            const int64_t pp =
-                                ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
-                            uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
-                            dst[0] = o2[0];
-                            dst[1] = o2[1];
+                            if (valid && (lane & 17) == 0) {
+                                const int64_t pp =
+                                    ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
+                                uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
+                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            }
                         }
-                        named_bar_sync(1 + eg, 128);
                     }
                 }
-            }
-            if (MODE == kHead) {
-#pragma unroll
-                for (int u = 0; u < MT; ++u) {
-                    const int r = u * 128 + m;
-                    const int yy = r / P, xx = r - yy * P;
-                    const int gy = ip.y0 + yy, gx = ip.x0 + xx;
-                    if (!(xx < kTW && yy < R && gx < p.w && gy < p.h)) continue;
+                if (MODE == kHead && valid) {
                     const int64_t pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
                     for (int j2 = 0; j2 < p.head_c; ++j2) {
-                        const float z = hacc[u][j2] + __ldg(p.head_b + j2);
+                        const float z = hacc[j2] + __ldg(p.head_b + j2);
                         p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
                     }
                 }
@@ -488,28 +445,28 @@ static CUtensorMapSwizzle swizzle_for(int row_bytes) {
                             : (row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
-// activations NHWC bf16, box {chunk, box_w columns, box_h rows, 1}
+// activations NHWC bf16, box {chunk, 16 columns, box_h rows, 1}
 static bool encode_act(CUtensorMap *map, const void *base, int c, int w, int h, int batch,
-                       int chunk, int box_w, int box_h) {
+                       int chunk, int box_h) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
     cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
-    cuuint32_t box[4] = {(cuuint32_t)chunk, (cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+    cuuint32_t box[4] = {(cuuint32_t)chunk, (cuuint32_t)kTW, (cuuint32_t)box_h, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides,
               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(chunk * 2),
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// weights [taps][n_total][ctot], box {chunk, bn, taps_per_box}
+// weights [taps][n_total][ctot], box {chunk, bn, kys}
 static bool encode_wts(CUtensorMap *map, const void *base, int ctot, int n_total, int taps,
-                       int chunk, int bn, int taps_box) {
+                       int chunk, int bn, int kys) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)ctot, (cuuint64_t)n_total, (cuuint64_t)taps};
     cuuint64_t strides[2] = {(cuuint64_t)ctot * 2, (cuuint64_t)n_total * ctot * 2};
-    cuuint32_t box[3] = {(cuuint32_t)chunk, (cuuint32_t)bn, (cuuint32_t)taps_box};
+    cuuint32_t box[3] = {(cuuint32_t)chunk, (cuuint32_t)bn, (cuuint32_t)kys};
     cuuint32_t es[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides,
               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(chunk * 2),
@@ -541,7 +498,7 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = 1;
     }
-    k_conv_p<BN, CHUNK, MODE><<<pl->grid, CfgP<BN, CHUNK, MODE>::kThreads, pl->smem, st>>>(
+    k_conv_p<BN, CHUNK, MODE><<<pl->grid, CfgP<BN, CHUNK>::kThreads, pl->smem, st>>>(
         pl->a0, pl->a1, pl->b, pl->p);
     return (int)cudaGetLastError();
 }
@@ -557,16 +514,6 @@ static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
 }
 
 static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : 1); }
-static int rows_for(int bn, bool conv3, bool pool) {
-    const int mt = mt_for(bn);
-    if (!conv3) return 8 * mt;
-    return (pool && (7 * mt) % 2) ? 7 * mt - 1 : 7 * mt;
-}
-static int epi_groups_for(int bn) {
-    const int item_cols = mt_for(bn) * bn;
-    const int acc = 512 / item_cols >= 4 ? 4 : 512 / item_cols;
-    return acc >= 4 ? 3 : (acc >= 3 ? 2 : 1);
-}
 
 }  // namespace unet
 }  // namespace ls
@@ -611,6 +558,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.c0 = c0;
     p.c1 = c1;
     p.ctot = c0 + c1;
+    p.kxs = ksize == 3 ? 3 : 1;
+    p.pad = ksize == 3 ? 1 : 0;
     p.n_total = n_total;
     p.cout = cout;
     p.act = act;
@@ -624,38 +573,35 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.head_b = d_head_b;
     p.head_c = head_c;
     p.head_out = d_head_out;
-    const bool conv3 = !transposed;
-    const int taps = conv3 ? 9 : 1, kys = conv3 ? 3 : 1, kxs = conv3 ? 3 : 1;
-    const int pitch = conv3 ? 18 : 16;
+    const int kys = p.kxs;
     const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
                                ~size_t(1023);
-    size_t res_bytes = 0, stage_alloc = 0;
+    size_t res_bytes = 0;
     int stages = 0;
-    // Fit >= 3 pipeline stages: first all taps per stage, then one kx per
-    // stage, then a narrower K chunk, then a narrower column tile.
+    // Fit >= 3 pipeline stages: first try whole-chunk stages (all kx boxes in
+    // one stage), then one kx per stage, then a narrower K chunk, then a
+    // narrower column tile.
     for (;;) {
         const int mt = mt_for(bn);
-        const int rows = rows_for(bn, conv3, d_pool != nullptr);
-        const int box_h = conv3 ? rows + 2 : rows;
+        const int box_h = kTH * mt + 2 * p.pad;
         const uint32_t row = (uint32_t)chunk * 2;
         p.tiles_x = (w + kTW - 1) / kTW;
-        p.tiles_y = (h + rows - 1) / rows;
+        p.tiles_y = (h + kTH * mt - 1) / (kTH * mt);
         p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
         p.n_tiles_n = (n_total + bn - 1) / bn;
         p.n_items = p.n_tiles_m * p.n_tiles_n;
         p.nq0 = c0 / chunk;
         p.nq = (c0 + c1) / chunk;
-        p.a_tx = (uint32_t)(pitch * box_h) * row;
+        p.a_tx = (uint32_t)(kTW * box_h) * row;
         p.a_bytes = (p.a_tx + 1023u) & ~1023u;
-        p.b_tap = (uint32_t)bn * row;
-        p.resident = (p.n_tiles_n == 1 && (size_t)p.nq * taps * p.b_tap <= kResidentMax) ? 1 : 0;
-        res_bytes = p.resident ? (size_t)p.nq * taps * p.b_tap : 0;
-        stage_alloc = d_pool ? (size_t)epi_groups_for(bn) * (size_t)(mt * 128) * 32 : 0;
-        const size_t fixed = res_bytes + const_bytes + stage_alloc + 512;
+        p.b_blk = (uint32_t)(kys * bn) * row;
+        const size_t nk = (size_t)p.kxs * p.nq;
+        p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
+        res_bytes = p.resident ? nk * p.b_blk : 0;
+        const size_t fixed = res_bytes + const_bytes + 512;
         bool fit = false;
-        for (int kxps = kxs; kxps >= 1 && !fit; kxps = kxps == 1 ? 0 : 1) {
-            const size_t raw = p.a_bytes + (p.resident ? 0 : (size_t)(kxps * kys) * p.b_tap);
-            const size_t stage_bytes = (raw + 1023) & ~size_t(1023);
+        for (int kxps = p.kxs; kxps >= 1 && !fit; kxps = kxps == 1 ? 0 : 1) {
+            const size_t stage_bytes = (size_t)kxps * (p.a_bytes + (p.resident ? 0 : p.b_blk));
             stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
             if (stages >= 3) {
                 p.kxps = kxps;
@@ -677,9 +623,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.stages = stages;
     p.off_b = (uint32_t)(stages * p.stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
-    p.off_stage = (uint32_t)(p.off_const + const_bytes);
-    p.stage_grp = d_pool ? (uint32_t)(mt_for(bn) * 128 * 32) : 0;
-    p.off_bar = (uint32_t)(p.off_stage + stage_alloc);
+    p.off_pool = (uint32_t)(p.off_const + const_bytes);
+    p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = bn;
     pl->chunk = chunk;
@@ -687,12 +632,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
-    const int box_h = rows_for(bn, conv3, d_pool != nullptr) + (conv3 ? 2 : 0);
-    bool ok = encode_act(&pl->a0, d_x0, c0, w, h, batch, chunk, pitch, box_h);
+    const int box_h = kTH * mt_for(bn) + 2 * p.pad;
+    bool ok = encode_act(&pl->a0, d_x0, c0, w, h, batch, chunk, box_h);
     ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0, w, h, batch, chunk,
-                          pitch, box_h);
-    ok = ok && encode_wts(&pl->b, d_w, p.ctot, n_total, taps, chunk, bn,
-                          p.resident ? taps : p.kxps * kys);
+                          box_h);
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, n_total, p.kxs * kys, chunk, bn, kys);
     if (!ok) {
         delete pl;
         return fail(LS_EINVAL);
