@@ -28,7 +28,7 @@ extern "C" {
 
 #define LS_EINVAL (-22)
 #define LS_TILE_POINTS 128          /* points per warp tile of the frame passes */
-#define LS_PACKED_COUNT_LIMIT 16843009u /* 255*count < 2^32 => packed sums exact */
+#define LS_PACKED_COUNT_LIMIT 65793u /* 255*count < 2^24 => f32 accumulator sums exact */
 
 /* Pinhole camera + pose, values exactly as CameraModel holds them
  * (geometry.py:62-108): rot row-major world->camera, p_c = R p + t. */
@@ -168,22 +168,24 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
  * work list is built first (ls_tile_worklist).
  * d_minz_bits: (H*W) u64, the f64 bit pattern of the running minimum,
  *   must hold +inf (0x7FF0000000000000) on entry.
- * d_accum2: (H*W x 2) u64 packed accumulators {r | g<<32, b | count<<32},
- *   zero on entry.  Exact while no pixel keeps > LS_PACKED_COUNT_LIMIT points;
- *   ls_frame_finish flags a frame where that bound could be exceeded. */
+ * d_accum4: (H*W x 4) f32 accumulators {sum r, sum g, sum b, count}, zero on
+ *   entry, one 16 B vector atomic per kept point.  Integer-valued f32 adds
+ *   are exact and order-free while every field stays < 2^24 (guaranteed while
+ *   no pixel keeps > LS_PACKED_COUNT_LIMIT points); ls_frame_finish flags a
+ *   frame where a field reached 2^24. */
 int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
                      uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                     uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream);
+                     uint64_t *d_minz_bits, float *d_accum4, void *stream);
 
 /* Pass 1 only / pass 2 only of ls_frame_project over an existing work list
  * (d_list NULL = all tiles).  Multi-GPU: an all-reduce MIN of d_minz_bits
- * runs between them, a reduce SUM of d_accum2 after. */
+ * runs between them, a reduce SUM of d_accum4 after. */
 int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
                    void *stream);
 int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                   const uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream);
+                   const uint64_t *d_minz_bits, float *d_accum4, void *stream);
 
 /* Level sizes of the min pyramid (filtering.py:67-83); returns the float
  * count of the workspace ls_frame_finish needs for levels 0..L-1. */
@@ -191,7 +193,7 @@ int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n);
 
 /* Assemble (render.py:146-161) + depth filter (filtering.py:60-147) + U-Net
  * input prep (weights.ts:90-95 normalizeDepth, bridge.ts:37-44 packing).
- *   in:  d_minz_bits, d_accum2 (consumed and reset to +inf / 0 for the next frame)
+ *   in:  d_minz_bits, d_accum4 (consumed and reset to +inf / 0 for the next frame)
  *   out: raw frame d_rgb (H,W,3) f32, d_depth (H,W) f32, d_alpha (H,W) u8
  *        filtered frame d_frgb/d_fdepth/d_falpha (any may be NULL),
  *        d_keep (H,W) u8 mask (may be NULL),
@@ -199,9 +201,9 @@ int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n);
  *          [r,g,b,zNear/max(d,zNear),alpha, 0...] of the FILTERED frame,
  *          rows >= H left untouched (caller zero-fills once).
  *   d_pyramid: ls_pyramid_floats(H,W,L) floats of scratch.
- *   d_flags: 1 int32; bit0 set if a pixel's packed count may have overflowed.
+ *   d_flags: 1 int32; bit0 set if a pixel's accumulator may have lost exactness.
  * filter==NULL skips the filter (raw frame only). */
-int ls_frame_finish(uint64_t *d_minz_bits, uint64_t *d_accum2, int64_t width, int64_t height,
+int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64_t height,
                     const ls_filter_params *filter, float *d_rgb, float *d_depth,
                     uint8_t *d_alpha, float *d_frgb, float *d_fdepth, uint8_t *d_falpha,
                     uint8_t *d_keep, uint16_t *d_unet_in, int64_t unet_h, int32_t unet_c,

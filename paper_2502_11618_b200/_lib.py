@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "liblidarsplat_cuda.so")
 
 LS_EINVAL = -22
 LS_TILE_POINTS = 128
-LS_PACKED_COUNT_LIMIT = 16843009
+LS_PACKED_COUNT_LIMIT = 65793
 INF_BITS = 0x7FF0000000000000
 
 

@@ -163,7 +163,7 @@ struct Levels {
 
 // 32x32 pixel block per CTA, 256 threads, 2x2 pixels per thread.
 __global__ void __launch_bounds__(256) k_assemble_pyramid(
-    unsigned long long *__restrict__ minz, unsigned long long *__restrict__ acc, int64_t H,
+    unsigned long long *__restrict__ minz, float4 *__restrict__ acc, int64_t H,
     int64_t W, Levels lv, int pool_levels, float *__restrict__ rgb, float *__restrict__ depth,
     uint8_t *__restrict__ alpha, int *__restrict__ flags) {
     __shared__ float s1[16][17];
@@ -176,8 +176,9 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     bool overflow = false;
     const int64_t x = bx * 32 + 2 * gx;
     // Issue every load of the thread's 2x2 pixels before any use (4 independent
-    // 16 B minz/accum pairs in flight), then compute, then vector stores.
-    unsigned long long key[2][2], wrg[2][2], wbn[2][2];
+    // 8 B minz + 16 B accum pairs in flight), then compute, then vector stores.
+    unsigned long long key[2][2];
+    float4 a[2][2];
     bool ok[2][2];
 #pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
@@ -187,15 +188,14 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
         ok[dy][1] = y < H && x + 1 < W;
         if (ok[dy][1] && (W & 1) == 0) {
             const ulonglong2 k2 = __ldcs(reinterpret_cast<const ulonglong2 *>(minz + p));
-            const ulonglong4 a4 = *reinterpret_cast<const ulonglong4 *>(acc + 2 * p);
             key[dy][0] = k2.x; key[dy][1] = k2.y;
-            wrg[dy][0] = a4.x; wbn[dy][0] = a4.y; wrg[dy][1] = a4.z; wbn[dy][1] = a4.w;
+            a[dy][0] = acc[p];
+            a[dy][1] = acc[p + 1];
         } else {
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx) {
                 key[dy][dx] = ok[dy][dx] ? minz[p + dx] : kInfBits;
-                wrg[dy][dx] = ok[dy][dx] ? acc[2 * (p + dx)] : 0ull;
-                wbn[dy][dx] = ok[dy][dx] ? acc[2 * (p + dx) + 1] : 0ull;
+                a[dy][dx] = ok[dy][dx] ? acc[p + dx] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
     }
@@ -207,16 +207,18 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
         uint8_t al[2];
 #pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
-            const unsigned long long cnt = wbn[dy][dx] >> 32;
+            // the f32 sums are exact integers while every field stays < 2^24
+            // (any partial sum reaching 2^24 leaves the final field >= 2^24)
+            const float4 f = a[dy][dx];
             d[dx] = 0.0f;
             c[dx][0] = c[dx][1] = c[dx][2] = 0.0f;
             al[dx] = 0;
-            if (cnt > 0) {
-                overflow |= cnt > LS_PACKED_COUNT_LIMIT;
-                const double denom = dmul((double)cnt, 255.0);
-                c[dx][0] = __double2float_rn(ddiv((double)(wrg[dy][dx] & 0xffffffffull), denom));
-                c[dx][1] = __double2float_rn(ddiv((double)(wrg[dy][dx] >> 32), denom));
-                c[dx][2] = __double2float_rn(ddiv((double)(wbn[dy][dx] & 0xffffffffull), denom));
+            if (f.w > 0.0f) {
+                overflow |= fmaxf(fmaxf(f.x, f.y), fmaxf(f.z, f.w)) >= kAccumExactLimit;
+                const double denom = dmul((double)f.w, 255.0);
+                c[dx][0] = __double2float_rn(ddiv((double)f.x, denom));
+                c[dx][1] = __double2float_rn(ddiv((double)f.y, denom));
+                c[dx][2] = __double2float_rn(ddiv((double)f.z, denom));
                 d[dx] = __double2float_rn(__longlong_as_double((long long)key[dy][dx]));
                 al[dx] = 1;
             }
@@ -234,7 +236,8 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
             *reinterpret_cast<uchar2 *>(alpha + p) = make_uchar2(al[0], al[1]);
             // consume-and-reset for the next frame
             *reinterpret_cast<ulonglong2 *>(minz + p) = make_ulonglong2(kInfBits, kInfBits);
-            *reinterpret_cast<ulonglong4 *>(acc + 2 * p) = make_ulonglong4(0ull, 0ull, 0ull, 0ull);
+            acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+            acc[p + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
         } else {
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx) {
@@ -246,8 +249,7 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
                 depth[q] = d[dx];
                 alpha[q] = al[dx];
                 minz[q] = kInfBits;
-                acc[2 * q] = 0ull;
-                acc[2 * q + 1] = 0ull;
+                acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
     }
@@ -499,7 +501,7 @@ int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n) {
     return total;
 }
 
-int ls_frame_finish(uint64_t *d_minz_bits, uint64_t *d_accum2, int64_t width, int64_t height,
+int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64_t height,
                     const ls_filter_params *filter, float *d_rgb, float *d_depth,
                     uint8_t *d_alpha, float *d_frgb, float *d_fdepth, uint8_t *d_falpha,
                     uint8_t *d_keep, uint16_t *d_unet_in, int64_t unet_h, int32_t unet_c,
@@ -520,7 +522,7 @@ int ls_frame_finish(uint64_t *d_minz_bits, uint64_t *d_accum2, int64_t width, in
     dim3 grid((unsigned)((width + 31) / 32), (unsigned)((height + 31) / 32));
     const int in_block = L < 5 ? L : 5;
     k_assemble_pyramid<<<grid, 256, 0, st>>>((unsigned long long *)d_minz_bits,
-                                             (unsigned long long *)d_accum2, height, width, lv,
+                                             reinterpret_cast<float4 *>(d_accum4), height, width, lv,
                                              in_block, d_rgb, d_depth, d_alpha, d_flags);
     LS_LAUNCH_CHECK();
     if (!filter) return 0;

@@ -241,8 +241,11 @@ __device__ __forceinline__ void red_min_u64(unsigned long long *p, unsigned long
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void red_add_u64(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// {r, g, b, 1} into a pixel's f32 accumulator: one 16 B vector reduction.
+__device__ __forceinline__ void red_add_v4f32(float *p, float r, float g, float b) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(r),
+                 "f"(g), "f"(b), "f"(1.0f)
+                 : "memory");
 }
 
 // Iterates the frame's tiles: the work list when culling, every tile otherwise.
@@ -285,7 +288,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ bits,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count,
-                                                     unsigned long long *__restrict__ minz) {
+                                                     unsigned long long *__restrict__ minz, int dbg) {
     const int lane = threadIdx.x & 31;
     for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
         const int64_t tile = e & ~kMixed;
@@ -296,13 +299,13 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
             c1 = __ldg(s.tile_c1 + tile);
         }
         int64_t pix[4];
+        double zc[4];
         unsigned long long key[4];
+        project4(P, cnt, c, pix, zc);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            double zc;
-            pix[k] = k < cnt ? project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc) : -1;
             if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
-            key[k] = (unsigned long long)__double_as_longlong(zc);
+            key[k] = (unsigned long long)__double_as_longlong(zc[k]);
         }
         if (PRECHECK) {
             unsigned long long cur[4];
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
             for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldca(minz + pix[k]) : 0ull;  // stale L1 is safe: min only decreases
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
+                if (pix[k] >= 0 && key[k] < cur[k] && !(dbg & 4)) red_min_u64(minz + pix[k], key[k]);
         } else {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -324,7 +327,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
-                                                     unsigned long long *__restrict__ acc) {
+                                                     float *__restrict__ acc, int dbg) {
     const int lane = threadIdx.x & 31;
     for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
         const int64_t tile = e & ~kMixed;
@@ -338,23 +341,21 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
         }
         int64_t pix[4];
         double zc[4];
+        project4(P, cnt, c, pix, zc);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            pix[k] = k < cnt ? project_point(P[3 * k], P[3 * k + 1], P[3 * k + 2], c, zc[k]) : -1;
+        for (int k = 0; k < 4; ++k)
             if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
-        }
         unsigned long long m[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;  // read-only in pass 2
+        for (int k = 0; k < 4; ++k)
+            m[k] = pix[k] >= 0 ? ((dbg & 2) ? 0x7FF0000000000000ull : __ldg(minz + pix[k])) : 0ull;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (pix[k] < 0) continue;
             if (!(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope))) continue;
-            const unsigned long long w_rg = (unsigned long long)color_byte(W, 3 * k) |
-                                            ((unsigned long long)color_byte(W, 3 * k + 1) << 32);
-            const unsigned long long w_bn = (unsigned long long)color_byte(W, 3 * k + 2) | (1ull << 32);
-            red_add_u64(acc + 2 * pix[k], w_rg);
-            red_add_u64(acc + 2 * pix[k] + 1, w_bn);
+            if (dbg & 1) continue;
+            red_add_v4f32(acc + 4 * pix[k], (float)color_byte(W, 3 * k),
+                          (float)color_byte(W, 3 * k + 1), (float)color_byte(W, 3 * k + 2));
         }
     });
 }
@@ -477,6 +478,14 @@ static bool scene_ok(const ls_scene *scene, const uint32_t *d_list) {
 }
 
 static int g_precheck = -1;  // pass-1 read-before-atomic (LS_PASS1_PRECHECK=0/1, default 1)
+static int proj_dbg() {  // experiments only: LS_PROJ_DBG bit0 no pass-2 REDs, bit1 no gathers, bit2 no pass-1 REDs
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_PROJ_DBG");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
 
 static bool use_precheck() {
     if (g_precheck < 0) {
@@ -510,17 +519,19 @@ int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
     if (use_precheck())
         k_frame_pass1<true><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits);
+            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits,
+            proj_dbg());
     else
         k_frame_pass1<false><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits);
+            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits,
+            proj_dbg());
     LS_LAUNCH_CHECK();
     return 0;
 }
 
 int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                   const uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
+                   const uint64_t *d_minz_bits, float *d_accum4, void *stream) {
     if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)))
         return LS_EINVAL;
     if (scene->n_points == 0) return 0;
@@ -529,14 +540,14 @@ int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     const double ope = 1.0 + eps_rel;
     k_frame_pass2<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
         a, make_cam(*cam), d_keep_bits, d_list, d_count, ope,
-        (const unsigned long long *)d_minz_bits, (unsigned long long *)d_accum2);
+        (const unsigned long long *)d_minz_bits, d_accum4, proj_dbg());
     LS_LAUNCH_CHECK();
     return 0;
 }
 
 int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
                      uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                     uint64_t *d_minz_bits, uint64_t *d_accum2, void *stream) {
+                     uint64_t *d_minz_bits, float *d_accum4, void *stream) {
     int rc = 0;
     if (d_keep_bits) {
         rc = ls_tile_worklist(scene, d_keep_bits, d_list, d_count, stream);
@@ -548,7 +559,7 @@ int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
     rc = ls_frame_pass1(scene, d_keep_bits, d_list, d_count, cam, d_minz_bits, stream);
     if (rc) return rc;
     return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits,
-                          d_accum2, stream);
+                          d_accum4, stream);
 }
 
 }  // extern "C"

@@ -76,7 +76,7 @@ class FrameRenderer:
 
     def check_flags(self) -> None:
         if int(self.bufs.flags.item()):
-            raise RuntimeError("packed accumulator bound exceeded; use project_points() for "
+            raise RuntimeError("f32 accumulator bound exceeded; use project_points() for "
                                "the exact path")
 
     def render(self, camera):

@@ -105,7 +105,8 @@ class FrameBuffers:
         self.width, self.height = int(width), int(height)
         npix = self.width * self.height
         self.minz = torch.full((npix,), _lib.INF_BITS, dtype=torch.int64, device=device)
-        self.accum = torch.zeros((npix, 2), dtype=torch.int64, device=device)
+        # {sum r, sum g, sum b, count} as f32 (exact integers below 2^24)
+        self.accum = torch.zeros((npix, 4), dtype=torch.float32, device=device)
         self.rgb = torch.empty((self.height, self.width, 3), dtype=torch.float32, device=device)
         self.depth = torch.empty((self.height, self.width), dtype=torch.float32, device=device)
         self.alpha = torch.empty((self.height, self.width), dtype=torch.uint8, device=device)
@@ -157,7 +158,7 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
 
 
 def _exact_frame(cloud, grid, camera, params):
-    """Exact (u64 x 4) path, used if a pixel may exceed the packed bound."""
+    """Exact (u64 x 4) path, used if a pixel may exceed the f32 accumulator bound."""
     cands = candidates(cloud, grid, camera)
     return project_candidates(cands, camera, params)
 

@@ -8,7 +8,7 @@ threads).  Per frame:
                list, pass 1 into a local minz
   collective : all-reduce MIN of minz -- u64 bit patterns of positive f64
                depths order like the doubles, and like int64 (< 2^63)
-  every rank : pass 2 against the GLOBAL minz into local packed accumulators
+  every rank : pass 2 against the GLOBAL minz into local f32 accumulators
   collective : reduce SUM of the accumulators to the frame's root
                (root = frame index mod world size, so consecutive frames'
                filter + U-Net run on different GPUs)
@@ -62,9 +62,10 @@ def merge_minz(minz_bits, group=None):
 
 
 def merge_accum(accum, root: int, group=None):
-    """Reduce SUM of the packed accumulators to ``root`` (two's complement int64
-    addition == u64 addition, so the packed {r | g<<32, b | count<<32} halves
-    add exactly while the packed bound holds)."""
+    """Reduce SUM of the {r, g, b, count} f32 accumulators to ``root``.  Every
+    field is an integer; f32 addition of integers is exact (hence order-free)
+    while the sums stay below 2^24, and a sum that reached 2^24 stays >= 2^24,
+    which ls_frame_finish flags."""
     import torch.distributed as dist
 
     dist.reduce(accum, dst=root, op=dist.ReduceOp.SUM, group=group)
@@ -162,4 +163,4 @@ class ShardedRenderer:
 
     def check_flags(self) -> None:
         if int(self.bufs.flags.item()):
-            raise RuntimeError("packed accumulator bound exceeded")
+            raise RuntimeError("f32 accumulator bound exceeded")

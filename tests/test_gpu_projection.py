@@ -202,3 +202,36 @@ def test_c1_reference_digest():
     assert dg(fr.rgb, fr.depth, fr.alpha) == info["frame"]
     ft = depth_filter(fr, FilterParams())
     assert dg(ft.rgb, ft.depth, ft.alpha) == info["filtered"]
+
+
+@pytest.mark.parametrize("n", [65793, 65794, 70_000])
+def test_f32_accumulator_bound(n):
+    """n white points in ONE pixel, all kept: the fast path's f32 sums are
+    exact below 2^24 (65,793 x 255 = 2^24 - 1 is the last unflagged count; at
+    65,794 a sum reaches 2^24 and the frame is flagged), and past the bound
+    project_points must fall back to the exact u64 path and still match the
+    oracle bit for bit."""
+    import torch
+
+    from lidarsplat import PointCloud, project_points
+    from paper_2502_11618_b200 import _lib
+    from paper_2502_11618_b200.render import FrameBuffers, _brute_scene, project_scene
+
+    assert _lib.LS_PACKED_COUNT_LIMIT == 65793
+    cam = make_camera()
+    pts = np.tile(np.array([[0.0, 0.0, 1.0]], np.float32), (n, 1))
+    cols = np.full((n, 3), 255, np.uint8)
+    cloud = PointCloud(pts, cols)
+    pos, col = cloud.device_arrays()
+    bufs = FrameBuffers(cam.width, cam.height, _lib.device())
+    project_scene(_brute_scene(cloud, pos, col), cam, 0.01, bufs, cull=False)
+    torch.cuda.synchronize()
+    got_flag = bool(int(bufs.flags.item()) & 1)
+    assert got_flag == (n * 255 >= 2 ** 24)
+    if not got_flag:
+        px, py = int(cam.cx), int(cam.cy)
+        assert tuple(bufs.rgb[py, px].tolist()) == (1.0, 1.0, 1.0)
+    fr = project_points(cloud, None, cam)
+    ref = O.project(pts, cols, np.array([0]), np.array([n]), cam, 0.01, O.PortKernels())
+    assert np.array_equal(fr.rgb, ref[0]) and np.array_equal(fr.depth, ref[1])
+    assert np.array_equal(fr.alpha, ref[2])

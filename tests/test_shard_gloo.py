@@ -3,7 +3,7 @@
 Each rank projects its contiguous shard of the cell-major scan with the CPU
 oracle kernels, then the SAME merge functions the GPU ShardedRenderer uses
 (paper_2502_11618_b200.shard.merge_minz / merge_accum: all-reduce MIN of the
-f64 bit patterns as int64, reduce SUM of the packed u64 accumulators) combine
+f64 bit patterns as int64, reduce SUM of the f32 {r,g,b,count} accumulators) combine
 them; the root's frame must equal the single-process oracle frame bit for bit
 (min and integer sums are order-free)."""
 
@@ -38,17 +38,14 @@ def _scene():
 
 
 def _pack(acc4):
-    """u64 x4 accumulators -> packed int64 x2 {r | g<<32, b | count<<32}."""
-    a = acc4.astype(np.uint64)
-    w0 = a[:, 0] | (a[:, 1] << np.uint64(32))
-    w1 = a[:, 2] | (a[:, 3] << np.uint64(32))
-    return np.stack([w0, w1], 1).view(np.int64)
+    """u64 x4 accumulators -> the GPU pass-2 layout, f32 {r, g, b, count}."""
+    assert int(acc4.max()) < 2 ** 24
+    return acc4.astype(np.float32)
 
 
 def _unpack(packed):
-    p = packed.view(np.uint64)
-    m = np.uint64(0xFFFFFFFF)
-    return np.stack([p[:, 0] & m, p[:, 0] >> np.uint64(32), p[:, 1] & m, p[:, 1] >> np.uint64(32)], 1)
+    assert float(packed.max()) < 2 ** 24
+    return packed.astype(np.uint64)
 
 
 def _worker(rank, world, port, out):
