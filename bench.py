@@ -277,8 +277,7 @@ def run_b200(args):
         t = torch.tensor([total_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    if not os.environ.get("LS_PROJ_DBG"):
-        renderer.check_flags()
+    renderer.check_flags()
     stage = {k: [] for k in ("cull", "pass1", "pass2", "filter", "unet")}
     for e in evs:
         stage["cull"].append(e[0].elapsed_time(e[1]))

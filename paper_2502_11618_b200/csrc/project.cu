@@ -13,9 +13,8 @@
 // lane owns 4 consecutive points = 48 contiguous bytes (3 x LDG.128) of xyz and
 // 12 bytes (3 x LDG.32) of rgb.  Per-tile occupied-cell spans (built once per
 // scan) let a warp skip a fully culled tile without touching its points.
-#include <stdlib.h>
-
 #include "ls_common.cuh"
+#include "umma.cuh"
 
 namespace ls {
 
@@ -248,112 +247,214 @@ __device__ __forceinline__ void red_add_v4f32(float *p, float r, float g, float 
                  : "memory");
 }
 
-// Iterates the frame's tiles: the work list when culling, every tile otherwise.
-// The next tile's list entry and points are loaded before the current tile is
-// processed, so each warp always has two tiles of loads in flight.
-template <typename F>
-__device__ __forceinline__ void for_each_tile(const SceneArgs &s, const uint32_t *__restrict__ list,
+// Iterates the frame's work items (the work list when culling, every tile
+// otherwise) through a per-warp ring of S shared-memory stages: lane 0 issues
+// bulk async copies (TMA engine, cp.async.bulk) of the tile's xyz (1536 B)
+// -- plus its rgb (384 B) for pass 2 -- into a stage, completion tracked by
+// the stage's mbarrier, S-1 items ahead of the one being processed.  Lanes
+// read their 4 points as 3 x LDS.128 (48 B stride) and colours as 3 x LDS.32
+// (12 B stride), both bank-conflict free.  The scan's last, partial tile (and
+// rgb of a scene whose colour base is not 16 B aligned) is read from global
+// memory.  The ring is kept small (2 stages): the per-pixel minz gathers of
+// both passes live off the L1 that the rest of the SM's 256 KB provides.
+constexpr int kPassWarps = 8;  // 256-thread CTAs
+constexpr int kPosBytes = LS_TILE_POINTS * 12, kColBytes = LS_TILE_POINTS * 3;
+enum RingMode { kXyz = 0, kXyzRgb = 1 };
+
+template <int S, int MODE>
+struct TileRing {
+    static constexpr int kStage = kPosBytes + (MODE == kXyz ? 0 : kColBytes);
+    static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8 + 4);
+};
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(umma::smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(umma::smem_u32(bar))
+        : "memory");
+}
+
+// What the body of a pass sees for one work item.
+struct Item {
+    uint32_t e;         // work-list entry (tile | kMixed)
+    int64_t base;       // first point of this lane
+    bool full;          // complete tile (all 128 points exist)
+    const uint8_t *st;  // the item's smem stage
+};
+
+template <int S, int MODE, typename F>
+__device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t *__restrict__ list,
                                               const uint32_t *__restrict__ count, F &&body) {
-    const int lane = threadIdx.x & 31;
+    using R = TileRing<S, MODE>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    uint8_t *ring = smem + (size_t)wib * S * R::kStage;
+    uint64_t *bars =
+        reinterpret_cast<uint64_t *>(smem + (size_t)kPassWarps * S * R::kStage) + wib * S;
+    uint32_t *ents =
+        reinterpret_cast<uint32_t *>(smem + (size_t)kPassWarps * S * (R::kStage + 8)) + wib * S;
     const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int64_t n_items = list ? (int64_t)__ldg(count) : s.n_tiles;
-    int64_t i = w0;
-    if (i >= n_items) return;
-    uint32_t e = list ? __ldg(list + i) : (uint32_t)i;
-    float P[12];
-    int cnt = load_points(s, (int64_t)(e & ~kMixed) * LS_TILE_POINTS + 4 * lane, P);
-    for (;;) {
-        const int64_t inext = i + nw;
-        const bool more = inext < n_items;
-        uint32_t en = 0;
-        float Pn[12];
-        int cntn = 0;
-        if (more) {
-            en = list ? __ldg(list + inext) : (uint32_t)inext;
-            cntn = load_points(s, (int64_t)(en & ~kMixed) * LS_TILE_POINTS + 4 * lane, Pn);
+    if (w0 >= n_items) return;
+    const int64_t nj = (n_items - w0 + nw - 1) / nw;  // this warp's items
+    const bool col_bulk = MODE != kXyz && (reinterpret_cast<uintptr_t>(s.col) & 15) == 0;
+    auto full = [&](int64_t tile) { return (tile + 1) * LS_TILE_POINTS <= s.n; };
+    // Work-list entries of items [32b, 32b+32) live one per lane (ecur), the
+    // next 32 in enext, so the issuing lane never waits on a list load.
+    auto entry_batch = [&](int64_t b) -> uint32_t {
+        const int64_t j = 32 * b + lane;
+        if (!list) return (uint32_t)(w0 + j * nw);
+        return j < nj ? __ldg(list + w0 + j * nw) : 0u;
+    };
+    uint32_t ecur = entry_batch(0), enext = entry_batch(1);
+    int64_t ebatch = 0;
+    auto entry = [&](int64_t j) -> uint32_t {  // warp-collective, j non-decreasing
+        if ((j >> 5) != ebatch) {
+            ecur = enext;
+            ++ebatch;
+            enext = entry_batch(ebatch + 1);
         }
-        body(e, cnt, P);
-        if (!more) break;
-        i = inext;
-        e = en;
-        cnt = cntn;
-#pragma unroll
-        for (int q = 0; q < 12; ++q) P[q] = Pn[q];
+        return __shfl_sync(0xffffffffu, ecur, (int)(j & 31));
+    };
+    auto issue = [&](uint32_t e, int q) {  // lane 0 only
+        const int64_t tile = e & ~kMixed;
+        ents[q] = e;
+        if (!full(tile)) {
+            umma::mbar_arrive(&bars[q]);
+            return;
+        }
+        const bool rgb = MODE == kXyzRgb && col_bulk;
+        umma::mbar_expect_tx(&bars[q], kPosBytes + (rgb ? kColBytes : 0));
+        uint8_t *dst = ring + q * R::kStage;
+        bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q]);
+        if (rgb) bulk_g2s(dst + kPosBytes, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q]);
+    };
+    if (lane == 0) {
+        for (int q = 0; q < S; ++q) umma::mbar_init(&bars[q], 1);
+        umma::fence_barrier_init();
+    }
+    for (int q = 0; q < S && q < nj; ++q) {
+        const uint32_t e = entry(q);
+        if (lane == 0) issue(e, q);
+    }
+    __syncwarp();
+    for (int64_t j = 0; j < nj; ++j) {
+        const int q = (int)(j % S);
+        umma::mbar_wait_spin(&bars[q], (uint32_t)((j / S) & 1));
+        Item it;
+        it.e = ents[q];
+        const int64_t tile = it.e & ~kMixed;
+        it.base = tile * LS_TILE_POINTS + 4 * lane;
+        it.full = full(tile);
+        it.st = ring + q * R::kStage;
+        uint32_t W[3] = {0u, 0u, 0u};
+        if (MODE != kXyz) {
+            if (it.full && col_bulk) {
+                const uint32_t *c4 = reinterpret_cast<const uint32_t *>(it.st + kPosBytes) + 3 * lane;
+                W[0] = c4[0];
+                W[1] = c4[1];
+                W[2] = c4[2];
+            } else {
+                const int64_t rem = s.n - it.base;
+                load_colors(s, it.base, rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0), W);
+            }
+        }
+        body(it, W);
+        if (j + S < nj) {
+            const uint32_t en = entry(j + S);
+            __syncwarp();
+            if (lane == 0) {
+                // the lanes' generic-proxy reads of stage q precede the async refill
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(en, q);
+            }
+        }
     }
 }
 
-template <bool PRECHECK>
+// The lane's 4 points of an item: from the stage when the tile is complete.
+__device__ __forceinline__ int item_points(const SceneArgs &s, const Item &it, float (&P)[12]) {
+    if (!it.full) return load_points(s, it.base, P);
+    const int lane = threadIdx.x & 31;
+    const float4 *p4 = reinterpret_cast<const float4 *>(it.st) + 3 * lane;
+    const float4 a = p4[0], b = p4[1], c = p4[2];
+    P[0] = a.x; P[1] = a.y; P[2] = a.z; P[3] = a.w;
+    P[4] = b.x; P[5] = b.y; P[6] = b.z; P[7] = b.w;
+    P[8] = c.x; P[9] = c.y; P[10] = c.z; P[11] = c.w;
+    return 4;
+}
+
+// Culled points of a mixed tile drop out (pix = -1).
+__device__ __forceinline__ void drop_culled(const SceneArgs &s, const uint32_t *__restrict__ bits,
+                                            const Item &it, int64_t (&pix)[4]) {
+    if (!(it.e & kMixed)) return;
+    const int64_t tile = it.e & ~kMixed;
+    const int c0 = __ldg(s.tile_c0 + tile), c1 = __ldg(s.tile_c1 + tile);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (pix[k] >= 0 && !point_kept(s, bits, c0, c1, it.base + k)) pix[k] = -1;
+}
+
+constexpr int kPass1Stages = 2, kPass2Stages = 2;
+constexpr size_t kSmem1 = TileRing<kPass1Stages, kXyz>::kBytes;
+constexpr size_t kSmem2 = TileRing<kPass2Stages, kXyzRgb>::kBytes;
+
+// Pass 1: per-pixel minimum depth.  A (possibly stale) L1 read of the pixel's
+// current minimum filters out points that cannot improve it before the atomic.
 __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ bits,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count,
-                                                     unsigned long long *__restrict__ minz, int dbg) {
-    const int lane = threadIdx.x & 31;
-    for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
-        const int64_t tile = e & ~kMixed;
-        const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
-        int c0 = 0, c1 = 0;
-        if (e & kMixed) {
-            c0 = __ldg(s.tile_c0 + tile);
-            c1 = __ldg(s.tile_c1 + tile);
-        }
+                                                     unsigned long long *__restrict__ minz) {
+    for_each_item<kPass1Stages, kXyz>(s, list, count, [&](const Item &it,
+                                                                 const uint32_t (&)[3]) {
+        float P[12];
+        const int cnt = item_points(s, it, P);
         int64_t pix[4];
         double zc[4];
-        unsigned long long key[4];
         project4(P, cnt, c, pix, zc);
+        drop_culled(s, bits, it, pix);
+        unsigned long long key[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
-            key[k] = (unsigned long long)__double_as_longlong(zc[k]);
-        }
-        if (PRECHECK) {
-            unsigned long long cur[4];
+        for (int k = 0; k < 4; ++k) key[k] = (unsigned long long)__double_as_longlong(zc[k]);
+        unsigned long long cur[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldca(minz + pix[k]) : 0ull;  // stale L1 is safe: min only decreases
+        for (int k = 0; k < 4; ++k)
+            cur[k] = pix[k] >= 0 ? __ldca(minz + pix[k]) : 0ull;  // stale L1 is safe: min only decreases
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (pix[k] >= 0 && key[k] < cur[k] && !(dbg & 4)) red_min_u64(minz + pix[k], key[k]);
-        } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (pix[k] >= 0) red_min_u64(minz + pix[k], key[k]);
-        }
+        for (int k = 0; k < 4; ++k)
+            if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
     });
 }
 
+// Pass 2: pixel and depth recomputed from the points (cheaper than the
+// reference's 16 B/candidate pix/z cache round trip; a cached variant was
+// measured no faster -- pass 2 is bound by the minz gathers and atomics).
 __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ bits,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
-                                                     float *__restrict__ acc, int dbg) {
-    const int lane = threadIdx.x & 31;
-    for_each_tile(s, list, count, [&](uint32_t e, int cnt, const float (&P)[12]) {
-        const int64_t tile = e & ~kMixed;
-        const int64_t base = tile * LS_TILE_POINTS + 4 * lane;
-        uint32_t W[3];
-        load_colors(s, base, cnt, W);
-        int c0 = 0, c1 = 0;
-        if (e & kMixed) {
-            c0 = __ldg(s.tile_c0 + tile);
-            c1 = __ldg(s.tile_c1 + tile);
-        }
+                                                     float *__restrict__ acc) {
+    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, [&](const Item &it,
+                                                                    const uint32_t (&W)[3]) {
+        float P[12];
+        const int cnt = item_points(s, it, P);
         int64_t pix[4];
         double zc[4];
         project4(P, cnt, c, pix, zc);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if ((e & kMixed) && pix[k] >= 0 && !point_kept(s, bits, c0, c1, base + k)) pix[k] = -1;
+        drop_culled(s, bits, it, pix);
         unsigned long long m[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            m[k] = pix[k] >= 0 ? ((dbg & 2) ? 0x7FF0000000000000ull : __ldg(minz + pix[k])) : 0ull;
+            m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             if (pix[k] < 0) continue;
             if (!(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope))) continue;
-            if (dbg & 1) continue;
             red_add_v4f32(acc + 4 * pix[k], (float)color_byte(W, 3 * k),
                           (float)color_byte(W, 3 * k + 1), (float)color_byte(W, 3 * k + 2));
         }
@@ -399,9 +500,34 @@ inline bool camera_ok(const ls_camera *cam) {
            cam->width * cam->height < (int64_t(1) << 40);
 }
 
-// Frame passes: 256-thread CTAs, up to 8 resident per SM (8 warps x 8 = 64
-// warps = full occupancy), grid-stride over warp tiles.
-inline int frame_grid(int64_t n_tiles) { return grid_for(n_tiles * 32, 256, 8); }
+// Frame passes: 256-thread CTAs with a dynamic-smem tile ring, exactly as
+// many as are co-resident (persistent, grid-stride over the work list; a
+// grid of several waves would leave a partial last wave).
+static int ring_blocks_per_sm(const void *fn, size_t smem) {
+    struct Entry {
+        const void *fn;
+        int blocks;
+    };
+    static Entry cache[8];
+    static int n = 0;
+    for (int i = 0; i < n; ++i)
+        if (cache[i].fn == fn) return cache[i].blocks;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // half of the unified 256 KB as shared memory: 4 CTAs' rings fit, and the
+    // other half stays L1 for the per-pixel minz gathers (measured: leaving the
+    // split to the driver shrinks L1 to ~30 KB and costs pass 1 ~60%)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 50);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 256, smem) != cudaSuccess || b < 1)
+        b = 1;
+    if (n < 8) cache[n++] = {fn, b};
+    return b;
+}
+
+template <typename K>
+inline int frame_grid(K kernel, size_t smem, int64_t n_tiles) {
+    return grid_for(n_tiles * 32, 256, ring_blocks_per_sm((const void *)kernel, smem));
+}
 
 }  // namespace ls
 
@@ -477,24 +603,6 @@ static bool scene_ok(const ls_scene *scene, const uint32_t *d_list) {
     return true;
 }
 
-static int g_precheck = -1;  // pass-1 read-before-atomic (LS_PASS1_PRECHECK=0/1, default 1)
-static int proj_dbg() {  // experiments only: LS_PROJ_DBG bit0 no pass-2 REDs, bit1 no gathers, bit2 no pass-1 REDs
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("LS_PROJ_DBG");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
-
-static bool use_precheck() {
-    if (g_precheck < 0) {
-        const char *e = getenv("LS_PASS1_PRECHECK");
-        g_precheck = (e && e[0] == '0') ? 0 : 1;
-    }
-    return g_precheck == 1;
-}
-
 int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
                      uint32_t *d_count, void *stream) {
     if (!scene_ok(scene, d_list) || !d_keep_bits || !d_list || !d_count) return LS_EINVAL;
@@ -517,14 +625,9 @@ int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    if (use_precheck())
-        k_frame_pass1<true><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits,
-            proj_dbg());
-    else
-        k_frame_pass1<false><<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-            a, make_cam(*cam), d_keep_bits, d_list, d_count, (unsigned long long *)d_minz_bits,
-            proj_dbg());
+    k_frame_pass1<<<frame_grid(k_frame_pass1, kSmem1, a.n_tiles), 256, kSmem1,
+                    (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
+                                            (unsigned long long *)d_minz_bits);
     LS_LAUNCH_CHECK();
     return 0;
 }
@@ -537,10 +640,10 @@ int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    const double ope = 1.0 + eps_rel;
-    k_frame_pass2<<<frame_grid(a.n_tiles), 256, 0, (cudaStream_t)stream>>>(
-        a, make_cam(*cam), d_keep_bits, d_list, d_count, ope,
-        (const unsigned long long *)d_minz_bits, d_accum4, proj_dbg());
+    k_frame_pass2<<<frame_grid(k_frame_pass2, kSmem2, a.n_tiles), 256, kSmem2,
+                    (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
+                                            1.0 + eps_rel, (const unsigned long long *)d_minz_bits,
+                                            d_accum4);
     LS_LAUNCH_CHECK();
     return 0;
 }

@@ -235,3 +235,26 @@ def test_f32_accumulator_bound(n):
     ref = O.project(pts, cols, np.array([0]), np.array([n]), cam, 0.01, O.PortKernels())
     assert np.array_equal(fr.rgb, ref[0]) and np.array_equal(fr.depth, ref[1])
     assert np.array_equal(fr.alpha, ref[2])
+
+
+@pytest.mark.parametrize("eps", [0.0, 1e-9, 0.01, 0.5])
+def test_soft_zbuffer_threshold_edges_match_oracle(rng, port, eps):
+    """Points sharing a line of sight at depths one f64 ulp apart, and eps = 0
+    (every winner exactly on the threshold): the keep test zc <= minz*(1+eps)
+    must agree with the oracle bit for bit, culled and brute force."""
+    from lidarsplat import PointCloud, RenderParams, build_grid, project_points
+
+    cloud = random_cloud(rng, 40_000, extent=6.0, offset=-3.0)
+    base = cloud.positions[:2000].astype(np.float64)
+    dup = np.concatenate([base, np.nextafter(base, np.inf)]).astype(np.float32)
+    pos = np.concatenate([cloud.positions, dup])
+    col = np.concatenate([cloud.colors, rng.integers(0, 256, (len(dup), 3), dtype=np.uint8)])
+    cloud = PointCloud(pos, col)
+    cam = random_view(rng, cloud)
+    params = RenderParams(zbuffer_epsilon_rel=eps)
+    for grid in (build_grid(cloud, 1.0), None):
+        a = project_points(cloud, grid, cam, params)
+        rgb, depth, alpha, _, _ = O.project(cloud.positions, cloud.colors, np.zeros(1, np.int64),
+                                            np.array([cloud.count], np.int64), cam, eps, port)
+        assert np.array_equal(a.rgb, rgb) and np.array_equal(a.depth, depth)
+        assert np.array_equal(a.alpha, alpha)
