@@ -299,7 +299,33 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     }
 }
 
-// One thread per coarse pixel; FINAL reads the full-resolution frame.
+// Writes one filtered pixel's U-Net input channels [r g b d' a 0 ...].
+__device__ __forceinline__ void store_unet_px(__nv_bfloat16 *__restrict__ dst, int unet_c, float r,
+                                              float g, float b, float dd, uint8_t a, double znear) {
+    // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
+    const float dn = dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear))) : 0.0f;
+    __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
+    __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
+    __nv_bfloat162 v45 = __floats2bfloat162_rn((float)a, 0.0f);
+    if ((unet_c & 7) == 0) {  // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
+        uint4 *o4 = reinterpret_cast<uint4 *>(dst);
+        o4[0] = make_uint4(*reinterpret_cast<uint32_t *>(&v01), *reinterpret_cast<uint32_t *>(&v23),
+                           *reinterpret_cast<uint32_t *>(&v45), 0u);
+        for (int c = 1; c < unet_c / 8; ++c) o4[c] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+        __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(dst);
+        const __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
+        o2[0] = v01;
+        o2[1] = v23;
+        o2[2] = v45;
+        for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
+    }
+}
+
+// One thread per COARSE pixel on a 2-D grid (32 x 8 threads per CTA, no
+// index division); FINAL reads the full-resolution frame and, where the
+// thread's two children of a fine row are both inside an even-width image,
+// moves them with 8 B (rgb, depth), 2 B (alpha) and 16 B (U-Net) accesses.
 template <bool FINAL>
 __global__ void __launch_bounds__(256) k_filter_step(
     const float *__restrict__ coarse, int64_t ch, int64_t cw, const float *__restrict__ fine,
@@ -308,74 +334,97 @@ __global__ void __launch_bounds__(256) k_filter_step(
     const float *__restrict__ rgb, const uint8_t *__restrict__ alpha, float *__restrict__ frgb,
     float *__restrict__ fdepth, uint8_t *__restrict__ falpha, uint8_t *__restrict__ keep_out,
     __nv_bfloat16 *__restrict__ unet_in, int unet_c, double znear) {
-    const int64_t n = ch * cw;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
-         q += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t cy = q / cw, cx = q - cy * cw;
-        const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
-        const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+    const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
+    if (cx >= cw || cy >= ch) return;
+    const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
+    const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+    const int64_t x = 2 * cx;
+    const bool pair = x + 1 < fw && (fw & 1) == 0;
 #pragma unroll
-        for (int dy = 0; dy < 2; ++dy) {
-            const int64_t y = 2 * cy + dy;
-            if (y >= fh) break;
+    for (int dy = 0; dy < 2; ++dy) {
+        const int64_t y = 2 * cy + dy;
+        if (y >= fh) break;
+        const int64_t p = y * fw + x;
+        if (!FINAL) {
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx) {
-                const int64_t x = 2 * cx + dx;
-                if (x >= fw) break;
-                const int64_t p = y * fw + x;
-                if (!FINAL) {
-                    const float f = fine[p];
-                    const bool k = keep_test(f, ref, fs);
-                    out[p] = k ? f : bilinear_at(coarse, ch, cw, y, x);
-                } else {
-                    const float d = fine[p];  // frame depth (0 = empty)
-                    const bool k = keep_test(sentinel(d), ref, fs);
-                    if (keep_out) keep_out[p] = (uint8_t)k;
-                    if (!rgb) continue;  // mask-only (filter_depth_image)
-                    // filtering.py:141-147: multiply by the f32 0/1 mask
-                    const float mk = k ? 1.0f : 0.0f;
-                    const float r = rgb[3 * p] * mk, g = rgb[3 * p + 1] * mk,
-                                b = rgb[3 * p + 2] * mk, dd = d * mk;
-                    const uint8_t a = (uint8_t)(alpha[p] * (uint8_t)k);
-                    if (frgb) {
-                        frgb[3 * p] = r;
-                        frgb[3 * p + 1] = g;
-                        frgb[3 * p + 2] = b;
-                    }
-                    if (fdepth) fdepth[p] = dd;
-                    if (falpha) falpha[p] = a;
-                    if (unet_in) {
-                        // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
-                        const float dn =
-                            dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear)))
-                                      : 0.0f;
-                        __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
-                        __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
-                        __nv_bfloat162 v45 = __floats2bfloat162_rn((float)a, 0.0f);
-                        const uint4 q0 = make_uint4(*reinterpret_cast<uint32_t *>(&v01),
-                                                    *reinterpret_cast<uint32_t *>(&v23),
-                                                    *reinterpret_cast<uint32_t *>(&v45), 0u);
-                        if ((unet_c & 7) == 0) {
-                            // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
-                            uint4 *o4 = reinterpret_cast<uint4 *>(unet_in + p * unet_c);
-                            o4[0] = q0;
-                            for (int c = 1; c < unet_c / 8; ++c) o4[c] = make_uint4(0u, 0u, 0u, 0u);
-                        } else {
-                            __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(unet_in + p * unet_c);
-                            const __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
-                            o2[0] = v01;
-                            o2[1] = v23;
-                            o2[2] = v45;
-                            for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
-                        }
-                    }
-                }
+                if (x + dx >= fw) break;
+                const float f = fine[p + dx];
+                out[p + dx] = keep_test(f, ref, fs) ? f : bilinear_at(coarse, ch, cw, y, x + dx);
             }
+            continue;
+        }
+        if (!pair) {  // odd width or the last column: scalar children
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                if (x + dx >= fw) break;
+                const int64_t q = p + dx;
+                const float dq = fine[q];  // frame depth (0 = empty)
+                const bool kq = keep_test(sentinel(dq), ref, fs);
+                if (keep_out) keep_out[q] = (uint8_t)kq;
+                if (!rgb) continue;  // mask-only (filter_depth_image)
+                const float m = kq ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
+                const float r = rgb[3 * q] * m, g = rgb[3 * q + 1] * m, b = rgb[3 * q + 2] * m,
+                            dd = dq * m;
+                const uint8_t a = (uint8_t)(alpha[q] * (uint8_t)kq);
+                if (frgb) {
+                    frgb[3 * q] = r;
+                    frgb[3 * q + 1] = g;
+                    frgb[3 * q + 2] = b;
+                }
+                if (fdepth) fdepth[q] = dd;
+                if (falpha) falpha[q] = a;
+                if (unet_in) store_unet_px(unet_in + q * unet_c, unet_c, r, g, b, dd, a, znear);
+            }
+            continue;
+        }
+        const float2 d2 = *reinterpret_cast<const float2 *>(fine + p);
+        const float d[2] = {d2.x, d2.y};
+        bool k[2];
+        float mk[2];
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            k[dx] = keep_test(sentinel(d[dx]), ref, fs);
+            mk[dx] = k[dx] ? 1.0f : 0.0f;
+        }
+        if (keep_out) *reinterpret_cast<uchar2 *>(keep_out + p) = make_uchar2(k[0], k[1]);
+        if (!rgb) continue;
+        const float2 *r2 = reinterpret_cast<const float2 *>(rgb + 3 * p);
+        const float2 a0 = r2[0], a1 = r2[1], a2 = r2[2];
+        const float c[2][3] = {{a0.x, a0.y, a1.x}, {a1.y, a2.x, a2.y}};
+        const uchar2 a2v = *reinterpret_cast<const uchar2 *>(alpha + p);
+        const uint8_t al[2] = {a2v.x, a2v.y};
+        float o[2][4];
+        uint8_t oa[2];
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+            o[dx][0] = c[dx][0] * mk[dx];
+            o[dx][1] = c[dx][1] * mk[dx];
+            o[dx][2] = c[dx][2] * mk[dx];
+            o[dx][3] = d[dx] * mk[dx];
+            oa[dx] = (uint8_t)(al[dx] * (uint8_t)k[dx]);
+        }
+        if (frgb) {
+            float2 *w2 = reinterpret_cast<float2 *>(frgb + 3 * p);
+            w2[0] = make_float2(o[0][0], o[0][1]);
+            w2[1] = make_float2(o[0][2], o[1][0]);
+            w2[2] = make_float2(o[1][1], o[1][2]);
+        }
+        if (fdepth) *reinterpret_cast<float2 *>(fdepth + p) = make_float2(o[0][3], o[1][3]);
+        if (falpha) *reinterpret_cast<uchar2 *>(falpha + p) = make_uchar2(oa[0], oa[1]);
+        if (unet_in) {
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx)
+                store_unet_px(unet_in + (p + dx) * unet_c, unet_c, o[dx][0], o[dx][1], o[dx][2],
+                              o[dx][3], oa[dx], znear);
         }
     }
 }
 
-inline int step_grid(int64_t n) { return grid_for(n, 256, 8); }
+inline dim3 step_grid2(int64_t ch, int64_t cw) {
+    return dim3((unsigned)((cw + 31) / 32), (unsigned)((ch + 7) / 8));
+}
 
 inline void level_sizes(int64_t H, int64_t W, int L, int64_t *h, int64_t *w) {
     h[0] = H;
@@ -401,14 +450,14 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
         const int64_t fh = lv.h[L - i], fw = lv.w[L - i];
         if (i < L) {
             const float *fine = lv.img[L - i - 1];
-            k_filter_step<false><<<step_grid(ch * cw), 256, 0, st>>>(
+            k_filter_step<false><<<step_grid2(ch, cw), dim3(32, 8), 0, st>>>(
                 coarse, ch, cw, fine, fh, fw, fs, et, up, nullptr, nullptr, nullptr, nullptr,
                 nullptr, nullptr, nullptr, 0, 0.0);
             LS_LAUNCH_CHECK();
             coarse = up;
             up += fh * fw;
         } else {
-            k_filter_step<true><<<step_grid(ch * cw), 256, 0, st>>>(
+            k_filter_step<true><<<step_grid2(ch, cw), dim3(32, 8), 0, st>>>(
                 coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, rgb, alpha, frgb, fdepth,
                 falpha, keep, unet_in, unet_c, znear);
             LS_LAUNCH_CHECK();

@@ -533,6 +533,12 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         if (status) *status = rc;
         return nullptr;
     };
+    // c0 = 8 (single source): the tensor has 8 channels per pixel and is read
+    // as a 16-channel K chunk whose upper half the TMA zero-fills (box wider
+    // than the tensor's channel extent) -- the network input's 5 live
+    // channels at half the bytes of a 16-channel layout
+    const int c0_tensor = c0;
+    if (c0 == 8 && c1 == 0) c0 = 16;
     if (!d_x0 || !d_w || !d_scale || !d_shift || batch < 1 || h < 1 || w < 1 || !chunk_ok(c0))
         return fail(LS_EINVAL);
     if (c1 < 0 || (c1 > 0 && (!d_x1 || !chunk_ok(c1)))) return fail(LS_EINVAL);
@@ -633,9 +639,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     const int box_h = kTH * mt_for(bn) + 2 * p.pad;
-    bool ok = encode_act(&pl->a0, d_x0, c0, w, h, batch, chunk, box_h);
-    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0, w, h, batch, chunk,
-                          box_h);
+    bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, box_h);
+    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
+                          chunk, box_h);
     ok = ok && encode_wts(&pl->b, d_w, p.ctot, n_total, p.kxs * kys, chunk, bn, kys);
     if (!ok) {
         delete pl;

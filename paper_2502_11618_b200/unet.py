@@ -247,11 +247,13 @@ def _pad16(c: int) -> int:
 class UNet:
     """Device U-Net; ``forward(x, out)`` enqueues one pass on the current stream.
 
-    x   : bf16 (B, H, W, in_pad) NHWC [r, g, b, d', alpha, 0...]
+    x   : bf16 (B, H, W, C) NHWC [r, g, b, d', alpha, 0...], C = in_pad (8) or 16;
+          8 channels are read as the first layer's 16-wide K chunk with the
+          upper half zero-filled by the TMA, so both give identical outputs
     out : f32  (B, H, W, outChannels), sigmoid output in [0, 1]
     """
 
-    in_pad = 16
+    in_pad = 8
 
     def __init__(self, cfg: UNetConfig, params: dict, device=None):
         import torch

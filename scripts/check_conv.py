@@ -25,6 +25,8 @@ def conv_case(c0, c1, cout, h, w, act, pool=False, head=False, batch=1, seed=0):
     hb = (torch.randn(3, generator=g) * 0.1).to(dev) if head else None
     ho = torch.empty(batch, h, w, 3, dtype=torch.float32, device=dev) if head else None
     wdev = wt.reshape(cout, 3, 3, cin).permute(2, 1, 0, 3).contiguous()  # [kx][ky][o][c]
+    if c0 == 8 and c1 == 0:  # 8-channel input: weight rows hold the 16-wide K chunk
+        wdev = torch.cat([wdev, torch.zeros_like(wdev)], -1).contiguous()
     rc = lib.ls_conv2d(x0.data_ptr(), c0, None if x1 is None else x1.data_ptr(), c1, batch, h, w,
                        wdev.data_ptr(), 3, cout, scale.data_ptr(), shift.data_ptr(), act, 0.1,
                        y.data_ptr(), yf.data_ptr(), _lib.ptr(pl), _lib.ptr(hw), _lib.ptr(hb),
@@ -72,6 +74,7 @@ if __name__ == "__main__":
     cases = [
         dict(c0=64, c1=0, cout=64, h=32, w=64, act=0),
         dict(c0=16, c1=0, cout=32, h=64, w=128, act=1),
+        dict(c0=8, c1=0, cout=32, h=64, w=128, act=1),
         dict(c0=32, c1=0, cout=32, h=64, w=128, act=1, pool=True),
         dict(c0=32, c1=32, cout=32, h=64, w=128, act=2, head=True),
         dict(c0=128, c1=128, cout=128, h=16, w=32, act=2),

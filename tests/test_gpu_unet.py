@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 LAYER_CASES = [
     dict(c0=64, c1=0, cout=64, h=32, w=64, act=0),
     dict(c0=16, c1=0, cout=32, h=64, w=128, act=1),
+    dict(c0=8, c1=0, cout=32, h=64, w=128, act=1),
     dict(c0=32, c1=0, cout=32, h=64, w=128, act=1, pool=True),
     dict(c0=32, c1=32, cout=32, h=64, w=128, act=2, head=True),
     dict(c0=128, c1=128, cout=128, h=16, w=32, act=2),
@@ -70,12 +71,12 @@ def _input(rng, h, w):
     return pack_input(rgb, depth, (depth > 0).astype(np.uint8), 0.1, 16)
 
 
-def _run_device(net, x):
+def _run_device(net, x, cpad=16):
     import torch
 
     dev = torch.device("cuda")
     b, h, w, _ = x.shape
-    xin = torch.zeros((b, h, w, 16), dtype=torch.bfloat16, device=dev)
+    xin = torch.zeros((b, h, w, cpad), dtype=torch.bfloat16, device=dev)
     xin[..., :5] = torch.from_numpy(x).to(dev).to(torch.bfloat16)
     out = torch.empty((b, h, w, net.cfg.outChannels), dtype=torch.float32, device=dev)
     net.forward(xin, out)
@@ -112,6 +113,16 @@ def test_unet_vs_f64_oracle(name, h, w):
     assert err <= 1.5e-2
     assert _psnr(got, ref) >= 40.0
     assert err <= 2 * max(floor, 1e-3)
+
+
+def test_eight_channel_input_identical():
+    """The engine's 8-channel input (TMA zero-fills channels 8..15 of the first
+    layer's K chunk) gives bit-identical outputs to the 16-channel layout."""
+    from paper_2502_11618_b200.unet import UNet
+
+    net = UNet.from_config("default", seed=5)
+    x = _input(np.random.default_rng(3), 64, 96)
+    assert np.array_equal(_run_device(net, x, 8), _run_device(net, x, 16))
 
 
 def test_divisibility_rejected():
