@@ -184,6 +184,11 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
     const int n_kg = p.kxs / p.kxps;  // stages per channel chunk
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // Programmatic dependent launch: let the next layer's CTAs start their own
+    // prologue as SMs free up; everything this kernel does before
+    // griddepcontrol.wait (barriers, TMEM, weights, epilogue constants) reads
+    // only data no earlier kernel writes.
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {
             for (int s = 0; s < S; ++s) {
@@ -232,6 +237,9 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                                     kx * KYS, bres);
                     }
             }
+            // the previous layer's activations are complete and visible past here;
+            // every global write of this kernel depends on loads issued after it
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             uint32_t it = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
                 const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
@@ -488,6 +496,16 @@ struct ls_conv_plan {
 namespace ls {
 namespace unet {
 
+// LS_UNET_PDL=0 launches the layers fully serialised (A/B measurements).
+static bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_UNET_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int BN, int CHUNK, int MODE>
 static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;  // idempotent: racing threads set the same value
@@ -498,9 +516,17 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
         if (e != cudaSuccess) return (int)e;
         attr_done = 1;
     }
-    k_conv_p<BN, CHUNK, MODE><<<pl->grid, CfgP<BN, CHUNK>::kThreads, pl->smem, st>>>(
-        pl->a0, pl->a1, pl->b, pl->p);
-    return (int)cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl->grid);
+    cfg.blockDim = dim3((unsigned)CfgP<BN, CHUNK>::kThreads);
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
 }
 
 template <int BN, int CHUNK>

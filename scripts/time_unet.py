@@ -5,7 +5,7 @@ import torch
 from paper_2502_11618_b200.unet import UNet
 net = UNet.from_config(sys.argv[1] if len(sys.argv) > 1 else "default", seed=7)
 h, w = 1088, 1920
-x = torch.rand((1, h, w, 16), device="cuda").to(torch.bfloat16)
+x = torch.rand((1, h, w, UNet.in_pad), device="cuda").to(torch.bfloat16)
 out = torch.empty((1, h, w, 3), device="cuda")
 for _ in range(3):
     net.forward(x, out)
