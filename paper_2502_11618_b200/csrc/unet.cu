@@ -70,6 +70,7 @@ struct ConvParamsP {
     uint32_t off_const;     // scale[n_total], shift[n_total], head_w (f32)
     uint32_t off_pool;      // (unused: pooling is done with warp shuffles)
     uint32_t off_bar;       // barriers
+    int dbg;                // experiments (LS_CONV_DBG): 1 no MMA, 2 no A/B TMA, 4 no stores
 };
 
 template <int BN, int CHUNK>
@@ -252,6 +253,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                         const uint32_t ph = (it / (uint32_t)S) & 1u;
                         mbar_wait(empty + s, ph ^ 1u);
                         uint8_t *st = smem + (size_t)s * p.stage_bytes;
+                        if (p.dbg & 2) {
+                            mbar_arrive(full + s);
+                            continue;
+                        }
                         mbar_expect_tx(full + s, p.kxps * (p.a_tx + (p.resident ? 0u : p.b_blk)));
                         for (int k = 0; k < p.kxps; ++k) {
                             const int kx = kg * p.kxps + k;
@@ -292,6 +297,9 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                                         ? sbase + p.off_b + (uint32_t)(q * p.kxs + kg * p.kxps) * p.b_blk
                                         : st + p.kxps * p.a_bytes) >>
                                    4);
+                        // (scripts/mma_rate.cu: a 128xNx16 MMA costs max(~45, N/2)
+                        // cycles whatever the accumulator order -- N=32 tiles top
+                        // out at 36% of the tensor peak)
                         for (int k = 0; k < p.kxps; ++k) {
 #pragma unroll
                             for (int u = 0; u < MT; ++u) {
@@ -302,6 +310,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                                         const uint32_t ao =
                                             k * a_box16 + ((u * kTH + ky) * kTW * C::kRow + 32 * j) / 16;
                                         const uint32_t bo = k * b_blk16 + (ky * BN * C::kRow + 32 * j) / 16;
+                                        if (!(p.dbg & 1))
                                         mma_bf16(d0 + u * BN, ((uint64_t)dhi << 32) | (a_lo + ao),
                                                  ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
                                                  (q | kg | k | ky | j) != 0 ? 1u : 0u);
@@ -333,92 +342,119 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
             fence_after_sync();
             const uint32_t tbase = tmem + ab * C::kItemCols + ((uint32_t)(quarter * 32) << 16);
             const int gx = ip.x0 + tx;
-#pragma unroll 1
-            for (int u = 0; u < MT; ++u) {
+            // 32-column groups of this item that hold real columns (n_total may
+            // end mid-tile, or be 16 mod 32)
+            const int rem = p.n_total - ip.nt * BN;
+            const int ng = rem >= BN ? BN / 32 : (rem + 31) / 32;
+            const int steps = MT * ng;
+            float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            // one 32-column group: scale/shift/act, bf16 pack, 32 B stores,
+            // pooling / head as the mode asks
+            auto process = [&](int u, int g, const uint32_t(&rr)[32]) {
                 const int gy = ip.y0 + u * kTH + ty;
                 const bool valid = gx < p.w && gy < p.h;
-                float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 1
-                for (int g = 0; g < BN / 32; ++g) {
-                    const int n0 = ip.nt * BN + g * 32;
-                    if (n0 >= p.n_total) break;  // uniform
-                    uint32_t rr[32];
-                    tmem_ld32(tbase + (uint32_t)(u * BN + g * 32), rr);
-                    if (u + 1 == MT && (g + 1 == BN / 32 || n0 + 32 >= p.n_total)) {
-                        // item fully read -> hand the TMEM buffer back early
-                        fence_before_sync();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(tempty + ab);
+                const int n0 = ip.nt * BN + g * 32;
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int n = n0 + h2 * 16;
+                    if (n >= p.n_total) break;  // uniform (n_total may be 16 mod 32)
+                    const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
+                    const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
+                    float v[16];
+#pragma unroll
+                    for (int i4 = 0; i4 < 4; ++i4) {
+                        const float4 sc = sc4[i4], sh = sh4[i4];
+                        const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+                        const float shv[4] = {sh.x, sh.y, sh.z, sh.w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            v[4 * i4 + j] = apply_act(
+                                fmaf(__uint_as_float(rr[h2 * 16 + 4 * i4 + j]), scv[j], shv[j]),
+                                p.act, p.alpha);
                     }
+                    if (MODE == kHead) {
+                        for (int j2 = 0; j2 < p.head_c; ++j2) {
 #pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2) {
-                        const int n = n0 + h2 * 16;
-                        if (n >= p.n_total) break;  // uniform (n_total may be 16 mod 32)
-                        float v[16];
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            v[i] = apply_act(fmaf(__uint_as_float(rr[h2 * 16 + i]), s_scale[n + i],
-                                                  s_shift[n + i]),
-                                             p.act, p.alpha);
-                        if (MODE == kHead) {
-                            for (int j2 = 0; j2 < p.head_c; ++j2) {
-#pragma unroll
-                                for (int i = 0; i < 16; ++i)
-                                    hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
-                            }
-                            if (!p.y && !p.y_f32) continue;  // head input not materialised
+                            for (int i = 0; i < 16; ++i)
+                                hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
                         }
-                        uint32_t pk[8];
+                        if (!p.y && !p.y_f32) continue;  // head input not materialised
+                    }
+                    uint32_t pk[8];
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-                        if (valid) {
-                            int64_t pix;
-                            int o = n;
-                            if (MODE == kTransposed) {
-                                const int dd = n / p.cout;
-                                o = n - dd * p.cout;
-                                pix = ((int64_t)ip.img * (2 * p.h) + 2 * gy + (dd >> 1)) * (2 * p.w) +
-                                      2 * gx + (dd & 1);
-                            } else {
-                                pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
-                            }
-                            if (p.y) {
-                                uint4 *dst = reinterpret_cast<uint4 *>(p.y + pix * p.cout + o);
-                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                            }
-                            if (p.y_f32) {
-                                float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + o);
-                                dst[0] = make_float4(v[0], v[1], v[2], v[3]);
-                                dst[1] = make_float4(v[4], v[5], v[6], v[7]);
-                                dst[2] = make_float4(v[8], v[9], v[10], v[11]);
-                                dst[3] = make_float4(v[12], v[13], v[14], v[15]);
-                            }
+                    for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                    if (valid) {
+                        int64_t pix;
+                        int o = n;
+                        if (MODE == kTransposed) {
+                            const int dd = n / p.cout;
+                            o = n - dd * p.cout;
+                            pix = ((int64_t)ip.img * (2 * p.h) + 2 * gy + (dd >> 1)) * (2 * p.w) +
+                                  2 * gx + (dd & 1);
+                        } else {
+                            pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
                         }
-                        if (MODE == kPool) {
+                        if (p.y && !(p.dbg & 4)) st_global_v8(p.y + pix * p.cout + o, pk);
+                        if (p.y_f32) {
+                            float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + o);
+                            dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                            dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                            dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+                            dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+                        }
+                    }
+                    if (MODE == kPool) {
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const uint32_t a1 = __shfl_xor_sync(0xffffffffu, pk[i], 1);
-                                const uint32_t a2 = __shfl_xor_sync(0xffffffffu, pk[i], 16);
-                                const uint32_t a3 = __shfl_xor_sync(0xffffffffu, pk[i], 17);
-                                pk[i] = hmax4(pk[i], a1, a2, a3);
-                            }
-                            if (valid && (lane & 17) == 0) {
-                                const int64_t pp =
-                                    ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
-                                uint4 *dst = reinterpret_cast<uint4 *>(p.pool + pp * p.cout + n);
-                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                            }
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t a1 = __shfl_xor_sync(0xffffffffu, pk[i], 1);
+                            const uint32_t a2 = __shfl_xor_sync(0xffffffffu, pk[i], 16);
+                            const uint32_t a3 = __shfl_xor_sync(0xffffffffu, pk[i], 17);
+                            pk[i] = hmax4(pk[i], a1, a2, a3);
+                        }
+                        if (valid && (lane & 17) == 0) {
+                            const int64_t pp =
+                                ((int64_t)ip.img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
+                            st_global_v8(p.pool + pp * p.cout + n, pk);
                         }
                     }
                 }
-                if (MODE == kHead && valid) {
-                    const int64_t pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
-                    for (int j2 = 0; j2 < p.head_c; ++j2) {
-                        const float z = hacc[j2] + __ldg(p.head_b + j2);
-                        p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                if (MODE == kHead && g + 1 == ng) {
+                    if (valid) {
+                        const int64_t pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
+                        for (int j2 = 0; j2 < p.head_c; ++j2) {
+                            const float z = hacc[j2] + __ldg(p.head_b + j2);
+                            p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                        }
                     }
+                    hacc[0] = hacc[1] = hacc[2] = hacc[3] = 0.0f;
+                }
+            };
+            auto col = [&](int s) -> uint32_t {
+                const int u = s / ng;
+                return tbase + (uint32_t)(u * BN + (s - u * ng) * 32);
+            };
+            // the TMEM buffer goes back to the MMA warp as soon as its last
+            // group is in registers
+            auto release = [&]() {
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + ab);
+            };
+            // two register buffers: group s+1's tcgen05.ld is in flight while
+            // group s is processed
+            uint32_t ra[32], rb[32];
+            tmem_ld32_async(col(0), ra);
+#pragma unroll 1
+            for (int s = 0; s < steps; s += 2) {
+                tmem_ld_wait(ra);
+                if (s + 1 < steps) tmem_ld32_async(col(s + 1), rb);
+                else release();
+                process(s / ng, s % ng, ra);
+                if (s + 1 < steps) {
+                    tmem_ld_wait(rb);
+                    if (s + 2 < steps) tmem_ld32_async(col(s + 2), ra);
+                    else release();
+                    process((s + 1) / ng, (s + 1) % ng, rb);
                 }
             }
         }
@@ -577,6 +613,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     if (n_total > 4096) return fail(LS_EINVAL);
     int bn = n_total >= 256 ? 256 : (n_total >= 128 ? 128 : (n_total >= 64 ? 64 : 32));
     if (n_total % bn) bn = 32;
+    // transposed convs are epilogue-bound (K is small, 4x cout outputs per
+    // input pixel): 128-column tiles leave room for 3 epilogue warpgroups
+    if (transposed && bn > 128) bn = 128;
     if (d_head_w && n_total > bn) return fail(LS_EINVAL);  // the head needs every channel
     int chunk = bn >= 256 ? 32 : 64;
     while (chunk > 16 && ((c0 % chunk) || (c1 % chunk))) chunk >>= 1;
@@ -605,6 +644,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.head_b = d_head_b;
     p.head_c = head_c;
     p.head_out = d_head_out;
+    p.dbg = getenv("LS_CONV_DBG") ? atoi(getenv("LS_CONV_DBG")) : 0;
     const int kys = p.kxs;
     const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
                                ~size_t(1023);
