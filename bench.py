@@ -309,16 +309,21 @@ def run_b200(args):
             roofline, roofline_unet = roofline_unet, roofline
         roofline["other"] = roofline_unet
     # ---- end to end through the public API (host result every frame) ----
+    # FrameRenderer.render_stream: every frame's camera goes in from the host
+    # and its full result comes back to pinned host memory; the copy-out of
+    # frame i overlaps the compute of frame i+1 (wall clock over K frames)
     e2e = None
     if world == 1:
-        for i in range(2):
-            renderer.render(cams[i % len(cams)])
+        for _ in renderer.render_stream([cams[i % len(cams)] for i in range(3)]):
+            pass
         torch.cuda.synchronize()
+        seq = [cams[(args.warmup + i) % len(cams)] for i in range(args.steps)]
         e0 = time.perf_counter()
-        for i in range(args.steps):
-            renderer.render(cams[(args.warmup + i) % len(cams)])
-        e_ms = (time.perf_counter() - e0) * 1e3 / args.steps
-        e2e = {"value": 1e3 / e_ms, "unit": "frames/s",
+        n_out = 0
+        for _ in renderer.render_stream(seq):
+            n_out += 1
+        e_ms = (time.perf_counter() - e0) * 1e3 / n_out
+        e2e = {"value": 1e3 / e_ms, "unit": "frames/s", "api": "FrameRenderer.render_stream",
                "h2d_bytes_per_step": 320,  # camera struct + 6 frustum planes (kernel params)
                "d2h_bytes_per_step": renderer.d2h_bytes}
     line = {

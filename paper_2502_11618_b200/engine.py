@@ -53,6 +53,12 @@ class FrameRenderer:
             self.unet_in = torch.zeros((1, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
             self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
         self._pinned = None
+        # render_stream state: a second device output set (frame i's copy-out
+        # overlaps frame i+1's compute), a copy stream, per-slot copy events
+        self._alt = None
+        self._copy_stream = None
+        self._copy_done = [None, None]
+        self._ring = None
 
     @property
     def launches_per_frame(self) -> int:
@@ -61,16 +67,32 @@ class FrameRenderer:
             n += self.unet.launches
         return n
 
-    def enqueue(self, camera, events=None) -> None:
+    def _outputs(self, slot: int):
+        """Device result tensors of output slot 0 or 1: the U-Net RGB, or the
+        filtered (rgb, depth, alpha) frame."""
+        import torch
+
+        if slot == 0:
+            if self.unet is not None:
+                return (self.rgb_out,)
+            return (self.frgb, self.fdepth, self.falpha)
+        if self._alt is None:
+            self._alt = tuple(torch.empty_like(t) for t in self._outputs(0))
+        return self._alt
+
+    def enqueue(self, camera, events=None, slot: int = 0) -> None:
         """Enqueue one full frame on the current stream (no host sync).
         ``events`` (optional list of 3 CUDA events) marks project / filter /
-        U-Net boundaries for per-stage timing."""
+        U-Net boundaries for per-stage timing.  ``slot`` selects the output
+        buffer set (render_stream alternates two)."""
+        outs = self._outputs(slot)
+        filtered = (self.frgb, self.fdepth, self.falpha) if self.unet is not None else outs
         project_scene(self.scene, camera, self.rp.zbuffer_epsilon_rel, self.bufs, cull=True,
-                      filter_params=self.fp, filtered=(self.frgb, self.fdepth, self.falpha),
+                      filter_params=self.fp, filtered=filtered,
                       unet_in=None if self.unet is None else self.unet_in[0],
                       pyramid=self.pyramid, stage_events=events)
         if self.unet is not None:
-            self.unet.forward(self.unet_in, self.rgb_out)
+            self.unet.forward(self.unet_in, outs[0])
         if events is not None:
             events[-1].record()
 
@@ -103,6 +125,65 @@ class FrameRenderer:
         if self.unet is not None:
             return self._pinned[0].numpy()
         return FrameRGBDA(*(t.numpy() for t in self._pinned))
+
+    def _host_set(self):
+        """One set of pinned host buffers matching the device results."""
+        import torch
+
+        if self.unet is not None:
+            return (torch.empty((self.height, self.width, 3), dtype=torch.float32,
+                                pin_memory=True),)
+        return tuple(torch.empty_like(t, device="cpu", pin_memory=True)
+                     for t in (self.frgb, self.fdepth, self.falpha))
+
+    def render_stream(self, cameras, depth: int = 2):
+        """Pipelined public call: yields each camera's host result, in order.
+
+        Frame i's device->host copy runs on a copy stream from one of two
+        device output sets while frame i+1 (and i+2) compute, so a stream of
+        frames costs max(compute, copy) per frame instead of their sum.  Each
+        yielded array lives in a ring of ``depth + 2`` pinned host buffers and
+        stays valid until the next frame has been yielded -- copy it to keep
+        it longer."""
+        import collections
+
+        import torch
+
+        comp = torch.cuda.current_stream()
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream()
+        copy = self._copy_stream
+        if self._ring is None or len(self._ring) != depth + 2:  # pinned once, reused
+            self._ring = [self._host_set() for _ in range(depth + 2)]
+        ring = self._ring
+        pending = collections.deque()
+
+        def result(item):
+            done, hs = item
+            done.synchronize()
+            if self.unet is not None:
+                return ring[hs][0].numpy()
+            return FrameRGBDA(*(t.numpy() for t in ring[hs]))
+
+        for i, cam in enumerate(cameras):
+            slot, hs = i % 2, i % (depth + 2)
+            if self._copy_done[slot] is not None:
+                comp.wait_event(self._copy_done[slot])  # slot's previous copy-out read it
+            self.enqueue(cam, slot=slot)
+            ready = torch.cuda.Event()
+            ready.record(comp)
+            copy.wait_event(ready)
+            with torch.cuda.stream(copy):
+                for dst, src in zip(ring[hs], self._outputs(slot)):
+                    dst.copy_(src[0, : self.height] if src.dim() == 4 else src, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(copy)
+            self._copy_done[slot] = done
+            pending.append((done, hs))
+            if len(pending) > depth:
+                yield result(pending.popleft())
+        while pending:
+            yield result(pending.popleft())
 
     @property
     def d2h_bytes(self) -> int:
