@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=2, help="cpu_baseline sample frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--views", type=int, default=8, help="camera poses cycled")
+    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
+                    help="N>1: frame-parallel replicas of the scan (default; each rank renders "
+                         "whole frames) or point-sharded frames (min/sum merges, root-side "
+                         "filter + U-Net)")
     return ap.parse_args()
 
 
@@ -235,12 +239,15 @@ def run_b200(args):
         from paper_2502_11618_b200.unet import UNet
 
         unet = UNet.from_config(args.unet, seed=7, device=torch.device("cuda", local))
-    if world > 1:
+    sharded = world > 1 and args.mode == "sharded"
+    if sharded:
         from paper_2502_11618_b200.shard import ShardedRenderer
 
         renderer = ShardedRenderer(grid, args.width, args.height, rank, world, unet=unet)
     else:
         renderer = FrameRenderer(grid, args.width, args.height, unet=unet)
+    # replicas: rank r renders its own frames (views offset by rank)
+    view0 = 0 if sharded else rank * args.steps
     # candidate counts per view (algorithmic bytes of the projection passes)
     n_cand = []
     for cam in cams:
@@ -248,9 +255,8 @@ def run_b200(args):
         s, e = grid.cell_ranges(cells)
         n_cand.append(int((e - s).sum()))
 
-    stream = torch.cuda.current_stream()
     for i in range(args.warmup):
-        renderer.enqueue(cams[i % len(cams)])
+        renderer.enqueue(cams[(view0 + i) % len(cams)])
     torch.cuda.synchronize()
     # ---- device-timed region (inputs resident in HBM) ----
     clocks = ClockSampler(local)
@@ -265,8 +271,14 @@ def run_b200(args):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
     for i in range(args.steps):
-        evs[i][0].record()
-        renderer.enqueue(cams[(args.warmup + i) % len(cams)], events=evs[i][1:])
+        cam = cams[(view0 + args.warmup + i) % len(cams)]
+        if sharded:  # root-side work is on a side stream: no per-stage events
+            renderer.enqueue(cam)
+        else:
+            evs[i][0].record()
+            renderer.enqueue(cam, events=evs[i][1:])
+    if sharded:
+        torch.cuda.current_stream().wait_stream(renderer.side)
     t_end.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -279,26 +291,31 @@ def run_b200(args):
         total_ms = float(t.item())
     renderer.check_flags()
     stage = {k: [] for k in ("cull", "pass1", "pass2", "filter", "unet")}
-    for e in evs:
+    for e in ([] if sharded else evs):
         stage["cull"].append(e[0].elapsed_time(e[1]))
         stage["pass1"].append(e[1].elapsed_time(e[2]))
         stage["pass2"].append(e[2].elapsed_time(e[3]))
         stage["filter"].append(e[3].elapsed_time(e[4]))
         stage["unet"].append(e[4].elapsed_time(e[5]))
+    # frames completed by the whole job in the timed region
+    frames = args.steps * (1 if sharded or world == 1 else world)
     ms = total_ms / args.steps
-    fps = 1e3 / ms
-    cand = [n_cand[(args.warmup + i) % len(cams)] for i in range(args.steps)]
+    fps = frames * 1e3 / total_ms
+    cand = [n_cand[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
     mean_cand = float(np.mean(cand))
     hbm, bf16, bf16s, peak_kind = measured_peaks()
-    t_proj = np.array(stage["pass1"]) + np.array(stage["pass2"])
-    proj_bytes = 27.0 * np.array(cand)  # 12 B pass 1 + 15 B pass 2 per candidate
-    proj_gbs = float(np.mean(proj_bytes / (t_proj * 1e-3)) / 1e9)
-    stages_ms = {k: float(np.mean(v)) for k, v in stage.items()}
-    roofline = {"kernel": "projection (k_frame_pass1 + k_frame_pass2)", "bound": "hbm",
+    proj_gbs = 0.0
+    if not sharded:
+        t_proj = np.array(stage["pass1"]) + np.array(stage["pass2"])
+        proj_bytes = 27.0 * np.array(cand)  # 12 B pass 1 + 15 B pass 2 per candidate
+        proj_gbs = float(np.mean(proj_bytes / (t_proj * 1e-3)) / 1e9)
+    stages_ms = {k: float(np.mean(v)) for k, v in stage.items()} if not sharded else None
+    roofline = None if sharded else {
+                "kernel": "projection (k_frame_pass1 + k_frame_pass2)", "bound": "hbm",
                 "achieved": proj_gbs, "peak": hbm, "unit": "GB/s", "frac": proj_gbs / hbm,
                 "traffic": None, "peak_kind": peak_kind,
                 "algorithmic": "27 B per candidate point"}
-    if unet is not None:
+    if unet is not None and not sharded:
         flops = unet.flops(args.width, renderer.unet_in.shape[1])
         tflops = flops / (stages_ms["unet"] * 1e-3) / 1e12
         roofline_unet = {"kernel": "U-Net (tcgen05 implicit-GEMM convs)", "bound": "tensor",
@@ -313,28 +330,37 @@ def run_b200(args):
     # and its full result comes back to pinned host memory; the copy-out of
     # frame i overlaps the compute of frame i+1 (wall clock over K frames)
     e2e = None
-    if world == 1:
-        for _ in renderer.render_stream([cams[i % len(cams)] for i in range(3)]):
+    if not sharded:
+        for _ in renderer.render_stream([cams[(view0 + i) % len(cams)] for i in range(3)]):
             pass
         torch.cuda.synchronize()
-        seq = [cams[(args.warmup + i) % len(cams)] for i in range(args.steps)]
+        seq = [cams[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
+        if world > 1:
+            torch.distributed.barrier()
         e0 = time.perf_counter()
         n_out = 0
         for _ in renderer.render_stream(seq):
             n_out += 1
-        e_ms = (time.perf_counter() - e0) * 1e3 / n_out
-        e2e = {"value": 1e3 / e_ms, "unit": "frames/s", "api": "FrameRenderer.render_stream",
+        e_s = time.perf_counter() - e0
+        if world > 1:  # slowest rank; every rank delivered n_out frames
+            t = torch.tensor([e_s], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_s = float(t.item())
+        e2e = {"value": n_out * world / e_s, "unit": "frames/s",
+               "api": "FrameRenderer.render_stream",
                "h2d_bytes_per_step": 320,  # camera struct + 6 frustum planes (kernel params)
                "d2h_bytes_per_step": renderer.d2h_bytes}
     line = {
-        "metric": METRIC, "value": fps * (1 if world == 1 else 1), "unit": "frames/s",
+        "metric": METRIC, "value": fps, "unit": "frames/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
+        "vs_baseline": None,
         "dtype": "f64" if unet is None else "f64+bf16",
         "data": "synthetic (seeded multi-station hall scan, random-init U-Net weights)",
         "config": {"workload": workload_name(args), "points": args.points,
                    "width": args.width, "height": args.height, "views": len(cams),
-                   "parallelism": f"point-shard{world}" if world > 1 else "single",
+                   "parallelism": (f"point-shard{world}" if sharded else
+                                   f"frame-replicas{world}" if world > 1 else "single"),
                    "l2": "inputs larger than L2 (scan 15 B/pt)"},
         "gpoints_per_s": mean_cand * fps / 1e9,
         "candidates_mean": mean_cand,

@@ -73,7 +73,14 @@ def merge_accum(accum, root: int, group=None):
 
 
 class ShardedRenderer:
-    """FrameRenderer over one shard of the scan, merged across ranks."""
+    """FrameRenderer over one shard of the scan, merged across ranks.
+
+    Streams: cull, passes and both collectives run on the caller's stream;
+    the root's assemble/filter/U-Net run on a side stream, so the next frame's
+    projection (and its collectives, in which every rank takes part) never
+    waits for a U-Net.  The per-frame pass buffers (minz, accum) alternate
+    between two sets; set k is reused only after the side stream has consumed
+    (and reset) it."""
 
     def __init__(self, grid, width: int, height: int, rank: int, world: int,
                  render_params: RenderParams | None = None,
@@ -92,7 +99,8 @@ class ShardedRenderer:
         offs = shard_cell_offsets(grid._device_field("cell_offsets", np.int64), start, end)
         self.scene = DeviceScene(full.positions[start:end], full.colors[start:end], offs,
                                  grid.origin, grid.cell_size, grid.dims)
-        self.bufs = FrameBuffers(width, height, self.device)
+        self.sets = [FrameBuffers(width, height, self.device) for _ in range(2)]
+        self.bufs = self.sets[0]
         h, w, dev = self.height, self.width, self.device
         self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.fdepth = torch.empty((h, w), dtype=torch.float32, device=dev)
@@ -105,6 +113,8 @@ class ShardedRenderer:
             uh = (h + unet.divisor - 1) // unet.divisor * unet.divisor
             self.unet_in = torch.zeros((1, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
             self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
+        self.side = torch.cuda.Stream()
+        self._consumed = [None, None]  # side-stream event: set k finished + reset
         self.frame_index = 0
 
     @property
@@ -114,32 +124,39 @@ class ShardedRenderer:
         n = 4 + (1 + self.fp.levels_n + (self.unet.launches if self.unet else 0)) / self.world
         return int(round(n))
 
-    def enqueue(self, camera, events=None) -> None:
+    def enqueue(self, camera) -> None:
         """Enqueue one frame (this rank's share) on the current stream."""
+        import torch
+
         lib = _lib.load()
-        st = _lib.stream_ptr()
-        ev = events or [None] * 5
+        main = torch.cuda.current_stream()
+        k = self.frame_index % 2
         root = self.frame_index % self.world
         self.frame_index += 1
+        b = self.sets[k]
+        if self._consumed[k] is not None:
+            main.wait_event(self._consumed[k])
         cam = _lib.make_camera(camera)
         sc = self.scene
+        st = _lib.stream_ptr()
         bits = sc.cull_bits(extract_frustum(camera).planes).data_ptr()
         tl, tc = sc.worklist()
-        if ev[0] is not None:
-            ev[0].record()
         _lib.check(lib.ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
-                                      self.bufs.minz.data_ptr(), st), "frame_pass1")
-        merge_minz(self.bufs.minz, self.group)
-        if ev[1] is not None:
-            ev[1].record()
+                                      b.minz.data_ptr(), st), "frame_pass1")
+        merge_minz(b.minz, self.group)
         _lib.check(lib.ls_frame_pass2(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
-                                      float(self.rp.zbuffer_epsilon_rel), self.bufs.minz.data_ptr(),
-                                      self.bufs.accum.data_ptr(), st), "frame_pass2")
-        merge_accum(self.bufs.accum, root, self.group)
-        if ev[2] is not None:
-            ev[2].record()
-        if self.rank == root:
-            b = self.bufs
+                                      float(self.rp.zbuffer_epsilon_rel), b.minz.data_ptr(),
+                                      b.accum.data_ptr(), st), "frame_pass2")
+        merge_accum(b.accum, root, self.group)
+        if self.rank != root:
+            b.minz.fill_(_lib.INF_BITS)
+            b.accum.zero_()
+            self._consumed[k] = None
+            return
+        merged = torch.cuda.Event()
+        merged.record(main)
+        self.side.wait_event(merged)
+        with torch.cuda.stream(self.side):
             _lib.check(lib.ls_frame_finish(
                 b.minz.data_ptr(), b.accum.data_ptr(), b.width, b.height,
                 _lib.make_filter(self.fp), b.rgb.data_ptr(), b.depth.data_ptr(),
@@ -148,19 +165,19 @@ class ShardedRenderer:
                                                        else self.unet_in[0]),
                 0 if self.unet_in is None else int(self.unet_in.shape[1]),
                 0 if self.unet_in is None else int(self.unet_in.shape[3]), 0.1,
-                self.pyramid.data_ptr(), b.flags.data_ptr(), st), "frame_finish")
-            if ev[3] is not None:
-                ev[3].record()
+                self.pyramid.data_ptr(), b.flags.data_ptr(), _lib.stream_ptr()),
+                "frame_finish")
+            done = torch.cuda.Event()
+            done.record(self.side)
+            self._consumed[k] = done
             if self.unet is not None:
                 self.unet.forward(self.unet_in, self.rgb_out)
-        else:
-            self.bufs.minz.fill_(_lib.INF_BITS)
-            self.bufs.accum.zero_()
-            if ev[3] is not None:
-                ev[3].record()
-        if events is not None:
-            events[-1].record()
+
+    def synchronize(self) -> None:
+        """Wait for this rank's side-stream work (the frames it is root of)."""
+        self.side.synchronize()
 
     def check_flags(self) -> None:
-        if int(self.bufs.flags.item()):
+        self.side.synchronize()
+        if any(int(b.flags.item()) for b in self.sets):
             raise RuntimeError("f32 accumulator bound exceeded")

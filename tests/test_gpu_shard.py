@@ -98,14 +98,22 @@ def test_sharded_renderer_single_rank_group():
     dist.init_process_group("nccl", rank=0, world_size=1,
                             device_id=torch.device("cuda", torch.cuda.current_device()))
     try:
+        from lidarsplat.unet import UNet
+
         cloud, cam, grid = _frame_setup(seed=5)
-        a = ShardedRenderer(grid, cam.width, cam.height, 0, 1)
-        b = FrameRenderer(grid, cam.width, cam.height)
-        for _ in range(2):
-            a.enqueue(cam)
-            b.enqueue(cam)
-        torch.cuda.synchronize()
-        assert torch.equal(a.frgb, b.frgb) and torch.equal(a.falpha, b.falpha)
-        assert torch.equal(a.fdepth, b.fdepth)
+        rng = np.random.default_rng(5)
+        views = [cam] + [random_view(rng, cloud, width=cam.width, height=cam.height)
+                         for _ in range(3)]
+        unet = UNet.from_config("reduced", seed=4)
+        a = ShardedRenderer(grid, cam.width, cam.height, 0, 1, unet=unet)
+        b = FrameRenderer(grid, cam.width, cam.height, unet=unet)
+        for v in views:  # root-side work runs on a side stream; compare every frame
+            a.enqueue(v)
+            b.enqueue(v)
+            torch.cuda.synchronize()
+            assert torch.equal(a.frgb, b.frgb) and torch.equal(a.falpha, b.falpha)
+            assert torch.equal(a.fdepth, b.fdepth)
+            assert torch.equal(a.rgb_out, b.rgb_out)
+        a.check_flags()
     finally:
         dist.destroy_process_group()
