@@ -46,7 +46,8 @@ typedef struct ls_conv_plan ls_conv_plan;
  *   pool    bf16 NHWC 2x2 max pool of y (maxPool2, grad64.ts:203-238)
  *   head    f32 NHWC (batch,H,W,head_c) = sigmoid(head_w[head_c][cout] . y + head_b)
  *           (the final 1x1 conv + sigmoid, unet.ts:183), head_c <= 4
- * Requirements: c0, c1 in {16, 32} or multiples of 64, or c0 = 8 with c1 = 0
+ * Requirements: LS_ACT_LEAKY alpha in [0, 1];
+ * c0, c1 in {16, 32} or multiples of 64, or c0 = 8 with c1 = 0
  * (read as 16 channels whose upper 8 are zero -- TMA out-of-bounds fill --
  * so W rows then hold 16 channels); cout multiple of 16;
  * columns (cout or 4*cout) <= 4096; h, w even when pooling.

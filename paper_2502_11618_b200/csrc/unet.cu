@@ -93,10 +93,19 @@ struct CfgP {
 template <int BN, int CHUNK>
 constexpr int threads_for() { return CfgP<BN, CHUNK>::kThreads; }
 
-__device__ __forceinline__ float apply_act(float v, int act, float alpha) {
-    if (act == LS_ACT_RELU) return v > 0.0f ? v : 0.0f;
-    if (act == LS_ACT_LEAKY) return v > 0.0f ? v : alpha * v;
-    return v;
+// Branch-free activation: max(v, slope * v) with slope 0 (ReLU), alpha (leaky,
+// 0 <= alpha <= 1) or 1 (none) -- the layer's slope is resolved once.
+__device__ __forceinline__ float act_slope(int act, float alpha) {
+    return act == LS_ACT_RELU ? 0.0f : (act == LS_ACT_LEAKY ? alpha : 1.0f);
+}
+
+__device__ __forceinline__ float apply_act(float v, float slope) { return fmaxf(v, slope * v); }
+
+__device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
+    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162 *>(&a);
+    __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162 *>(&b);
+    __nv_bfloat162 m = __hmax2(x, y);
+    return *reinterpret_cast<uint32_t *>(&m);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -333,6 +342,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
         const int quarter = warp & 3;            // TMEM lane quarter this warp may access
         const int m = quarter * 32 + lane;
         const int tx = m % kTW, ty = m / kTW;
+        const float slope = act_slope(p.act, p.alpha);
         uint32_t acc = (uint32_t)eg;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
@@ -370,7 +380,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                         for (int j = 0; j < 4; ++j)
                             v[4 * i4 + j] = apply_act(
                                 fmaf(__uint_as_float(rr[h2 * 16 + 4 * i4 + j]), scv[j], shv[j]),
-                                p.act, p.alpha);
+                                slope);
                     }
                     if (MODE == kHead) {
                         for (int j2 = 0; j2 < p.head_c; ++j2) {
@@ -464,6 +474,270 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// cout = 32 convolutions (the four full-resolution layers).  A 128xNx16 MMA
+// costs max(~45, ~40 + N/4) cycles (scripts/mma_rate.cu), so N = 32 tiles run
+// at 36% of the tensor peak at best.  Here the three kx taps are stacked
+// along N ([kx][co], N = 96) -- each A operand read now feeds 96 columns --
+// and the kx sum moves to the epilogue:
+//     out(r, c) = T0(r, c-1) + T1(r, c) + T2(r, c+1)
+// with lanes c +- 1 of the same 16-lane pixel row (warp shuffles).  A tile is
+// 8 rows x 16 columns of INPUT pixels whose columns 1..14 are outputs (tiles
+// advance by 14 columns); ky stays a descriptor row offset into one (8+2) x 16
+// TMA box per K chunk.  Per K chunk: 3 MMAs of ~56 cycles instead of 9 of
+// ~46, and one halo box instead of three.  Weights stay resident, loaded as
+// nine 32-row blocks from the ABI's [tap][n][c] layout.
+constexpr int kKxCols = 14;  // output columns per tile
+
+template <int CHUNK>
+struct CfgKx {
+    static constexpr uint32_t kRow = CHUNK * 2;
+    static constexpr uint32_t kLayout =
+        CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
+    static constexpr int kN = 96;         // 3 kx x 32 output channels
+    static constexpr int kAcc = 5;        // 5 x 96 TMEM columns
+    static constexpr int kEpiGroups = 4;
+    static constexpr int kThreads = 64 + 128 * kEpiGroups;
+    static constexpr int kTmemCols = 512;
+};
+
+template <int CHUNK, int MODE>
+__global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
+    const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+    const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
+    using C = CfgKx<CHUNK>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    const int S = p.stages;
+    float *sconst = reinterpret_cast<float *>(smem + p.off_const);
+    const float *s_scale = sconst;
+    const float *s_shift = sconst + p.n_total;
+    const float *s_hw = sconst + 2 * p.n_total;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + C::kAcc;
+    uint64_t *bres = tempty + C::kAcc;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
+    const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
+    const float r_tx = 1.0f / (float)p.tiles_x;
+    auto pos = [&](int item, int &img, int &x0, int &y0) {
+        img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
+        const int r = item - img * p.tiles_x * p.tiles_y;
+        const int ty = fdiv(r, p.tiles_x, r_tx);
+        y0 = ty * kTH;
+        x0 = (r - ty * p.tiles_x) * kKxCols;
+    };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, 1);
+            }
+            for (int a = 0; a < C::kAcc; ++a) {
+                mbar_init(tfull + a, 1);
+                mbar_init(tempty + a, 4);
+            }
+            mbar_init(bres, 1);
+            fence_barrier_init();
+            tma_prefetch(&mA0);
+            if (p.c1 > 0) tma_prefetch(&mA1);
+            tma_prefetch(&mB);
+        }
+        __syncwarp();
+        tmem_alloc(tslot, C::kTmemCols);
+    } else if (warp >= 2) {
+        const int t = threadIdx.x - 64;
+        constexpr int kEpiThreads = 128 * C::kEpiGroups;
+        for (int i = t; i < p.n_total; i += kEpiThreads) {
+            sconst[i] = p.scale[i];
+            sconst[p.n_total + i] = p.shift[i];
+        }
+        if (MODE == kHead)
+            for (int i = t; i < p.head_c * p.cout; i += kEpiThreads)
+                sconst[2 * p.n_total + i] = p.head_w[i];
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ------------------------------ TMA producer ------------------------------
+            // resident weights: block (q, ky) = 96 rows [kx][co], from taps kx*3+ky
+            mbar_expect_tx(bres, (uint32_t)(9 * p.nq) * p.b_blk);
+            for (int q = 0; q < p.nq; ++q) {
+                const bool second = q >= p.nq0;
+                const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
+                for (int ky = 0; ky < 3; ++ky)
+                    for (int kx = 0; kx < 3; ++kx)
+                        tma_load_3d(smem + p.off_b + ((q * 3 + ky) * 3 + kx) * p.b_blk, &mB, kc, 0,
+                                    kx * 3 + ky, bres);
+            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            uint32_t it = 0;
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+                int img, x0, y0;
+                pos(item, img, x0, y0);
+                for (int q = 0; q < p.nq; ++q, ++it) {
+                    const bool second = q >= p.nq0;
+                    const int c = (second ? q - p.nq0 : q) * CHUNK;
+                    const int s = (int)(it % (uint32_t)S);
+                    const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    mbar_wait(empty + s, ph ^ 1u);
+                    if (p.dbg & 2) {
+                        mbar_arrive(full + s);
+                        continue;
+                    }
+                    mbar_expect_tx(full + s, p.a_tx);
+                    tma_load_4d(smem + (size_t)s * p.stage_bytes, second ? &mA1 : &mA0, c, x0 - 1,
+                                y0 - 1, img, full + s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ------------------------------- MMA issuer -------------------------------
+            const uint32_t idesc = idesc_bf16(128, C::kN);
+            const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
+            const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
+            mbar_wait(bres, 0);
+            uint32_t it = 0, acc = 0;
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
+                const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
+                mbar_wait(tempty + ab, aph ^ 1u);
+                fence_after_sync();
+                const uint32_t d0 = tmem + ab * C::kN;
+                for (int q = 0; q < p.nq; ++q, ++it) {
+                    const int s = (int)(it % (uint32_t)S);
+                    const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    mbar_wait(full + s, ph);
+                    fence_after_sync();
+                    const uint32_t a_lo = dlo + ((sbase + (uint32_t)s * p.stage_bytes) >> 4);
+                    const uint32_t b_lo = dlo + ((sbase + p.off_b + (uint32_t)(q * 9) * p.b_blk) >> 4);
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+#pragma unroll
+                        for (int j = 0; j < CHUNK / 16; ++j) {
+                            const uint32_t ao = (ky * kTW * C::kRow + 32 * j) / 16;
+                            const uint32_t bo = (ky * C::kN * C::kRow + 32 * j) / 16;
+                            if (!(p.dbg & 1))
+                            mma_bf16(d0, ((uint64_t)dhi << 32) | (a_lo + ao),
+                                     ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
+                                     (q | ky | j) != 0 ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(empty + s);
+                }
+                mma_commit(tfull + ab);
+            }
+        }
+    } else {
+        // --------------------------------- epilogue ---------------------------------
+        const int eg = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + lane;
+        const int tx = m % kTW, ty = m / kTW;  // input pixel of this lane
+        const float slope = act_slope(p.act, p.alpha);
+        uint32_t acc = (uint32_t)eg;
+        for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
+             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
+            int img, x0, y0;
+            pos(item, img, x0, y0);
+            const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
+            mbar_wait(tfull + ab, aph);
+            fence_after_sync();
+            const uint32_t tbase = tmem + ab * C::kN + ((uint32_t)(quarter * 32) << 16);
+            const int gx = x0 + tx - 1, gy = y0 + ty;
+            const bool inner = tx >= 1 && tx <= kKxCols;
+            const bool valid = inner && gx < p.w && gy < p.h;
+            float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const int n = h2 * 16;
+                uint32_t t0[16], t1[16], t2[16];
+                tmem_ld16_async(tbase + (uint32_t)(0 * 32 + n), t0);
+                tmem_ld16_async(tbase + (uint32_t)(1 * 32 + n), t1);
+                tmem_ld16_async(tbase + (uint32_t)(2 * 32 + n), t2);
+                tmem_ld_wait3(t0, t1, t2);
+                if (h2 == 1) {  // item fully read -> hand the TMEM buffer back
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty + ab);
+                }
+                const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
+                const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
+                float v[16];
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                    const float4 sc = sc4[i4], sh = sh4[i4];
+                    const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+                    const float shv[4] = {sh.x, sh.y, sh.z, sh.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int i = 4 * i4 + j;
+                        // T0 of the left neighbour, T2 of the right one
+                        const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(t0[i]), 1);
+                        const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(t2[i]), 1);
+                        const float d = (left + __uint_as_float(t1[i])) + right;
+                        v[i] = apply_act(fmaf(d, scv[j], shv[j]), slope);
+                    }
+                }
+                if (MODE == kHead) {
+                    for (int j2 = 0; j2 < p.head_c; ++j2) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
+                    }
+                    if (!p.y && !p.y_f32) continue;
+                }
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                if (valid) {
+                    const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
+                    if (p.y && !(p.dbg & 4)) st_global_v8(p.y + pix * p.cout + n, pk);
+                    if (p.y_f32) {
+                        float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + n);
+                        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                        dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+                        dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+                    }
+                }
+                if (MODE == kPool) {
+                    // output column gx = x0 + tx - 1 with x0 even: pairs (tx, tx+1), tx odd;
+                    // rows pair as lanes ^16 (ty even / odd in the same warp)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const uint32_t a = hmax2u(pk[i], __shfl_down_sync(0xffffffffu, pk[i], 1));
+                        pk[i] = hmax2u(a, __shfl_xor_sync(0xffffffffu, a, 16));
+                    }
+                    if (valid && (tx & 1) && !(ty & 1)) {
+                        const int64_t pp = ((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
+                        st_global_v8(p.pool + pp * p.cout + n, pk);
+                    }
+                }
+            }
+            if (MODE == kHead && valid) {
+                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
+                for (int j2 = 0; j2 < p.head_c; ++j2) {
+                    const float z = hacc[j2] + __ldg(p.head_b + j2);
+                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                }
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+}
+
 // ------------------------------------------------------------------ host ---
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -526,6 +800,7 @@ struct ls_conv_plan {
     CUtensorMap a0, a1, b;
     ConvParamsP p;
     int bn, chunk, grid, mode;
+    int kind;  // 0: k_conv_p, 1: k_conv_kx (cout = 32, kx taps stacked along N)
     size_t smem;
 };
 
@@ -565,6 +840,48 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
 }
 
+template <int CHUNK, int MODE>
+static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(k_conv_kx<CHUNK, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(kSmemBudget + 2048));
+        if (e != cudaSuccess) return (int)e;
+        attr_done = 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl->grid);
+    cfg.blockDim = dim3((unsigned)CfgKx<CHUNK>::kThreads);
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_kx<CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
+}
+
+template <int CHUNK>
+static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
+    switch (pl->mode) {
+        case kPlain: return launch_kx_m<CHUNK, kPlain>(pl, st);
+        case kPool: return launch_kx_m<CHUNK, kPool>(pl, st);
+        default: return launch_kx_m<CHUNK, kHead>(pl, st);
+    }
+}
+
+// LS_CONV_KX=0 keeps cout = 32 layers on the generic kernel (A/B measurements).
+static bool kx_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_CONV_KX");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 template <int BN, int CHUNK>
 static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
     switch (pl->mode) {
@@ -581,6 +898,92 @@ static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : 1); }
 }  // namespace ls
 
 static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0); }
+
+// Plan of a cout = 32, 3x3 layer on k_conv_kx (null when it does not fit).
+// c0 is the K-chunk channel count of source 0 (8 -> 16), c0_tensor its tensor.
+static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const uint16_t *d_x1,
+                             int c1, int batch, int h, int w, const uint16_t *d_w,
+                             const float *d_scale, const float *d_shift, int act, float alpha,
+                             uint16_t *d_y, float *d_y_f32, uint16_t *d_pool,
+                             const float *d_head_w, const float *d_head_b, int head_c,
+                             float *d_head_out) {
+    using namespace ls::unet;
+    int chunk = 64;
+    while (chunk > 16 && ((c0 % chunk) || (c1 % chunk))) chunk >>= 1;
+    if ((c0 % chunk) || (c1 % chunk)) return nullptr;
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
+    if (!pl) return nullptr;
+    ConvParamsP &p = pl->p;
+    p = ConvParamsP{};
+    p.batch = batch;
+    p.h = h;
+    p.w = w;
+    p.c0 = c0;
+    p.c1 = c1;
+    p.ctot = c0 + c1;
+    p.kxs = 3;
+    p.kxps = 1;
+    p.pad = 1;
+    p.n_total = 32;
+    p.cout = 32;
+    p.act = act;
+    p.alpha = alpha;
+    p.scale = d_scale;
+    p.shift = d_shift;
+    p.y = reinterpret_cast<__nv_bfloat16 *>(d_y);
+    p.y_f32 = d_y_f32;
+    p.pool = reinterpret_cast<__nv_bfloat16 *>(d_pool);
+    p.head_w = d_head_w;
+    p.head_b = d_head_b;
+    p.head_c = head_c;
+    p.head_out = d_head_out;
+    p.dbg = getenv("LS_CONV_DBG") ? atoi(getenv("LS_CONV_DBG")) : 0;
+    p.tiles_x = (w + kKxCols - 1) / kKxCols;
+    p.tiles_y = (h + kTH - 1) / kTH;
+    p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
+    p.n_tiles_n = 1;
+    p.n_items = p.n_tiles_m;
+    p.nq0 = c0 / chunk;
+    p.nq = (c0 + c1) / chunk;
+    const uint32_t row = (uint32_t)chunk * 2;
+    p.a_tx = (uint32_t)(kTW * (kTH + 2)) * row;
+    p.a_bytes = (p.a_tx + 1023u) & ~1023u;
+    p.b_blk = 32u * row;
+    p.resident = 1;
+    const size_t res_bytes = (size_t)9 * p.nq * p.b_blk;
+    const size_t const_bytes =
+        ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
+    const size_t fixed = res_bytes + const_bytes + 512;
+    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.a_bytes) : 0;
+    if (stages < 3) {
+        delete pl;
+        return nullptr;
+    }
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    p.stage_bytes = p.a_bytes;
+    p.off_b = (uint32_t)(stages * p.stage_bytes);
+    p.off_const = (uint32_t)(p.off_b + res_bytes);
+    p.off_pool = (uint32_t)(p.off_const + const_bytes);
+    p.off_bar = p.off_pool;
+    pl->smem = 1024 + p.off_bar + 512;
+    pl->bn = 32;
+    pl->chunk = chunk;
+    pl->kind = 1;
+    pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, kTH + 2);
+    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
+                          chunk, kTH + 2);
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, 32, 9, chunk, 32, 1);
+    if (!ok) {
+        delete pl;
+        return nullptr;
+    }
+    return pl;
+}
 
 extern "C" {
 
@@ -605,12 +1008,23 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         return fail(LS_EINVAL);
     if (c1 < 0 || (c1 > 0 && (!d_x1 || !chunk_ok(c1)))) return fail(LS_EINVAL);
     if (cout < 16 || cout % 16 || (ksize != 1 && ksize != 3)) return fail(LS_EINVAL);
+    // the fused epilogue evaluates leaky ReLU as max(v, alpha * v)
+    if (act == LS_ACT_LEAKY && !(alpha >= 0.0f && alpha <= 1.0f)) return fail(LS_EINVAL);
     if (transposed && (ksize != 1 || c1 != 0 || d_pool || d_head_w)) return fail(LS_EINVAL);
     if (!transposed && ksize != 3) return fail(LS_EINVAL);  // 1x1 convs are fused heads
     if (d_pool && (h % 2 || w % 2)) return fail(LS_EINVAL);
     if (d_head_w && (head_c < 1 || head_c > 4 || !d_head_b || !d_head_out)) return fail(LS_EINVAL);
     const int n_total = transposed ? 4 * cout : cout;
     if (n_total > 4096) return fail(LS_EINVAL);
+    if (!transposed && cout == 32 && kx_enabled()) {
+        ls_conv_plan *pk = plan_kx(d_x0, c0_tensor, c0, d_x1, c1, batch, h, w, d_w, d_scale, d_shift,
+                                   act, alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
+                                   d_head_out);
+        if (pk) {
+            if (status) *status = 0;
+            return pk;
+        }  // no fit: fall through to the generic kernel
+    }
     int bn = n_total >= 256 ? 256 : (n_total >= 128 ? 128 : (n_total >= 64 ? 64 : 32));
     if (n_total % bn) bn = 32;
     // transposed convs are epilogue-bound (K is small, 4x cout outputs per
@@ -622,6 +1036,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
 
     ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
     if (!pl) return fail(LS_EINVAL);
+    pl->kind = 0;
     ConvParamsP &p = pl->p;
     p.batch = batch;
     p.h = h;
@@ -720,6 +1135,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
 int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     if (!pl) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
+    if (pl->kind == 1) {
+        if (pl->chunk == 16) return launch_kx<16>(pl, st);
+        if (pl->chunk == 32) return launch_kx<32>(pl, st);
+        return launch_kx<64>(pl, st);
+    }
 #define LS_CASE(B, K) \
     if (pl->bn == B && pl->chunk == K) return launch_p<B, K>(pl, st);
     LS_CASE(32, 16) LS_CASE(32, 32) LS_CASE(32, 64)

@@ -69,6 +69,10 @@ int main() {
     cudaMalloc(&d, 256 * sizeof(long long));
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    run<96, 64, 1>(d, n_sm);
+    run<96, 32, 1>(d, n_sm);
+    run<80, 64, 1>(d, n_sm);
+    run<112, 64, 1>(d, n_sm);
     run<32, 64, 1>(d, n_sm);
     run<32, 64, 4>(d, n_sm);
     run<32, 32, 4>(d, n_sm);
