@@ -209,6 +209,14 @@ int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64
                     uint8_t *d_keep, uint16_t *d_unet_in, int64_t unet_h, int32_t unet_c,
                     double unet_znear, float *d_pyramid, int32_t *d_flags, void *stream);
 
+/* Bridge input (FE:bridge.ts:31-53 UNetBridgeModel.reconstruct + FE:model/
+ * weights.ts:90-95 normalizeDepth): d_planes is an RGDA tensor's (5,H,W) f32
+ * planes [r, g, b, depth, alpha]; writes the first H*W pixels of the U-Net's
+ * bf16 NHWC input, unet_c channels [r, g, b, zNear/max(d,zNear) (0 if d <= 0),
+ * alpha, 0...] (unet_c even, >= 6; 16 B aligned when a multiple of 8). */
+int ls_unet_pack_rgbda(const float *d_planes, int64_t height, int64_t width, int32_t unet_c,
+                       double unet_znear, uint16_t *d_unet_in, void *stream);
+
 /* Depth filter of an arbitrary (H,W) depth image (0 = empty): the keep mask
  * of filtering.py:124-131 filter_depth_image. */
 int ls_filter_depth_image(const float *d_depth, int64_t height, int64_t width,

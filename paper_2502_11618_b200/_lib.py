@@ -94,6 +94,7 @@ SIGNATURES = {
     "ls_frame_finish": (ctypes.c_int, [_P, _P, _I64, _I64, ctypes.POINTER(LsFilterParams),
                                        _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _D, _P, _P,
                                        _P]),
+    "ls_unet_pack_rgbda": (ctypes.c_int, [_P, _I64, _I64, _I32, _D, _P, _P]),
     "ls_filter_depth_image": (ctypes.c_int, [_P, _I64, _I64, ctypes.POINTER(LsFilterParams),
                                              _P, _P, _P]),
     "ls_depth_filter_frame": (ctypes.c_int, [_P, _P, _P, _I64, _I64,

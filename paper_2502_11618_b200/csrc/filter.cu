@@ -301,12 +301,12 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
 
 // Writes one filtered pixel's U-Net input channels [r g b d' a 0 ...].
 __device__ __forceinline__ void store_unet_px(__nv_bfloat16 *__restrict__ dst, int unet_c, float r,
-                                              float g, float b, float dd, uint8_t a, double znear) {
+                                              float g, float b, float dd, float a, double znear) {
     // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
     const float dn = dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear))) : 0.0f;
     __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
     __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
-    __nv_bfloat162 v45 = __floats2bfloat162_rn((float)a, 0.0f);
+    __nv_bfloat162 v45 = __floats2bfloat162_rn(a, 0.0f);
     if ((unet_c & 7) == 0) {  // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
         uint4 *o4 = reinterpret_cast<uint4 *>(dst);
         o4[0] = make_uint4(*reinterpret_cast<uint32_t *>(&v01), *reinterpret_cast<uint32_t *>(&v23),
@@ -420,6 +420,17 @@ __global__ void __launch_bounds__(256) k_filter_step(
                               o[dx][3], oa[dx], znear);
         }
     }
+}
+
+// Bridge input (FE:bridge.ts:31-53): an RGDA tensor's five f32 planes ->
+// the U-Net's bf16 NHWC input, one thread per pixel.
+__global__ void __launch_bounds__(256) k_pack_rgbda(const float *__restrict__ planes, int64_t n_px,
+                                                    int64_t width, __nv_bfloat16 *__restrict__ out,
+                                                    int unet_c, double znear) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_px;
+         i += (int64_t)gridDim.x * blockDim.x)
+        store_unet_px(out + i * unet_c, unet_c, planes[i], planes[n_px + i], planes[2 * n_px + i],
+                      planes[3 * n_px + i], planes[4 * n_px + i], znear);
 }
 
 inline dim3 step_grid2(int64_t ch, int64_t cw) {
@@ -584,6 +595,19 @@ int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64
                             filter->edge_threshold, nullptr, d_rgb, d_alpha, d_frgb, d_fdepth,
                             d_falpha, d_keep, reinterpret_cast<__nv_bfloat16 *>(d_unet_in),
                             unet_c, unet_znear, st);
+}
+
+int ls_unet_pack_rgbda(const float *d_planes, int64_t height, int64_t width, int32_t unet_c,
+                       double unet_znear, uint16_t *d_unet_in, void *stream) {
+    if (!d_planes || !d_unet_in || height <= 0 || width <= 0 || unet_c < 6 || (unet_c & 1) ||
+        !(unet_znear > 0.0))
+        return LS_EINVAL;
+    if ((unet_c & 7) == 0 && (reinterpret_cast<uintptr_t>(d_unet_in) & 15)) return LS_EINVAL;
+    const int64_t n = height * width;
+    k_pack_rgbda<<<grid_for(n, 256, 8), 256, 0, (cudaStream_t)stream>>>(
+        d_planes, n, width, reinterpret_cast<__nv_bfloat16 *>(d_unet_in), unet_c, unet_znear);
+    LS_LAUNCH_CHECK();
+    return 0;
 }
 
 int ls_filter_depth_image(const float *d_depth, int64_t height, int64_t width,
