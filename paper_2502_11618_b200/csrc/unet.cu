@@ -70,7 +70,6 @@ struct ConvParamsP {
     uint32_t off_const;     // scale[n_total], shift[n_total], head_w (f32)
     uint32_t off_pool;      // (unused: pooling is done with warp shuffles)
     uint32_t off_bar;       // barriers
-    int dbg;                // experiments (LS_CONV_DBG): 1 no MMA, 2 no A/B TMA, 4 no stores
 };
 
 template <int BN, int CHUNK>
@@ -262,10 +261,6 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                         const uint32_t ph = (it / (uint32_t)S) & 1u;
                         mbar_wait(empty + s, ph ^ 1u);
                         uint8_t *st = smem + (size_t)s * p.stage_bytes;
-                        if (p.dbg & 2) {
-                            mbar_arrive(full + s);
-                            continue;
-                        }
                         mbar_expect_tx(full + s, p.kxps * (p.a_tx + (p.resident ? 0u : p.b_blk)));
                         for (int k = 0; k < p.kxps; ++k) {
                             const int kx = kg * p.kxps + k;
@@ -319,7 +314,6 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                                         const uint32_t ao =
                                             k * a_box16 + ((u * kTH + ky) * kTW * C::kRow + 32 * j) / 16;
                                         const uint32_t bo = k * b_blk16 + (ky * BN * C::kRow + 32 * j) / 16;
-                                        if (!(p.dbg & 1))
                                         mma_bf16(d0 + u * BN, ((uint64_t)dhi << 32) | (a_lo + ao),
                                                  ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
                                                  (q | kg | k | ky | j) != 0 ? 1u : 0u);
@@ -404,7 +398,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
                         } else {
                             pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
                         }
-                        if (p.y && !(p.dbg & 4)) st_global_v8(p.y + pix * p.cout + o, pk);
+                        if (p.y) st_global_v8(p.y + pix * p.cout + o, pk);
                         if (p.y_f32) {
                             float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + o);
                             dst[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -489,23 +483,23 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
 // nine 32-row blocks from the ABI's [tap][n][c] layout.
 constexpr int kKxCols = 14;  // output columns per tile
 
-template <int CHUNK>
+template <int CHUNK, int COUT>
 struct CfgKx {
     static constexpr uint32_t kRow = CHUNK * 2;
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
-    static constexpr int kN = 96;         // 3 kx x 32 output channels
-    static constexpr int kAcc = 5;        // 5 x 96 TMEM columns
-    static constexpr int kEpiGroups = 4;
+    static constexpr int kN = 3 * COUT;                  // [kx][co]: 96 or 192 columns
+    static constexpr int kAcc = 480 / kN;                // TMEM buffers: 5 or 2
+    static constexpr int kEpiGroups = kAcc >= 4 ? 4 : kAcc;
     static constexpr int kThreads = 64 + 128 * kEpiGroups;
     static constexpr int kTmemCols = 512;
 };
 
-template <int CHUNK, int MODE>
-__global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
+template <int CHUNK, int COUT, int MODE>
+__global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
-    using C = CfgKx<CHUNK>;
+    using C = CfgKx<CHUNK, COUT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -569,7 +563,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
     if (warp == 0) {
         if (lane == 0) {
             // ------------------------------ TMA producer ------------------------------
-            // resident weights: block (q, ky) = 96 rows [kx][co], from taps kx*3+ky
+            // resident weights: block (q, ky) = 3*COUT rows [kx][co], from taps kx*3+ky
             mbar_expect_tx(bres, (uint32_t)(9 * p.nq) * p.b_blk);
             for (int q = 0; q < p.nq; ++q) {
                 const bool second = q >= p.nq0;
@@ -590,10 +584,6 @@ __global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
                     const int s = (int)(it % (uint32_t)S);
                     const uint32_t ph = (it / (uint32_t)S) & 1u;
                     mbar_wait(empty + s, ph ^ 1u);
-                    if (p.dbg & 2) {
-                        mbar_arrive(full + s);
-                        continue;
-                    }
                     mbar_expect_tx(full + s, p.a_tx);
                     tma_load_4d(smem + (size_t)s * p.stage_bytes, second ? &mA1 : &mA0, c, x0 - 1,
                                 y0 - 1, img, full + s);
@@ -626,7 +616,6 @@ __global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
                         for (int j = 0; j < CHUNK / 16; ++j) {
                             const uint32_t ao = (ky * kTW * C::kRow + 32 * j) / 16;
                             const uint32_t bo = (ky * C::kN * C::kRow + 32 * j) / 16;
-                            if (!(p.dbg & 1))
                             mma_bf16(d0, ((uint64_t)dhi << 32) | (a_lo + ao),
                                      ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
                                      (q | ky | j) != 0 ? 1u : 0u);
@@ -657,15 +646,15 @@ __global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
             const bool inner = tx >= 1 && tx <= kKxCols;
             const bool valid = inner && gx < p.w && gy < p.h;
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll 1
+            for (int h2 = 0; h2 < COUT / 16; ++h2) {
                 const int n = h2 * 16;
                 uint32_t t0[16], t1[16], t2[16];
-                tmem_ld16_async(tbase + (uint32_t)(0 * 32 + n), t0);
-                tmem_ld16_async(tbase + (uint32_t)(1 * 32 + n), t1);
-                tmem_ld16_async(tbase + (uint32_t)(2 * 32 + n), t2);
+                tmem_ld16_async(tbase + (uint32_t)(0 * COUT + n), t0);
+                tmem_ld16_async(tbase + (uint32_t)(1 * COUT + n), t1);
+                tmem_ld16_async(tbase + (uint32_t)(2 * COUT + n), t2);
                 tmem_ld_wait3(t0, t1, t2);
-                if (h2 == 1) {  // item fully read -> hand the TMEM buffer back
+                if (h2 == COUT / 16 - 1) {  // item fully read -> hand the TMEM buffer back
                     fence_before_sync();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(tempty + ab);
@@ -701,7 +690,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK>::kThreads) k_conv_kx(
                 for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
                 if (valid) {
                     const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
-                    if (p.y && !(p.dbg & 4)) st_global_v8(p.y + pix * p.cout + n, pk);
+                    if (p.y) st_global_v8(p.y + pix * p.cout + n, pk);
                     if (p.y_f32) {
                         float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + n);
                         dst[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -840,11 +829,11 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
 }
 
-template <int CHUNK, int MODE>
+template <int CHUNK, int COUT, int MODE>
 static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_kx<CHUNK, MODE>,
+        cudaError_t e = cudaFuncSetAttribute(k_conv_kx<CHUNK, COUT, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
@@ -852,7 +841,7 @@ static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)CfgKx<CHUNK>::kThreads);
+    cfg.blockDim = dim3((unsigned)CfgKx<CHUNK, COUT>::kThreads);
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -860,16 +849,22 @@ static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_kx<CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_kx<CHUNK, COUT, MODE>, pl->a0, pl->a1, pl->b,
+                                   pl->p);
+}
+
+template <int CHUNK, int COUT>
+static int launch_kx_c(const ls_conv_plan *pl, cudaStream_t st) {
+    switch (pl->mode) {
+        case kPlain: return launch_kx_m<CHUNK, COUT, kPlain>(pl, st);
+        case kPool: return launch_kx_m<CHUNK, COUT, kPool>(pl, st);
+        default: return launch_kx_m<CHUNK, COUT, kHead>(pl, st);
+    }
 }
 
 template <int CHUNK>
 static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
-    switch (pl->mode) {
-        case kPlain: return launch_kx_m<CHUNK, kPlain>(pl, st);
-        case kPool: return launch_kx_m<CHUNK, kPool>(pl, st);
-        default: return launch_kx_m<CHUNK, kHead>(pl, st);
-    }
+    return pl->p.cout == 32 ? launch_kx_c<CHUNK, 32>(pl, st) : launch_kx_c<CHUNK, 64>(pl, st);
 }
 
 // LS_CONV_KX=0 keeps cout = 32 layers on the generic kernel (A/B measurements).
@@ -899,10 +894,11 @@ static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : 1); }
 
 static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0); }
 
-// Plan of a cout = 32, 3x3 layer on k_conv_kx (null when it does not fit).
-// c0 is the K-chunk channel count of source 0 (8 -> 16), c0_tensor its tensor.
+// Plan of a cout = 32 / 64, 3x3 layer on k_conv_kx (null when it does not
+// fit).  c0 is the K-chunk channel count of source 0 (8 -> 16), c0_tensor
+// its tensor's.
 static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const uint16_t *d_x1,
-                             int c1, int batch, int h, int w, const uint16_t *d_w,
+                             int c1, int cout, int batch, int h, int w, const uint16_t *d_w,
                              const float *d_scale, const float *d_shift, int act, float alpha,
                              uint16_t *d_y, float *d_y_f32, uint16_t *d_pool,
                              const float *d_head_w, const float *d_head_b, int head_c,
@@ -924,8 +920,8 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     p.kxs = 3;
     p.kxps = 1;
     p.pad = 1;
-    p.n_total = 32;
-    p.cout = 32;
+    p.n_total = cout;
+    p.cout = cout;
     p.act = act;
     p.alpha = alpha;
     p.scale = d_scale;
@@ -937,7 +933,6 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     p.head_b = d_head_b;
     p.head_c = head_c;
     p.head_out = d_head_out;
-    p.dbg = getenv("LS_CONV_DBG") ? atoi(getenv("LS_CONV_DBG")) : 0;
     p.tiles_x = (w + kKxCols - 1) / kKxCols;
     p.tiles_y = (h + kTH - 1) / kTH;
     p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
@@ -948,11 +943,11 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     const uint32_t row = (uint32_t)chunk * 2;
     p.a_tx = (uint32_t)(kTW * (kTH + 2)) * row;
     p.a_bytes = (p.a_tx + 1023u) & ~1023u;
-    p.b_blk = 32u * row;
+    p.b_blk = (uint32_t)cout * row;
     p.resident = 1;
     const size_t res_bytes = (size_t)9 * p.nq * p.b_blk;
     const size_t const_bytes =
-        ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
+        ((size_t)(2 * cout + (d_head_w ? head_c * cout : 0)) * 4 + 1023) & ~size_t(1023);
     const size_t fixed = res_bytes + const_bytes + 512;
     int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.a_bytes) : 0;
     if (stages < 3) {
@@ -967,7 +962,7 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
     p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
-    pl->bn = 32;
+    pl->bn = cout;
     pl->chunk = chunk;
     pl->kind = 1;
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
@@ -977,7 +972,7 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, kTH + 2);
     ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
                           chunk, kTH + 2);
-    ok = ok && encode_wts(&pl->b, d_w, p.ctot, 32, 9, chunk, 32, 1);
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, cout, 9, chunk, cout, 1);
     if (!ok) {
         delete pl;
         return nullptr;
@@ -1016,8 +1011,13 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     if (d_head_w && (head_c < 1 || head_c > 4 || !d_head_b || !d_head_out)) return fail(LS_EINVAL);
     const int n_total = transposed ? 4 * cout : cout;
     if (n_total > 4096) return fail(LS_EINVAL);
-    if (!transposed && cout == 32 && kx_enabled()) {
-        ls_conv_plan *pk = plan_kx(d_x0, c0_tensor, c0, d_x1, c1, batch, h, w, d_w, d_scale, d_shift,
+    // cout = 64 items hold 192 TMEM columns (2 buffers): worth it only when the
+    // K loop is long enough to cover the buffer round trip (measured: K = 128
+    // 94 -> 66 us, K = 32 / 64 slower)
+    const bool kx_fit = cout == 32 || (cout == 64 && c0 + c1 >= 128 && !d_head_w);
+    if (!transposed && kx_fit && kx_enabled()) {
+        ls_conv_plan *pk = plan_kx(d_x0, c0_tensor, c0, d_x1, c1, cout, batch, h, w, d_w, d_scale,
+                                   d_shift,
                                    act, alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
                                    d_head_out);
         if (pk) {
@@ -1059,7 +1059,6 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.head_b = d_head_b;
     p.head_c = head_c;
     p.head_out = d_head_out;
-    p.dbg = getenv("LS_CONV_DBG") ? atoi(getenv("LS_CONV_DBG")) : 0;
     const int kys = p.kxs;
     const size_t const_bytes = ((size_t)(2 * n_total + (d_head_w ? head_c * cout : 0)) * 4 + 1023) &
                                ~size_t(1023);
