@@ -646,7 +646,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
             const bool inner = tx >= 1 && tx <= kKxCols;
             const bool valid = inner && gx < p.w && gy < p.h;
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll 1
+#pragma unroll(COUT == 32 ? 2 : 1)
             for (int h2 = 0; h2 < COUT / 16; ++h2) {
                 const int n = h2 * 16;
                 uint32_t t0[16], t1[16], t2[16];
