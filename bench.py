@@ -315,12 +315,25 @@ def run_b200(args):
                 "achieved": proj_gbs, "peak": hbm, "unit": "GB/s", "frac": proj_gbs / hbm,
                 "traffic": None, "peak_kind": peak_kind,
                 "algorithmic": "27 B per candidate point"}
+    # DRAM traffic of the same kernels from a committed ncu capture (bench.py
+    # cannot profile itself): profiles/r01_traffic.json
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh)
+    if roofline is not None and "projection_dram_bytes_per_candidate" in traffic:
+        roofline["traffic"] = traffic["projection_dram_bytes_per_candidate"] * mean_cand
+        roofline["traffic_source"] = "profiles/r01_traffic.json (ncu dram bytes per candidate x candidates)"
     if unet is not None and not sharded:
         flops = unet.flops(args.width, renderer.unet_in.shape[1])
         tflops = flops / (stages_ms["unet"] * 1e-3) / 1e12
         roofline_unet = {"kernel": "U-Net (tcgen05 implicit-GEMM convs)", "bound": "tensor",
                          "achieved": tflops, "peak": bf16, "unit": "TFLOP/s",
-                         "frac": tflops / bf16, "traffic": None, "peak_kind": peak_kind,
+                         "frac": tflops / bf16,
+                         "traffic": traffic.get("unet_dram_bytes_per_frame"),
+                         "traffic_source": "profiles/r01_traffic.json (ncu dram bytes, 22 launches)",
+                         "peak_kind": peak_kind,
                          "algorithmic": f"{flops / 1e12:.4f} TFLOP per frame"}
         if stages_ms["unet"] > stages_ms["pass1"] + stages_ms["pass2"]:
             roofline, roofline_unet = roofline_unet, roofline
