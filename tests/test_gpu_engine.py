@@ -45,3 +45,22 @@ def test_render_stream_equals_render(with_unet):
     # frames differ from one another (the ring really carried distinct results)
     first = streamed[0] if with_unet else streamed[0][1]
     assert any(not np.array_equal(first, s if with_unet else s[1]) for s in streamed[1:])
+
+
+def test_ply_load_stages_device_copy(tmp_path):
+    """load_ply(device=True) leaves the scan resident: build_grid reuses the
+    staged tensors and renders the same frame as a host-loaded cloud."""
+    from paper_2502_11618_b200 import build_grid, project_points
+    from paper_2502_11618_b200.io import load_ply, save_ply
+
+    rng = np.random.default_rng(8)
+    cloud = random_cloud(rng, 50_000, extent=8.0, offset=-4.0)
+    save_ply(cloud, tmp_path / "c.ply")
+    staged = load_ply(tmp_path / "c.ply", device=True)
+    assert staged._device, "device copy not staged"
+    pos, _ = staged.device_arrays()
+    assert pos.is_cuda and pos.shape == (50_000, 3)
+    cam = random_view(rng, cloud)
+    a = project_points(staged, build_grid(staged, 1.0), cam)
+    b = project_points(cloud, build_grid(cloud, 1.0), cam)
+    assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.depth, b.depth)
