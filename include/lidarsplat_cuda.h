@@ -124,6 +124,16 @@ int ls_assemble(const double *d_minz, const uint64_t *d_accum, int64_t n_pixels,
  *      the render service run on a device-resident scan).
  * ---------------------------------------------------------------------- */
 
+/* Device-scan order (internal to the fast path; the public grid fields keep
+ * the reference's stable order): d_order receives the permutation that sorts
+ * points by (cell id, 30-bit Morton code of the in-cell position).  Applied
+ * to cell-major points it keeps every cell's range and makes each warp tile
+ * spatially compact.  Workspace: ls_morton_order_workspace(n, n_cells). */
+size_t ls_morton_order_workspace(int64_t n, int64_t n_cells);
+int ls_morton_order(const float *d_positions, int64_t n, const double origin[3],
+                    double cell_size, const int64_t dims[3], int64_t *d_order, void *d_workspace,
+                    size_t workspace_bytes, void *stream);
+
 /* Gather the cloud into cell-major order (grid.py:126-127). */
 int ls_gather_points(const float *d_positions, const uint8_t *d_colors, const int64_t *d_order,
                      int64_t n, float *d_sorted_positions, uint8_t *d_sorted_colors,

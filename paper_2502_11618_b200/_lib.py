@@ -76,6 +76,8 @@ SIGNATURES = {
     "ls_filter_keep": (ctypes.c_int, [_P, _I64, _I64, _P, _P, _I64, _I64, _D, _P, _P]),
     "ls_bilinear_fill": (ctypes.c_int, [_P, _I64, _I64, _P, _I64, _I64, _P, _P]),
     "ls_assemble": (ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _P]),
+    "ls_morton_order_workspace": (_SZ, [_I64, _I64]),
+    "ls_morton_order": (ctypes.c_int, [_P, _I64, _P, _D, _P, _P, _P, _SZ, _P]),
     "ls_gather_points": (ctypes.c_int, [_P, _P, _P, _I64, _P, _P, _P]),
     "ls_occupied_workspace": (_SZ, [_I64]),
     "ls_occupied_cells": (ctypes.c_int, [_P, _I64, _P, _P, _P, _P, _SZ, _P]),

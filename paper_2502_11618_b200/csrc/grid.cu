@@ -67,6 +67,46 @@ __global__ void k_gather(const float *__restrict__ pos, const uint8_t *__restric
     }
 }
 
+// Device-scan order (internal; the public grid keeps the reference's stable
+// order): cell-major as before, and inside a cell by the 30-bit Morton code of
+// the point's in-cell position, so consecutive points -- one warp tile -- are
+// spatial neighbours that land on the same or adjacent pixels (the frame
+// passes then merge same-pixel updates inside the warp).  Any in-cell order
+// renders the same frame: both frame reductions are order-free.
+__device__ __forceinline__ uint64_t spread3(uint32_t v) {  // 10 bits -> every 3rd of 30
+    uint64_t x = v & 1023u;
+    x = (x | (x << 16)) & 0x030000FFull;
+    x = (x | (x << 8)) & 0x0300F00Full;
+    x = (x | (x << 4)) & 0x030C30C3ull;
+    x = (x | (x << 2)) & 0x09249249ull;
+    return x;
+}
+
+__global__ void k_morton_keys(const float *__restrict__ pos, int64_t n, double ox, double oy,
+                              double oz, double cell, int64_t dx, int64_t dy, int64_t dz,
+                              uint64_t *__restrict__ keys, int64_t *__restrict__ iota) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double fx = ddiv(dsub((double)pos[3 * k], ox), cell);
+        const double fy = ddiv(dsub((double)pos[3 * k + 1], oy), cell);
+        const double fz = ddiv(dsub((double)pos[3 * k + 2], oz), cell);
+        int64_t ix = __double2ll_rd(fx), iy = __double2ll_rd(fy), iz = __double2ll_rd(fz);
+        // in-cell coordinate quantised to 10 bits (clamped: points on the far
+        // faces of boundary cells)
+        auto q = [](double f, int64_t i) -> uint32_t {
+            const double t = (f - (double)i) * 1024.0;
+            return t <= 0.0 ? 0u : (t >= 1023.0 ? 1023u : (uint32_t)t);
+        };
+        const uint32_t qx = q(fx, ix), qy = q(fy, iy), qz = q(fz, iz);
+        ix = ix < 0 ? 0 : (ix > dx - 1 ? dx - 1 : ix);
+        iy = iy < 0 ? 0 : (iy > dy - 1 ? dy - 1 : iy);
+        iz = iz < 0 ? 0 : (iz > dz - 1 ? dz - 1 : iz);
+        const uint64_t id = (uint64_t)((ix * dy + iy) * dz + iz);
+        keys[k] = (id << 30) | spread3(qx) | (spread3(qy) << 1) | (spread3(qz) << 2);
+        iota[k] = k;
+    }
+}
+
 inline int end_bit_for(int64_t n_cells) {
     int b = 1;
     while (b < 32 && (int64_t(1) << b) < n_cells) ++b;
@@ -129,6 +169,41 @@ int ls_counting_sort(const int64_t *d_ids, int64_t n, int64_t n_cells, int64_t *
                                                                      d_offsets);
     LS_LAUNCH_CHECK();
     return 0;
+}
+
+size_t ls_morton_order_workspace(int64_t n, int64_t n_cells) {
+    if (n <= 0 || n_cells <= 0 || n >= (int64_t(1) << 31) || n_cells > (int64_t(1) << 32))
+        return 0;
+    size_t temp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, temp, (const uint64_t *)nullptr, (uint64_t *)nullptr,
+                                    (const int64_t *)nullptr, (int64_t *)nullptr, (int)n, 0,
+                                    30 + end_bit_for(n_cells));
+    return a256(8 * (size_t)n) * 3 + a256(temp);
+}
+
+int ls_morton_order(const float *d_positions, int64_t n, const double origin[3],
+                    double cell_size, const int64_t dims[3], int64_t *d_order, void *d_workspace,
+                    size_t workspace_bytes, void *stream) {
+    if (n <= 0 || cell_size <= 0 || !origin || !dims || !d_order) return LS_EINVAL;
+    const int64_t n_cells = dims[0] * dims[1] * dims[2];
+    const size_t need = ls_morton_order_workspace(n, n_cells);
+    if (need == 0 || workspace_bytes < need) return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    char *w = (char *)d_workspace;
+    uint64_t *keys_in = (uint64_t *)w;
+    w += a256(8 * (size_t)n);
+    uint64_t *keys_out = (uint64_t *)w;
+    w += a256(8 * (size_t)n);
+    int64_t *iota = (int64_t *)w;
+    w += a256(8 * (size_t)n);
+    size_t temp = need - 3 * a256(8 * (size_t)n);
+    k_morton_keys<<<grid_for(n, 256), 256, 0, st>>>(d_positions, n, origin[0], origin[1],
+                                                    origin[2], cell_size, dims[0], dims[1],
+                                                    dims[2], keys_in, iota);
+    LS_LAUNCH_CHECK();
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(w, temp, keys_in, keys_out, iota, d_order,
+                                                    (int)n, 0, 30 + end_bit_for(n_cells), st);
+    return (int)e;
 }
 
 int ls_gather_points(const float *d_positions, const uint8_t *d_colors, const int64_t *d_order,

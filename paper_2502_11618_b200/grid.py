@@ -12,6 +12,8 @@ ascending cell ids as the reference.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -20,6 +22,7 @@ from .errors import InvalidCloudError
 from .geometry import Frustum
 
 MAX_CELLS = 1 << 31
+USE_MORTON = os.environ.get("LS_MORTON", "1") != "0"
 CULL_SLACK = 1e-7  # reference grid.py:22
 
 
@@ -179,13 +182,38 @@ class UniformGrid:
         return t
 
     def scene(self) -> DeviceScene:
-        """The resident device scan used by the frame passes."""
+        """The resident device scan used by the frame passes: cell-major like
+        the public fields, and inside each cell in Morton order of the point's
+        in-cell position (ls_morton_order), so a warp tile is spatially compact
+        (LS_MORTON=0 keeps the reference's in-cell order; frames are identical
+        either way -- both frame reductions are order-free)."""
         if self._scene is None:
-            self._scene = DeviceScene(
-                self._device_field("sorted_positions", np.float32),
-                self._device_field("sorted_colors", np.uint8),
-                self._device_field("cell_offsets", np.int64),
-                self._origin, self._cell_size, self._dims)
+            import torch
+
+            pos = self._device_field("sorted_positions", np.float32)
+            col = self._device_field("sorted_colors", np.uint8)
+            n = int(pos.shape[0])
+            if USE_MORTON and n > 0:
+                lib = _lib.load()
+                dims = np.ascontiguousarray(self._dims, np.int64)
+                origin = np.ascontiguousarray(self._origin, np.float64)
+                ws_bytes = lib.ls_morton_order_workspace(n, int(dims.prod()))
+                if ws_bytes:
+                    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=pos.device)
+                    order = torch.empty(n, dtype=torch.int64, device=pos.device)
+                    st = _lib.stream_ptr()
+                    _lib.check(lib.ls_morton_order(pos.data_ptr(), n, origin.ctypes.data,
+                                                   float(self._cell_size), dims.ctypes.data,
+                                                   order.data_ptr(), ws.data_ptr(), ws_bytes, st),
+                               "morton_order")
+                    del ws
+                    mpos, mcol = torch.empty_like(pos), torch.empty_like(col)
+                    _lib.check(lib.ls_gather_points(pos.data_ptr(), col.data_ptr(),
+                                                    order.data_ptr(), n, mpos.data_ptr(),
+                                                    mcol.data_ptr(), st), "gather_points")
+                    pos, col = mpos, mcol
+            self._scene = DeviceScene(pos, col, self._device_field("cell_offsets", np.int64),
+                                      self._origin, self._cell_size, self._dims)
         return self._scene
 
 
