@@ -236,6 +236,11 @@ __device__ __forceinline__ uint32_t color_byte(const uint32_t (&W)[3], int b) {
     return (W[b >> 2] >> (8 * (b & 3))) & 0xffu;
 }
 
+__device__ __forceinline__ uint32_t color_byte3(uint3 W, int b) {
+    const uint32_t w = (b >> 2) == 0 ? W.x : ((b >> 2) == 1 ? W.y : W.z);
+    return (w >> (8 * (b & 3))) & 0xffu;
+}
+
 __device__ __forceinline__ void red_min_u64(unsigned long long *p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -350,16 +355,16 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         it.base = tile * LS_TILE_POINTS + 4 * lane;
         it.full = full(tile);
         it.st = ring + q * R::kStage;
-        uint32_t W[3] = {0u, 0u, 0u};
+        uint3 W = make_uint3(0u, 0u, 0u);  // the lane's 12 colour bytes (by value)
         if (MODE != kXyz) {
             if (it.full && col_bulk) {
                 const uint32_t *c4 = reinterpret_cast<const uint32_t *>(it.st + kPosBytes) + 3 * lane;
-                W[0] = c4[0];
-                W[1] = c4[1];
-                W[2] = c4[2];
+                W = make_uint3(c4[0], c4[1], c4[2]);
             } else {
+                uint32_t w3[3];
                 const int64_t rem = s.n - it.base;
-                load_colors(s, it.base, rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0), W);
+                load_colors(s, it.base, rem >= 4 ? 4 : (rem > 0 ? (int)rem : 0), w3);
+                W = make_uint3(w3[0], w3[1], w3[2]);
             }
         }
         body(it, W);
@@ -398,6 +403,31 @@ __device__ __forceinline__ void drop_culled(const SceneArgs &s, const uint32_t *
         if (pix[k] >= 0 && !point_kept(s, bits, c0, c1, it.base + k)) pix[k] = -1;
 }
 
+// ---- same-pixel merging inside a lane (pass 2) ---------------------------
+// A lane's 4 points are consecutive in the Morton-ordered scan; above ~1
+// point per pixel they often share a pixel.  Folding a later point into an
+// earlier one on the same pixel is exact (integer colour sums) and saves its
+// vector atomic.  (Measured and dropped: the same fold for pass 1's minimum,
+// and cross-lane grouping with match.any -- both cost more than they saved.)
+__device__ __forceinline__ void merge_lane_sum(int64_t (&pix)[4], uint32_t (&sum)[4][4]) {
+#pragma unroll
+    for (int k = 1; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < k; ++j)
+            if (pix[k] >= 0 && pix[k] == pix[j]) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) sum[j][c] += sum[k][c];
+                pix[k] = -1;
+            }
+}
+
+// {r, g, b, n} into a pixel's f32 accumulator: one 16 B vector reduction.
+__device__ __forceinline__ void red_add_v4c(float *p, float r, float g, float b, float n) {
+    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(r),
+                 "f"(g), "f"(b), "f"(n)
+                 : "memory");
+}
+
 constexpr int kPass1Stages = 2, kPass2Stages = 2;
 constexpr size_t kSmem1 = TileRing<kPass1Stages, kXyz>::kBytes;
 constexpr size_t kSmem2 = TileRing<kPass2Stages, kXyzRgb>::kBytes;
@@ -409,8 +439,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count,
                                                      unsigned long long *__restrict__ minz) {
-    for_each_item<kPass1Stages, kXyz>(s, list, count, [&](const Item &it,
-                                                                 const uint32_t (&)[3]) {
+    for_each_item<kPass1Stages, kXyz>(s, list, count, [&](const Item &it, uint3) {
         float P[12];
         const int cnt = item_points(s, it, P);
         int64_t pix[4];
@@ -439,8 +468,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
                                                      float *__restrict__ acc) {
-    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, [&](const Item &it,
-                                                                    const uint32_t (&W)[3]) {
+    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, [&](const Item &it, uint3 W) {
         float P[12];
         const int cnt = item_points(s, it, P);
         int64_t pix[4];
@@ -451,13 +479,22 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;
+        uint32_t sum[4][4];  // r, g, b, count of the kept points
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (pix[k] < 0) continue;
-            if (!(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope))) continue;
-            red_add_v4f32(acc + 4 * pix[k], (float)color_byte(W, 3 * k),
-                          (float)color_byte(W, 3 * k + 1), (float)color_byte(W, 3 * k + 2));
+            if (pix[k] >= 0 && !(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope)))
+                pix[k] = -1;
+            sum[k][0] = color_byte3(W, 3 * k);
+            sum[k][1] = color_byte3(W, 3 * k + 1);
+            sum[k][2] = color_byte3(W, 3 * k + 2);
+            sum[k][3] = 1u;
         }
+        merge_lane_sum(pix, sum);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (pix[k] >= 0)
+                red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
+                            (float)sum[k][3]);
     });
 }
 
