@@ -178,6 +178,12 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
  * work list is built first (ls_tile_worklist).
  * d_minz_bits: (H*W) u64, the f64 bit pattern of the running minimum,
  *   must hold +inf (0x7FF0000000000000) on entry.
+ * d_cache: NULL (pass 2 re-projects every candidate), or
+ *   ls_frame_cache_bytes(scene) bytes of 16 B aligned scratch: pass 1 then
+ *   records each candidate's pixel and f32-rounded-down depth and pass 2
+ *   decides from them (a candidate within one f32 ulp of the soft z-buffer
+ *   threshold re-derives its exact f64 depth).  Same frame either way.
+ *   Requires W*H < 2^32 - 1.
  * d_accum4: (H*W x 4) f32 accumulators {sum r, sum g, sum b, count}, zero on
  *   entry, one 16 B vector atomic per kept point.  Integer-valued f32 adds
  *   are exact and order-free while every field stays < 2^24 (guaranteed while
@@ -185,17 +191,22 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
  *   frame where a field reached 2^24. */
 int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
                      uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                     uint64_t *d_minz_bits, float *d_accum4, void *stream);
+                     uint64_t *d_minz_bits, uint32_t *d_cache, float *d_accum4, void *stream);
+
+/* Bytes of the optional pass-1 -> pass-2 cache: 1 KB per warp tile. */
+size_t ls_frame_cache_bytes(const ls_scene *scene);
 
 /* Pass 1 only / pass 2 only of ls_frame_project over an existing work list
- * (d_list NULL = all tiles).  Multi-GPU: an all-reduce MIN of d_minz_bits
- * runs between them, a reduce SUM of d_accum4 after. */
+ * (d_list NULL = all tiles); with a cache both passes must see the same list.
+ * Multi-GPU: an all-reduce MIN of d_minz_bits runs between them, a reduce SUM
+ * of d_accum4 after. */
 int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
-                   void *stream);
+                   uint32_t *d_cache, void *stream);
 int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                   const uint64_t *d_minz_bits, float *d_accum4, void *stream);
+                   const uint64_t *d_minz_bits, const uint32_t *d_cache, float *d_accum4,
+                   void *stream);
 
 /* Level sizes of the min pyramid (filtering.py:67-83); returns the float
  * count of the workspace ls_frame_finish needs for levels 0..L-1. */

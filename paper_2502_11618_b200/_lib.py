@@ -87,11 +87,12 @@ SIGNATURES = {
     "ls_cull_compact": (ctypes.c_int, [_P, _P, _I64, _P, _P, _P, _SZ, _P]),
     "ls_tile_worklist": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _P, _P, _P]),
     "ls_frame_project": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _P, _P,
-                                        ctypes.POINTER(LsCamera), _D, _P, _P, _P]),
+                                        ctypes.POINTER(LsCamera), _D, _P, _P, _P, _P]),
+    "ls_frame_cache_bytes": (_SZ, [ctypes.POINTER(LsScene)]),
     "ls_frame_pass1": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _P, _P,
-                                      ctypes.POINTER(LsCamera), _P, _P]),
+                                      ctypes.POINTER(LsCamera), _P, _P, _P]),
     "ls_frame_pass2": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _P, _P,
-                                      ctypes.POINTER(LsCamera), _D, _P, _P, _P]),
+                                      ctypes.POINTER(LsCamera), _D, _P, _P, _P, _P]),
     "ls_pyramid_floats": (_I64, [_I64, _I64, _I32]),
     "ls_frame_finish": (ctypes.c_int, [_P, _P, _I64, _I64, ctypes.POINTER(LsFilterParams),
                                        _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _D, _P, _P,

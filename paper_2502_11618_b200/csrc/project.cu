@@ -264,11 +264,14 @@ __device__ __forceinline__ void red_add_v4f32(float *p, float r, float g, float 
 // both passes live off the L1 that the rest of the SM's 256 KB provides.
 constexpr int kPassWarps = 8;  // 256-thread CTAs
 constexpr int kPosBytes = LS_TILE_POINTS * 12, kColBytes = LS_TILE_POINTS * 3;
-enum RingMode { kXyz = 0, kXyzRgb = 1 };
+constexpr int kCacheBytes = LS_TILE_POINTS * 8;  // [128 x u32 pixel][128 x f32 depth]
+// kXyz: pass 1 | kXyzRgb: pass 2 recomputing | kCacheRgb: pass 2 from the cache
+enum RingMode { kXyz = 0, kXyzRgb = 1, kCacheRgb = 2 };
 
 template <int S, int MODE>
 struct TileRing {
-    static constexpr int kStage = kPosBytes + (MODE == kXyz ? 0 : kColBytes);
+    static constexpr int kMain = MODE == kCacheRgb ? kCacheBytes : kPosBytes;
+    static constexpr int kStage = kMain + (MODE == kXyz ? 0 : kColBytes);
     static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8 + 4);
 };
 
@@ -284,6 +287,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // What the body of a pass sees for one work item.
 struct Item {
     uint32_t e;         // work-list entry (tile | kMixed)
+    int64_t index;      // position in the work list (the item's cache block)
     int64_t base;       // first point of this lane
     bool full;          // complete tile (all 128 points exist)
     const uint8_t *st;  // the item's smem stage
@@ -291,7 +295,8 @@ struct Item {
 
 template <int S, int MODE, typename F>
 __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t *__restrict__ list,
-                                              const uint32_t *__restrict__ count, F &&body) {
+                                              const uint32_t *__restrict__ count,
+                                              const uint32_t *__restrict__ cache, F &&body) {
     using R = TileRing<S, MODE>;
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -324,18 +329,23 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         }
         return __shfl_sync(0xffffffffu, ecur, (int)(j & 31));
     };
-    auto issue = [&](uint32_t e, int q) {  // lane 0 only
+    auto issue = [&](uint32_t e, int64_t j, int q) {  // lane 0 only
         const int64_t tile = e & ~kMixed;
         ents[q] = e;
-        if (!full(tile)) {
+        const bool f = full(tile);
+        // the cache block is always complete (pass 1 writes all 128 slots)
+        if (!f && MODE != kCacheRgb) {
             umma::mbar_arrive(&bars[q]);
             return;
         }
-        const bool rgb = MODE == kXyzRgb && col_bulk;
-        umma::mbar_expect_tx(&bars[q], kPosBytes + (rgb ? kColBytes : 0));
+        const bool rgb = MODE != kXyz && f && col_bulk;
+        umma::mbar_expect_tx(&bars[q], R::kMain + (rgb ? kColBytes : 0));
         uint8_t *dst = ring + q * R::kStage;
-        bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q]);
-        if (rgb) bulk_g2s(dst + kPosBytes, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q]);
+        if (MODE == kCacheRgb)
+            bulk_g2s(dst, cache + (w0 + j * nw) * (kCacheBytes / 4), kCacheBytes, &bars[q]);
+        else
+            bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q]);
+        if (rgb) bulk_g2s(dst + R::kMain, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q]);
     };
     if (lane == 0) {
         for (int q = 0; q < S; ++q) umma::mbar_init(&bars[q], 1);
@@ -343,7 +353,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
     }
     for (int q = 0; q < S && q < nj; ++q) {
         const uint32_t e = entry(q);
-        if (lane == 0) issue(e, q);
+        if (lane == 0) issue(e, q, q);
     }
     __syncwarp();
     for (int64_t j = 0; j < nj; ++j) {
@@ -351,6 +361,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         umma::mbar_wait_spin(&bars[q], (uint32_t)((j / S) & 1));
         Item it;
         it.e = ents[q];
+        it.index = w0 + j * nw;
         const int64_t tile = it.e & ~kMixed;
         it.base = tile * LS_TILE_POINTS + 4 * lane;
         it.full = full(tile);
@@ -358,7 +369,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         uint3 W = make_uint3(0u, 0u, 0u);  // the lane's 12 colour bytes (by value)
         if (MODE != kXyz) {
             if (it.full && col_bulk) {
-                const uint32_t *c4 = reinterpret_cast<const uint32_t *>(it.st + kPosBytes) + 3 * lane;
+                const uint32_t *c4 = reinterpret_cast<const uint32_t *>(it.st + R::kMain) + 3 * lane;
                 W = make_uint3(c4[0], c4[1], c4[2]);
             } else {
                 uint32_t w3[3];
@@ -374,7 +385,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
             if (lane == 0) {
                 // the lanes' generic-proxy reads of stage q precede the async refill
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue(en, q);
+                issue(en, j + S, q);
             }
         }
     }
@@ -429,23 +440,40 @@ __device__ __forceinline__ void red_add_v4c(float *p, float r, float g, float b,
 }
 
 constexpr int kPass1Stages = 2, kPass2Stages = 2;
+constexpr uint32_t kNoPixel = 0xFFFFFFFFu;
 constexpr size_t kSmem1 = TileRing<kPass1Stages, kXyz>::kBytes;
 constexpr size_t kSmem2 = TileRing<kPass2Stages, kXyzRgb>::kBytes;
+constexpr size_t kSmem2c = TileRing<kPass2Stages, kCacheRgb>::kBytes;
 
 // Pass 1: per-pixel minimum depth.  A (possibly stale) L1 read of the pixel's
 // current minimum filters out points that cannot improve it before the atomic.
+// With a cache, every slot's pixel (kNoPixel when rejected) and its depth
+// rounded toward -inf to f32 are also recorded, one 1 KB block per work item.
 __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ bits,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count,
-                                                     unsigned long long *__restrict__ minz) {
-    for_each_item<kPass1Stages, kXyz>(s, list, count, [&](const Item &it, uint3) {
+                                                     unsigned long long *__restrict__ minz,
+                                                     uint32_t *__restrict__ cache) {
+    for_each_item<kPass1Stages, kXyz>(s, list, count, nullptr, [&](const Item &it, uint3) {
         float P[12];
         const int cnt = item_points(s, it, P);
         int64_t pix[4];
         double zc[4];
         project4(P, cnt, c, pix, zc);
         drop_culled(s, bits, it, pix);
+        if (cache) {
+            const int lane = threadIdx.x & 31;
+            uint32_t *blk = cache + it.index * (kCacheBytes / 4);
+            reinterpret_cast<uint4 *>(blk)[lane] =
+                make_uint4(pix[0] >= 0 ? (uint32_t)pix[0] : kNoPixel,
+                           pix[1] >= 0 ? (uint32_t)pix[1] : kNoPixel,
+                           pix[2] >= 0 ? (uint32_t)pix[2] : kNoPixel,
+                           pix[3] >= 0 ? (uint32_t)pix[3] : kNoPixel);
+            reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
+                make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
+                            __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+        }
         unsigned long long key[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) key[k] = (unsigned long long)__double_as_longlong(zc[k]);
@@ -459,16 +487,14 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
     });
 }
 
-// Pass 2: pixel and depth recomputed from the points (cheaper than the
-// reference's 16 B/candidate pix/z cache round trip; a cached variant was
-// measured no faster -- pass 2 is bound by the minz gathers and atomics).
+// Pass 2, recompute mode: pixel and depth again from the points.
 __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ bits,
                                                      const uint32_t *__restrict__ list,
                                                      const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
                                                      float *__restrict__ acc) {
-    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, [&](const Item &it, uint3 W) {
+    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, nullptr, [&](const Item &it, uint3 W) {
         float P[12];
         const int cnt = item_points(s, it, P);
         int64_t pix[4];
@@ -484,6 +510,58 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
         for (int k = 0; k < 4; ++k) {
             if (pix[k] >= 0 && !(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope)))
                 pix[k] = -1;
+            sum[k][0] = color_byte3(W, 3 * k);
+            sum[k][1] = color_byte3(W, 3 * k + 1);
+            sum[k][2] = color_byte3(W, 3 * k + 2);
+            sum[k][3] = 1u;
+        }
+        merge_lane_sum(pix, sum);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (pix[k] >= 0)
+                red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
+                            (float)sum[k][3]);
+    });
+}
+
+// Pass 2, cached mode: no projection (pass 2 is instruction-issue bound once
+// the scan is Morton ordered).  With T = minz * (1 + eps) in f64 and the
+// cached zlo = RD_f32(zc) <= zc <= nextup(zlo): nextup(zlo) <= T keeps,
+// zlo > T drops, and only a slot within one f32 ulp of T re-derives its
+// exact f64 depth from the point -- the same decision as re-projecting.
+__global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam c,
+                                                            const uint32_t *__restrict__ list,
+                                                            const uint32_t *__restrict__ count,
+                                                            const uint32_t *__restrict__ cache,
+                                                            double ope,
+                                                            const unsigned long long *__restrict__ minz,
+                                                            float *__restrict__ acc) {
+    const int lane = threadIdx.x & 31;
+    for_each_item<kPass2Stages, kCacheRgb>(s, list, count, cache, [&](const Item &it, uint3 W) {
+        const uint4 pw = reinterpret_cast<const uint4 *>(it.st)[lane];
+        const float4 zw = reinterpret_cast<const float4 *>(it.st + 4 * LS_TILE_POINTS)[lane];
+        int64_t pix[4] = {pw.x == kNoPixel ? -1 : (int64_t)pw.x, pw.y == kNoPixel ? -1 : (int64_t)pw.y,
+                          pw.z == kNoPixel ? -1 : (int64_t)pw.z, pw.w == kNoPixel ? -1 : (int64_t)pw.w};
+        const float zlo[4] = {zw.x, zw.y, zw.z, zw.w};
+        unsigned long long m[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;
+        uint32_t sum[4][4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (pix[k] >= 0) {
+                const double t = dmul(__longlong_as_double((long long)m[k]), ope);
+                bool keep = (double)__int_as_float(__float_as_int(zlo[k]) + 1) <= t;
+                if (!keep && !((double)zlo[k] > t)) {  // within one f32 ulp: exact depth
+                    const float *p = s.pos + 3 * (it.base + k);
+                    const double x = (double)__ldg(p), y = (double)__ldg(p + 1),
+                                 z = (double)__ldg(p + 2);
+                    const double zc =
+                        dadd(dadd(dadd(dmul(c.r[6], x), dmul(c.r[7], y)), dmul(c.r[8], z)), c.t[2]);
+                    keep = zc <= t;
+                }
+                if (!keep) pix[k] = -1;
+            }
             sum[k][0] = color_byte3(W, 3 * k);
             sum[k][1] = color_byte3(W, 3 * k + 1);
             sum[k][2] = color_byte3(W, 3 * k + 2);
@@ -654,40 +732,61 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
     return 0;
 }
 
+size_t ls_frame_cache_bytes(const ls_scene *scene) {
+    if (!scene || scene->n_points <= 0) return 0;
+    return (size_t)((scene->n_points + LS_TILE_POINTS - 1) / LS_TILE_POINTS) * kCacheBytes;
+}
+
+static bool cache_ok(const ls_camera *cam, const void *d_cache) {
+    // u32 pixel slots with kNoPixel reserved; 16 B vector stores / bulk copies
+    return !d_cache || (cam->width * cam->height < (int64_t)kNoPixel &&
+                        (reinterpret_cast<uintptr_t>(d_cache) & 15) == 0);
+}
+
 int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
-                   void *stream) {
-    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)))
+                   uint32_t *d_cache, void *stream) {
+    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)) ||
+        !cache_ok(cam, d_cache))
         return LS_EINVAL;
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
     k_frame_pass1<<<frame_grid(k_frame_pass1, kSmem1, a.n_tiles), 256, kSmem1,
                     (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
-                                            (unsigned long long *)d_minz_bits);
+                                            (unsigned long long *)d_minz_bits, d_cache);
     LS_LAUNCH_CHECK();
     return 0;
 }
 
 int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                   const uint64_t *d_minz_bits, float *d_accum4, void *stream) {
-    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)))
+                   const uint64_t *d_minz_bits, const uint32_t *d_cache, float *d_accum4,
+                   void *stream) {
+    if (!scene_ok(scene, d_list) || !camera_ok(cam) || (d_list && (!d_count || !d_keep_bits)) ||
+        !cache_ok(cam, d_cache))
         return LS_EINVAL;
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    k_frame_pass2<<<frame_grid(k_frame_pass2, kSmem2, a.n_tiles), 256, kSmem2,
-                    (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
-                                            1.0 + eps_rel, (const unsigned long long *)d_minz_bits,
-                                            d_accum4);
+    const double ope = 1.0 + eps_rel;
+    if (d_cache)
+        k_frame_pass2_cached<<<frame_grid(k_frame_pass2_cached, kSmem2c, a.n_tiles), 256, kSmem2c,
+                               (cudaStream_t)stream>>>(a, make_cam(*cam), d_list, d_count, d_cache,
+                                                       ope, (const unsigned long long *)d_minz_bits,
+                                                       d_accum4);
+    else
+        k_frame_pass2<<<frame_grid(k_frame_pass2, kSmem2, a.n_tiles), 256, kSmem2,
+                        (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
+                                                ope, (const unsigned long long *)d_minz_bits,
+                                                d_accum4);
     LS_LAUNCH_CHECK();
     return 0;
 }
 
 int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
                      uint32_t *d_count, const ls_camera *cam, double eps_rel,
-                     uint64_t *d_minz_bits, float *d_accum4, void *stream) {
+                     uint64_t *d_minz_bits, uint32_t *d_cache, float *d_accum4, void *stream) {
     int rc = 0;
     if (d_keep_bits) {
         rc = ls_tile_worklist(scene, d_keep_bits, d_list, d_count, stream);
@@ -696,9 +795,9 @@ int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
         d_list = nullptr;
         d_count = nullptr;
     }
-    rc = ls_frame_pass1(scene, d_keep_bits, d_list, d_count, cam, d_minz_bits, stream);
+    rc = ls_frame_pass1(scene, d_keep_bits, d_list, d_count, cam, d_minz_bits, d_cache, stream);
     if (rc) return rc;
-    return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits,
+    return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits, d_cache,
                           d_accum4, stream);
 }
 

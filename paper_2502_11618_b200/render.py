@@ -14,6 +14,7 @@ backend-protocol twins).  Both return frames identical to the reference's.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -113,6 +114,27 @@ class FrameBuffers:
         self.flags = torch.zeros(1, dtype=torch.int32, device=device)
 
 
+# Pass-1 -> pass-2 cache (ls_frame_cache_bytes): pass 2 decides from each
+# candidate's cached pixel + f32 depth instead of re-projecting.  Frames are
+# identical either way; LS_FRAME_CACHE=0 selects re-projection.
+USE_FRAME_CACHE = os.environ.get("LS_FRAME_CACHE", "1") != "0"
+
+
+def frame_cache(scene, camera: CameraModel):
+    """The scene's pass-1 -> pass-2 cache (allocated once per scene), or None
+    when disabled or the frame is too large for u32 pixel slots."""
+    if not USE_FRAME_CACHE or camera.width * camera.height >= 0xFFFFFFFF:
+        return None
+    c = getattr(scene, "_frame_cache", None)
+    if c is None:
+        import torch
+
+        nbytes = int(_lib.load().ls_frame_cache_bytes(scene.struct))
+        c = torch.empty(max(nbytes // 4, 4), dtype=torch.int32, device=_lib.device())
+        scene._frame_cache = c
+    return c
+
+
 def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs: FrameBuffers,
                   cull: bool = True, filter_params=None, filtered=None, keep=None,
                   unet_in=None, unet_znear: float = 0.1, pyramid=None,
@@ -132,12 +154,13 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
         lst, cnt = tl.data_ptr(), tc.data_ptr()
     if ev[0] is not None:
         ev[0].record()
-    _lib.check(lib.ls_frame_pass1(scene.struct, bits, lst, cnt, cam, bufs.minz.data_ptr(), st),
-               "frame_pass1")
+    cache = _lib.ptr(frame_cache(scene, camera))
+    _lib.check(lib.ls_frame_pass1(scene.struct, bits, lst, cnt, cam, bufs.minz.data_ptr(), cache,
+                                  st), "frame_pass1")
     if ev[1] is not None:
         ev[1].record()
     _lib.check(lib.ls_frame_pass2(scene.struct, bits, lst, cnt, cam, float(eps_rel),
-                                  bufs.minz.data_ptr(), bufs.accum.data_ptr(), st),
+                                  bufs.minz.data_ptr(), cache, bufs.accum.data_ptr(), st),
                "frame_pass2")
     if ev[2] is not None:
         ev[2].record()

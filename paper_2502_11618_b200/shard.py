@@ -29,6 +29,7 @@ from .filtering import FilterParams
 from .frame import RenderParams
 from .geometry import extract_frustum
 from .grid import DeviceScene
+from .render import frame_cache
 
 
 def shard_bounds(n_points: int, rank: int, world: int):
@@ -141,12 +142,13 @@ class ShardedRenderer:
         st = _lib.stream_ptr()
         bits = sc.cull_bits(extract_frustum(camera).planes).data_ptr()
         tl, tc = sc.worklist()
+        cache = _lib.ptr(frame_cache(sc, camera))
         _lib.check(lib.ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
-                                      b.minz.data_ptr(), st), "frame_pass1")
+                                      b.minz.data_ptr(), cache, st), "frame_pass1")
         merge_minz(b.minz, self.group)
         _lib.check(lib.ls_frame_pass2(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
                                       float(self.rp.zbuffer_epsilon_rel), b.minz.data_ptr(),
-                                      b.accum.data_ptr(), st), "frame_pass2")
+                                      cache, b.accum.data_ptr(), st), "frame_pass2")
         merge_accum(b.accum, root, self.group)
         if self.rank != root:
             b.minz.fill_(_lib.INF_BITS)

@@ -111,7 +111,7 @@ int main(void) {
     for (int i = 0; i < W * H; ++i) h_inf[i] = 0x7FF0000000000000ull;
     cudaMemcpy(d_minz, h_inf, 8 * W * H, cudaMemcpyHostToDevice);
     cudaMemset(d_acc, 0, 16 * W * H);
-    CK(ls_frame_project(&sc, NULL, NULL, NULL, &cam, 0.01, d_minz, d_acc, st));
+    CK(ls_frame_project(&sc, NULL, NULL, NULL, &cam, 0.01, d_minz, NULL, d_acc, st));
     float *d_rgb = dalloc(12 * W * H), *d_depth = dalloc(4 * W * H);
     unsigned char *d_alpha = dalloc(W * H);
     int32_t *d_flags = dalloc(4);

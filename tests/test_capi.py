@@ -52,7 +52,7 @@ def test_workspace_queries_need_no_gpu():
 def test_invalid_arguments_rejected_before_launch():
     lib = _lib.load()
     assert lib.ls_min_pool_2x2(None, 0, 5, None, None) == _lib.LS_EINVAL
-    assert lib.ls_frame_pass1(None, None, None, None, None, None, None) == _lib.LS_EINVAL
+    assert lib.ls_frame_pass1(None, None, None, None, None, None, None, None) == _lib.LS_EINVAL
     f = _lib.LsFilterParams()
     f.levels_n, f.filter_strength, f.edge_threshold = 5, 0.1, 0.25
     # 16x16 is too small for 5 levels (filtering.py:75-78)

@@ -237,13 +237,18 @@ def test_f32_accumulator_bound(n):
     assert np.array_equal(fr.alpha, ref[2])
 
 
+@pytest.mark.parametrize("cache", [False, True])
 @pytest.mark.parametrize("eps", [0.0, 1e-9, 0.01, 0.5])
-def test_soft_zbuffer_threshold_edges_match_oracle(rng, port, eps):
+def test_soft_zbuffer_threshold_edges_match_oracle(rng, port, monkeypatch, eps, cache):
     """Points sharing a line of sight at depths one f64 ulp apart, and eps = 0
     (every winner exactly on the threshold): the keep test zc <= minz*(1+eps)
     must agree with the oracle bit for bit, culled and brute force."""
     from lidarsplat import PointCloud, RenderParams, build_grid, project_points
+    from paper_2502_11618_b200 import render
 
+    # cached pass 2 decides from f32 depths; eps = 0 puts every winner exactly
+    # on the threshold, forcing its exact re-derivation path
+    monkeypatch.setattr(render, "USE_FRAME_CACHE", cache)
     cloud = random_cloud(rng, 40_000, extent=6.0, offset=-3.0)
     base = cloud.positions[:2000].astype(np.float64)
     dup = np.concatenate([base, np.nextafter(base, np.inf)]).astype(np.float32)

@@ -28,14 +28,19 @@ def _frame_setup(n=400_000, seed=3):
     return cloud, cam, build_grid(cloud, 1.0)
 
 
+@pytest.mark.parametrize("cached", [False, True])
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_virtual_shards_bit_identical(world):
+def test_virtual_shards_bit_identical(world, cached):
+    """Shards projected separately, minz merged by MIN and accumulators by SUM,
+    equal the single-scene frame.  Recompute mode rebuilds each shard's work
+    list for pass 2 (list order is irrelevant); cached mode reuses pass 1's
+    list and cache, as it must."""
     import torch
 
     from lidarsplat import _lib
     from lidarsplat.geometry import extract_frustum
     from lidarsplat.grid import DeviceScene
-    from lidarsplat.render import FrameBuffers, project_scene
+    from lidarsplat.render import FrameBuffers, frame_cache, project_scene
     from lidarsplat.shard import shard_bounds, shard_cell_offsets
 
     cloud, cam, grid = _frame_setup()
@@ -57,15 +62,20 @@ def test_virtual_shards_bit_identical(world):
         bufs.append(b)
         sc.cull_bits(extract_frustum(cam).planes)
         tl, tc = sc.worklist()
+        cache = _lib.ptr(frame_cache(sc, cam)) if cached else None
         _lib.check(lib.ls_frame_pass1(sc.struct, sc.keep_bits.data_ptr(), tl.data_ptr(),
-                                      tc.data_ptr(), c, b.minz.data_ptr(), st), "pass1")
+                                      tc.data_ptr(), c, b.minz.data_ptr(), cache, st), "pass1")
     gmin = torch.stack([b.minz for b in bufs]).min(0).values
     for sc, b in zip(scenes, bufs):
         b.minz.copy_(gmin)
-        sc.cull_bits(extract_frustum(cam).planes)
-        tl, tc = sc.worklist()
+        cache = None
+        if cached:
+            tl, tc, cache = sc.tile_list, sc.tile_count, _lib.ptr(frame_cache(sc, cam))
+        else:
+            sc.cull_bits(extract_frustum(cam).planes)
+            tl, tc = sc.worklist()
         _lib.check(lib.ls_frame_pass2(sc.struct, sc.keep_bits.data_ptr(), tl.data_ptr(),
-                                      tc.data_ptr(), c, 0.01, b.minz.data_ptr(),
+                                      tc.data_ptr(), c, 0.01, b.minz.data_ptr(), cache,
                                       b.accum.data_ptr(), st), "pass2")
     root = bufs[world - 1]
     root.accum.copy_(torch.stack([b.accum for b in bufs]).sum(0))
