@@ -611,7 +611,10 @@ inline SceneArgs scene_args(const ls_scene &s) {
 }
 
 inline bool camera_ok(const ls_camera *cam) {
-    return cam && cam->width > 0 && cam->height > 0 && cam->z_near > 0.0 &&
+    // width/height < 2^31: the frame passes test 0 <= u < W on the low word
+    // of u + 2^52 (ls_common.cuh project4)
+    return cam && cam->width > 0 && cam->height > 0 && cam->width < (int64_t(1) << 31) &&
+           cam->height < (int64_t(1) << 31) && cam->z_near > 0.0 &&
            cam->width * cam->height < (int64_t(1) << 40);
 }
 

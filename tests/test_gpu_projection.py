@@ -263,3 +263,27 @@ def test_soft_zbuffer_threshold_edges_match_oracle(rng, port, monkeypatch, eps, 
                                             np.array([cloud.count], np.int64), cam, eps, port)
         assert np.array_equal(a.rgb, rgb) and np.array_equal(a.depth, depth)
         assert np.array_equal(a.alpha, alpha)
+
+
+def test_frame_edges_match_oracle(port):
+    """Points landing exactly on u = 0 / v = 0 (kept), u = W / v = H (dropped),
+    just inside / outside either edge, and on -0.0: the frame passes' integer
+    range test (low word of u + 2^52) must agree with the reference's f64
+    comparisons (render.py / _native.pyx:98-117) bit for bit."""
+    from lidarsplat import CameraModel, PointCloud, RenderParams, RigidTransform, project_points
+
+    cam = CameraModel(fx=64.0, fy=64.0, cx=0.0, cy=0.0, width=64, height=48,
+                      world_to_camera=RigidTransform.identity())
+    z = 2.0
+    xs = [0.0, -0.0, 1e-30, -1e-30, 2.0, 2.0 - 2 ** -20, 2.0 + 2 ** -20, 1.0, 63 / 32, 65 / 32]
+    ys = [0.0, -0.0, 1e-30, -1e-30, 1.5, 1.5 - 2 ** -20, 1.5 + 2 ** -20, 0.75, 47 / 32, 49 / 32]
+    pts = np.array([[x, y, z] for x in xs for y in ys], np.float32)
+    rng = np.random.default_rng(0)
+    cols = rng.integers(0, 256, (len(pts), 3), dtype=np.uint8)
+    cloud = PointCloud(pts, cols)
+    fr = project_points(cloud, None, cam, RenderParams())
+    ref = O.project(pts, cols, np.zeros(1, np.int64), np.array([len(pts)], np.int64), cam, 0.01,
+                    port)
+    assert np.array_equal(fr.rgb, ref[0]) and np.array_equal(fr.depth, ref[1])
+    assert np.array_equal(fr.alpha, ref[2])
+    assert 0 < int(fr.alpha.sum()) < len(pts)
