@@ -259,11 +259,12 @@ def run_b200(args):
         renderer.enqueue(cams[(view0 + i) % len(cams)])
     torch.cuda.synchronize()
     # ---- device-timed region (inputs resident in HBM) ----
+    # The K timed frames run uninstrumented: an event recorded between two
+    # kernels ends the programmatic-dependent-launch overlap at that boundary
+    # (~3% of a frame).  The per-stage breakdown used for the rooflines comes
+    # from a second, instrumented pass over the same frames afterwards.
     clocks = ClockSampler(local)
     clocks.start()
-    nst = 5
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)]
-           for _ in range(args.steps)]
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -271,12 +272,7 @@ def run_b200(args):
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record()
     for i in range(args.steps):
-        cam = cams[(view0 + args.warmup + i) % len(cams)]
-        if sharded:  # root-side work is on a side stream: no per-stage events
-            renderer.enqueue(cam)
-        else:
-            evs[i][0].record()
-            renderer.enqueue(cam, events=evs[i][1:])
+        renderer.enqueue(cams[(view0 + args.warmup + i) % len(cams)])
     if sharded:
         torch.cuda.current_stream().wait_stream(renderer.side)
     t_end.record()
@@ -289,6 +285,15 @@ def run_b200(args):
         t = torch.tensor([total_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
+    # instrumented pass (stage events), not part of the timed value
+    nst = 5
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)]
+           for _ in range(args.steps)]
+    if not sharded:  # root-side work is on a side stream: no per-stage events
+        for i in range(args.steps):
+            evs[i][0].record()
+            renderer.enqueue(cams[(view0 + args.warmup + i) % len(cams)], events=evs[i][1:])
+        torch.cuda.synchronize()
     renderer.check_flags()
     stage = {k: [] for k in ("cull", "pass1", "pass2", "filter", "unet")}
     for e in ([] if sharded else evs):
@@ -378,6 +383,8 @@ def run_b200(args):
         "gpoints_per_s": mean_cand * fps / 1e9,
         "candidates_mean": mean_cand,
         "stages_ms": stages_ms,
+        "stages_note": "per-stage CUDA events from a second, instrumented pass over the same "
+                       "frames; value / ms_per_step come from the uninstrumented timed pass",
         "roofline": roofline,
         "clocks": clk,
         "e2e": e2e,
