@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(256) k_cull(const int64_t *__restrict__ cells,
                                               double ox, double oy, double oz, double cell,
                                               int64_t dy, int64_t dz, Planes pl, double slack,
                                               uint32_t *__restrict__ bits) {
+    pdl_wait();  // the previous frame's kernels may still be draining
     const int lane = threadIdx.x & 31;
     const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(256) k_cull(const int64_t *__restrict__ cells,
         const uint32_t word = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) bits[base >> 5] = word;
     }
+    pdl_trigger();
 }
 
 // predicate bits for occupied cells: offsets[c+1] > offsets[c]
@@ -177,11 +179,12 @@ int ls_cull(const ls_scene *scene, const double h_planes[24], double slack,
     Planes pl;
     for (int i = 0; i < 24; ++i) pl.p[i] = h_planes[i];
     const int64_t n_words = (scene->n_occ + 31) / 32;
-    k_cull<<<grid_for(n_words * 32, 256), 256, 0, (cudaStream_t)stream>>>(
-        scene->d_occ_cells, scene->n_occ, scene->origin[0], scene->origin[1], scene->origin[2],
-        scene->cell_size, scene->dims[1], scene->dims[2], pl, slack, d_keep_bits);
-    LS_LAUNCH_CHECK();
-    return 0;
+    cudaError_t e = launch_pdl(k_cull, dim3(grid_for(n_words * 32, 256)), dim3(256), 0,
+                               (cudaStream_t)stream, scene->d_occ_cells, scene->n_occ,
+                               scene->origin[0], scene->origin[1], scene->origin[2],
+                               scene->cell_size, scene->dims[1], scene->dims[2], pl, slack,
+                               d_keep_bits);
+    return (int)e;
 }
 
 size_t ls_compact_workspace(int64_t n_items) {

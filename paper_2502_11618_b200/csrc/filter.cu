@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     unsigned long long *__restrict__ minz, float4 *__restrict__ acc, int64_t H,
     int64_t W, Levels lv, int pool_levels, float *__restrict__ rgb, float *__restrict__ depth,
     uint8_t *__restrict__ alpha, int *__restrict__ flags) {
+    pdl_wait();  // launched with PDL after pass 2; its trigger is completion
     __shared__ float s1[16][17];
     __shared__ float s2[8][9];
     __shared__ float s3[4][5];
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(256) k_filter_step(
     const float *__restrict__ rgb, const uint8_t *__restrict__ alpha, float *__restrict__ frgb,
     float *__restrict__ fdepth, uint8_t *__restrict__ falpha, uint8_t *__restrict__ keep_out,
     __nv_bfloat16 *__restrict__ unet_in, int unet_c, double znear) {
+    pdl_wait();
     const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
     if (cx >= cw || cy >= ch) return;
@@ -420,6 +422,7 @@ __global__ void __launch_bounds__(256) k_filter_step(
                               o[dx][3], oa[dx], znear);
         }
     }
+    pdl_trigger();
 }
 
 // Bridge input (FE:bridge.ts:31-53): an RGDA tensor's five f32 planes ->
@@ -461,17 +464,17 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
         const int64_t fh = lv.h[L - i], fw = lv.w[L - i];
         if (i < L) {
             const float *fine = lv.img[L - i - 1];
-            k_filter_step<false><<<step_grid2(ch, cw), dim3(32, 8), 0, st>>>(
-                coarse, ch, cw, fine, fh, fw, fs, et, up, nullptr, nullptr, nullptr, nullptr,
-                nullptr, nullptr, nullptr, 0, 0.0);
-            LS_LAUNCH_CHECK();
+            cudaError_t e = launch_pdl(k_filter_step<false>, step_grid2(ch, cw), dim3(32, 8), 0, st,
+                                       coarse, ch, cw, fine, fh, fw, fs, et, up, nullptr, nullptr,
+                                       nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0);
+            if (e != cudaSuccess) return (int)e;
             coarse = up;
             up += fh * fw;
         } else {
-            k_filter_step<true><<<step_grid2(ch, cw), dim3(32, 8), 0, st>>>(
-                coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, rgb, alpha, frgb, fdepth,
-                falpha, keep, unet_in, unet_c, znear);
-            LS_LAUNCH_CHECK();
+            cudaError_t e = launch_pdl(k_filter_step<true>, step_grid2(ch, cw), dim3(32, 8), 0, st,
+                                       coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, rgb,
+                                       alpha, frgb, fdepth, falpha, keep, unet_in, unet_c, znear);
+            if (e != cudaSuccess) return (int)e;
         }
     }
     return 0;
@@ -581,10 +584,11 @@ int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64
     }
     dim3 grid((unsigned)((width + 31) / 32), (unsigned)((height + 31) / 32));
     const int in_block = L < 5 ? L : 5;
-    k_assemble_pyramid<<<grid, 256, 0, st>>>((unsigned long long *)d_minz_bits,
-                                             reinterpret_cast<float4 *>(d_accum4), height, width, lv,
-                                             in_block, d_rgb, d_depth, d_alpha, d_flags);
-    LS_LAUNCH_CHECK();
+    cudaError_t e = launch_pdl(k_assemble_pyramid, grid, dim3(256), 0, st,
+                               (unsigned long long *)d_minz_bits,
+                               reinterpret_cast<float4 *>(d_accum4), height, width, lv, in_block,
+                               d_rgb, d_depth, d_alpha, d_flags);
+    if (e != cudaSuccess) return (int)e;
     if (!filter) return 0;
     for (int k = 6; k <= L; ++k) {  // levels beyond the in-block five
         k_min_pool<<<grid_for(lv.h[k] * lv.w[k], 256), 256, 0, st>>>(lv.img[k - 2], lv.h[k - 1],

@@ -169,6 +169,7 @@ constexpr uint32_t kMixed = 0x80000000u;
 __global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *__restrict__ bits,
                                                    uint32_t *__restrict__ list,
                                                    uint32_t *__restrict__ count) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31);
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *
         if (keep_any)
             list[off + __popc(vote & ((1u << lane) - 1u))] = (uint32_t)t | (cull_any ? kMixed : 0u);
     }
+    pdl_trigger();
 }
 
 // Loads the lane's 4 points (xyz) -- vectorised when the group is complete.
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ count,
                                                      unsigned long long *__restrict__ minz,
                                                      uint32_t *__restrict__ cache) {
+    pdl_wait();
     for_each_item<kPass1Stages, kXyz>(s, list, count, nullptr, [&](const Item &it, uint3) {
         float P[12];
         const int cnt = item_points(s, it, P);
@@ -485,6 +488,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
         for (int k = 0; k < 4; ++k)
             if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
     });
+    pdl_trigger();
 }
 
 // Pass 2, recompute mode: pixel and depth again from the points.
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                                                      const uint32_t *__restrict__ count, double ope,
                                                      const unsigned long long *__restrict__ minz,
                                                      float *__restrict__ acc) {
+    pdl_wait();
     for_each_item<kPass2Stages, kXyzRgb>(s, list, count, nullptr, [&](const Item &it, uint3 W) {
         float P[12];
         const int cnt = item_points(s, it, P);
@@ -522,6 +527,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
                 red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
                             (float)sum[k][3]);
     });
+    pdl_trigger();
 }
 
 // Pass 2, cached mode: no projection (pass 2 is instruction-issue bound once
@@ -537,6 +543,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
                                                             const unsigned long long *__restrict__ minz,
                                                             float *__restrict__ acc) {
     const int lane = threadIdx.x & 31;
+    pdl_wait();
     for_each_item<kPass2Stages, kCacheRgb>(s, list, count, cache, [&](const Item &it, uint3 W) {
         const uint4 pw = reinterpret_cast<const uint4 *>(it.st)[lane];
         const float4 zw = reinterpret_cast<const float4 *>(it.st + 4 * LS_TILE_POINTS)[lane];
@@ -574,6 +581,7 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
                 red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
                             (float)sum[k][3]);
     });
+    pdl_trigger();
 }
 
 // Per-scan: occupied-cell span of every warp tile.
@@ -730,9 +738,8 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    k_tile_list<<<grid_for(a.n_tiles, 256, 8), 256, 0, st>>>(a, d_keep_bits, d_list, d_count);
-    LS_LAUNCH_CHECK();
-    return 0;
+    return (int)launch_pdl(k_tile_list, dim3(grid_for(a.n_tiles, 256, 8)), dim3(256), 0, st, a,
+                           d_keep_bits, d_list, d_count);
 }
 
 size_t ls_frame_cache_bytes(const ls_scene *scene) {
@@ -755,11 +762,9 @@ int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
-    k_frame_pass1<<<frame_grid(k_frame_pass1, kSmem1, a.n_tiles), 256, kSmem1,
-                    (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
-                                            (unsigned long long *)d_minz_bits, d_cache);
-    LS_LAUNCH_CHECK();
-    return 0;
+    return (int)launch_pdl(k_frame_pass1, dim3(frame_grid(k_frame_pass1, kSmem1, a.n_tiles)),
+                           dim3(256), kSmem1, (cudaStream_t)stream, a, make_cam(*cam), d_keep_bits,
+                           d_list, d_count, (unsigned long long *)d_minz_bits, d_cache);
 }
 
 int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
@@ -774,17 +779,14 @@ int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
     const double ope = 1.0 + eps_rel;
     if (d_cache)
-        k_frame_pass2_cached<<<frame_grid(k_frame_pass2_cached, kSmem2c, a.n_tiles), 256, kSmem2c,
-                               (cudaStream_t)stream>>>(a, make_cam(*cam), d_list, d_count, d_cache,
-                                                       ope, (const unsigned long long *)d_minz_bits,
-                                                       d_accum4);
-    else
-        k_frame_pass2<<<frame_grid(k_frame_pass2, kSmem2, a.n_tiles), 256, kSmem2,
-                        (cudaStream_t)stream>>>(a, make_cam(*cam), d_keep_bits, d_list, d_count,
-                                                ope, (const unsigned long long *)d_minz_bits,
-                                                d_accum4);
-    LS_LAUNCH_CHECK();
-    return 0;
+        return (int)launch_pdl(k_frame_pass2_cached,
+                               dim3(frame_grid(k_frame_pass2_cached, kSmem2c, a.n_tiles)),
+                               dim3(256), kSmem2c, (cudaStream_t)stream, a, make_cam(*cam), d_list,
+                               d_count, d_cache, ope, (const unsigned long long *)d_minz_bits,
+                               d_accum4);
+    return (int)launch_pdl(k_frame_pass2, dim3(frame_grid(k_frame_pass2, kSmem2, a.n_tiles)),
+                           dim3(256), kSmem2, (cudaStream_t)stream, a, make_cam(*cam), d_keep_bits,
+                           d_list, d_count, ope, (const unsigned long long *)d_minz_bits, d_accum4);
 }
 
 int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_t *d_list,
