@@ -161,6 +161,12 @@ __device__ __forceinline__ bool point_kept(const SceneArgs &s, const uint32_t *_
     return (__ldg(bits + (lo >> 5)) >> (lo & 31)) & 1u;
 }
 
+__global__ void k_zero_count(uint32_t *__restrict__ count) {
+    pdl_wait();
+    if (threadIdx.x == 0) *count = 0u;
+    pdl_trigger();
+}
+
 // Work list of the frame: one u32 per non-culled warp tile, bit 31 = mixed
 // (some of its cells culled).  One thread per tile, warp-aggregated append;
 // list order is irrelevant (both passes are order-free reductions).
@@ -733,7 +739,8 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
                      uint32_t *d_count, void *stream) {
     if (!scene_ok(scene, d_list) || !d_keep_bits || !d_list || !d_count) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(uint32_t), st);
+    // a one-thread kernel instead of a memset node keeps the PDL chain unbroken
+    cudaError_t e = launch_pdl(k_zero_count, dim3(1), dim3(32), 0, st, d_count);
     if (e != cudaSuccess) return (int)e;
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);

@@ -18,9 +18,10 @@ from .filtering import FilterParams
 from .frame import FrameRGBDA, RenderParams
 from .render import FrameBuffers, project_scene
 
-# kernel launches per frame of the fused path: cull, tile work list, pass 1,
-# pass 2, assemble+pyramid, L filter steps (+ U-Net layers when attached)
-BASE_LAUNCHES = 5
+# kernel launches per frame of the fused path: cull, work-list counter reset,
+# tile work list, pass 1, pass 2, assemble+pyramid, L filter steps (+ U-Net
+# layers when attached)
+BASE_LAUNCHES = 6
 
 
 class FrameRenderer:

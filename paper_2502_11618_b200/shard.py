@@ -120,9 +120,9 @@ class ShardedRenderer:
 
     @property
     def launches_per_frame(self) -> int:
-        # cull, work list, pass 1, pass 2 on every rank; finish + filter + U-Net
-        # on the root (1/world of the frames)
-        n = 4 + (1 + self.fp.levels_n + (self.unet.launches if self.unet else 0)) / self.world
+        # cull, counter reset, work list, pass 1, pass 2 on every rank; finish +
+        # filter + U-Net on the root (1/world of the frames)
+        n = 5 + (1 + self.fp.levels_n + (self.unet.launches if self.unet else 0)) / self.world
         return int(round(n))
 
     def enqueue(self, camera) -> None:
