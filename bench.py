@@ -245,7 +245,10 @@ def run_b200(args):
 
         renderer = ShardedRenderer(grid, args.width, args.height, rank, world, unet=unet)
     else:
-        renderer = FrameRenderer(grid, args.width, args.height, unet=unet)
+        # with a U-Net the f32 filtered frame is an intermediate the U-Net does
+        # not read (it reads the packed bf16 input of the same filter kernel)
+        renderer = FrameRenderer(grid, args.width, args.height, unet=unet,
+                                 filtered_outputs=unet is None)
     # replicas: rank r renders its own frames (views offset by rank)
     view0 = 0 if sharded else rank * args.steps
     # candidate counts per view (algorithmic bytes of the projection passes)

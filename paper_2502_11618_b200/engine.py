@@ -26,7 +26,11 @@ BASE_LAUNCHES = 6
 
 class FrameRenderer:
     def __init__(self, grid, width: int, height: int, render_params: RenderParams | None = None,
-                 filter_params: FilterParams | None = None, unet=None):
+                 filter_params: FilterParams | None = None, unet=None,
+                 filtered_outputs: bool = True):
+        """``filtered_outputs=False`` (only with a U-Net): the f32 filtered frame
+        (frgb/fdepth/falpha, 17 B/px) is not materialised -- the U-Net reads
+        the packed bf16 input the same filter kernel writes."""
         import torch
 
         self.device = _lib.device()
@@ -44,6 +48,7 @@ class FrameRenderer:
             raise ValueError(f"image {w}x{h} too small for {self.fp.levels_n} pyramid levels")
         self.pyramid = torch.empty(int(n), dtype=torch.float32, device=dev)
         self.unet = unet
+        self.filtered_outputs = bool(filtered_outputs) or unet is None
         self.unet_in = None
         self.rgb_out = None
         if unet is not None:
@@ -87,7 +92,12 @@ class FrameRenderer:
         U-Net boundaries for per-stage timing.  ``slot`` selects the output
         buffer set (render_stream alternates two)."""
         outs = self._outputs(slot)
-        filtered = (self.frgb, self.fdepth, self.falpha) if self.unet is not None else outs
+        if self.unet is None:
+            filtered = outs
+        elif self.filtered_outputs:
+            filtered = (self.frgb, self.fdepth, self.falpha)
+        else:
+            filtered = (None, None, None)
         project_scene(self.scene, camera, self.rp.zbuffer_epsilon_rel, self.bufs, cull=True,
                       filter_params=self.fp, filtered=filtered,
                       unet_in=None if self.unet is None else self.unet_in[0],

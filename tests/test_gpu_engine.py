@@ -64,3 +64,21 @@ def test_ply_load_stages_device_copy(tmp_path):
     a = project_points(staged, build_grid(staged, 1.0), cam)
     b = project_points(cloud, build_grid(cloud, 1.0), cam)
     assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.depth, b.depth)
+
+
+def test_unfiltered_outputs_same_reconstruction():
+    """filtered_outputs=False (the f32 filtered frame is not written) gives a
+    bit-identical U-Net reconstruction."""
+    from paper_2502_11618_b200 import build_grid
+    from paper_2502_11618_b200.engine import FrameRenderer
+    from paper_2502_11618_b200.unet import UNet
+
+    rng = np.random.default_rng(12)
+    cloud = random_cloud(rng, 150_000, extent=10.0, offset=-5.0)
+    views = [random_view(rng, cloud, width=256, height=192) for _ in range(3)]
+    grid = build_grid(cloud, 1.0)
+    unet = UNet.from_config("reduced", seed=2)
+    a = FrameRenderer(grid, 256, 192, unet=unet)
+    b = FrameRenderer(grid, 256, 192, unet=unet, filtered_outputs=False)
+    for v in views:
+        assert np.array_equal(a.render(v), b.render(v))
