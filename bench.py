@@ -42,7 +42,7 @@ METRIC = "frames/sec at 1920x1080 for N-M-point scan (1/2/4/8 B200); Gpoints/s p
 def parse():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--points", type=int, default=20_000_000)
