@@ -553,19 +553,22 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
     for_each_item<kPass2Stages, kCacheRgb>(s, list, count, cache, [&](const Item &it, uint3 W) {
         const uint4 pw = reinterpret_cast<const uint4 *>(it.st)[lane];
         const float4 zw = reinterpret_cast<const float4 *>(it.st + 4 * LS_TILE_POINTS)[lane];
-        int64_t pix[4] = {pw.x == kNoPixel ? -1 : (int64_t)pw.x, pw.y == kNoPixel ? -1 : (int64_t)pw.y,
-                          pw.z == kNoPixel ? -1 : (int64_t)pw.z, pw.w == kNoPixel ? -1 : (int64_t)pw.w};
+        uint32_t pix[4] = {pw.x, pw.y, pw.z, pw.w};
         const float zlo[4] = {zw.x, zw.y, zw.z, zw.w};
         unsigned long long m[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldg(minz + pix[k]) : 0ull;
+        for (int k = 0; k < 4; ++k) m[k] = pix[k] != kNoPixel ? __ldg(minz + pix[k]) : 0ull;
         uint32_t sum[4][4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (pix[k] >= 0) {
+            if (pix[k] != kNoPixel) {
                 const double t = dmul(__longlong_as_double((long long)m[k]), ope);
-                bool keep = (double)__int_as_float(__float_as_int(zlo[k]) + 1) <= t;
-                if (!keep && !((double)zlo[k] > t)) {  // within one f32 ulp: exact depth
+                // for a float z: (double)z <= T  <=>  z <= RD_f32(T), and
+                // z > T  <=>  z > RD_f32(T) (no float lies strictly between
+                // RD(T) and RU(T)), so both tests run in f32 against one rounding
+                const float trd = __double2float_rd(t);
+                bool keep = __int_as_float(__float_as_int(zlo[k]) + 1) <= trd;
+                if (!keep && !(zlo[k] > trd)) {  // within one f32 ulp: exact depth
                     const float *p = s.pos + 3 * (it.base + k);
                     const double x = (double)__ldg(p), y = (double)__ldg(p + 1),
                                  z = (double)__ldg(p + 2);
@@ -573,19 +576,28 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
                         dadd(dadd(dadd(dmul(c.r[6], x), dmul(c.r[7], y)), dmul(c.r[8], z)), c.t[2]);
                     keep = zc <= t;
                 }
-                if (!keep) pix[k] = -1;
+                if (!keep) pix[k] = kNoPixel;
             }
             sum[k][0] = color_byte3(W, 3 * k);
             sum[k][1] = color_byte3(W, 3 * k + 1);
             sum[k][2] = color_byte3(W, 3 * k + 2);
             sum[k][3] = 1u;
         }
-        merge_lane_sum(pix, sum);
+        // fold the lane's same-pixel points (integer sums: exact)
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+#pragma unroll
+            for (int j = 0; j < k; ++j)
+                if (pix[k] != kNoPixel && pix[k] == pix[j]) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) sum[j][q] += sum[k][q];
+                    pix[k] = kNoPixel;
+                }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (pix[k] >= 0)
-                red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
-                            (float)sum[k][3]);
+            if (pix[k] != kNoPixel)
+                red_add_v4c(acc + 4 * (size_t)pix[k], (float)sum[k][0], (float)sum[k][1],
+                            (float)sum[k][2], (float)sum[k][3]);
     });
     pdl_trigger();
 }
