@@ -208,6 +208,34 @@ int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
                    const uint64_t *d_minz_bits, const uint32_t *d_cache, float *d_accum4,
                    void *stream);
 
+/* Multi-view batched projection (render.py:84-143 project_candidates, run
+ * once per view): ONE read of the culled scan's tiles feeds
+ * n_views <= LS_MAX_VIEWS cameras of the same width/height.  Every view's
+ * frame is bit-identical to ls_frame_project of that view alone (same f64
+ * arithmetic, same per-view culling, order-free reductions).
+ * d_keep_bits: NULL = no cull, else n_views blocks of bits_stride u32 words,
+ *   block v = ls_cull of view v (bits_stride >= ceil(n_occ/32)); the work
+ *   list is built over their union: d_list n_tiles entries, d_status n_tiles
+ *   u32 (per entry: bit 2v = view v keeps a cell of the tile, bit 2v+1 = view
+ *   v also culls one), d_count 1 u32 (reset by the call).
+ * d_minz_bits: n_views x (W*H) u64, +inf on entry (view v at v*W*H).
+ * d_cache: NULL (pass 2 re-projects), or ls_frame_views_cache_bytes(scene,
+ *   n_views) bytes, 16 B aligned: pass 1 records each (candidate, view)'s
+ *   pixel and f32-rounded-down depth, pass 2 decides from them (the
+ *   ls_frame_project cache rule, per view).  Same frames either way.
+ * d_accum4: n_views x (W*H*4) f32, zero on entry; one ls_frame_finish per view
+ *   (at the view's offsets) folds them into frames. */
+#define LS_MAX_VIEWS 8
+int ls_tile_worklist_views(const ls_scene *scene, const uint32_t *d_keep_bits,
+                           int64_t bits_stride, int32_t n_views, uint32_t *d_list,
+                           uint32_t *d_status, uint32_t *d_count, void *stream);
+int ls_frame_project_views(const ls_scene *scene, const uint32_t *d_keep_bits,
+                           int64_t bits_stride, uint32_t *d_list, uint32_t *d_status,
+                           uint32_t *d_count, const ls_camera *cams, int32_t n_views,
+                           double eps_rel, uint64_t *d_minz_bits, uint32_t *d_cache,
+                           float *d_accum4, void *stream);
+size_t ls_frame_views_cache_bytes(const ls_scene *scene, int32_t n_views);
+
 /* Level sizes of the min pyramid (filtering.py:67-83); returns the float
  * count of the workspace ls_frame_finish needs for levels 0..L-1. */
 int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n);

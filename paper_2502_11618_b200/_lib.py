@@ -21,6 +21,7 @@ LIB_PATH = os.path.join(_HERE, "liblidarsplat_cuda.so")
 LS_EINVAL = -22
 LS_TILE_POINTS = 128
 LS_PACKED_COUNT_LIMIT = 65793
+LS_MAX_VIEWS = 8
 INF_BITS = 0x7FF0000000000000
 
 
@@ -93,6 +94,11 @@ SIGNATURES = {
                                       ctypes.POINTER(LsCamera), _P, _P, _P]),
     "ls_frame_pass2": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _P, _P,
                                       ctypes.POINTER(LsCamera), _D, _P, _P, _P, _P]),
+    "ls_tile_worklist_views": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _I64, _I32, _P, _P,
+                                              _P, _P]),
+    "ls_frame_project_views": (ctypes.c_int, [ctypes.POINTER(LsScene), _P, _I64, _P, _P, _P,
+                                              _P, _I32, _D, _P, _P, _P, _P]),
+    "ls_frame_views_cache_bytes": (_SZ, [ctypes.POINTER(LsScene), _I32]),
     "ls_pyramid_floats": (_I64, [_I64, _I64, _I32]),
     "ls_frame_finish": (ctypes.c_int, [_P, _P, _I64, _I64, ctypes.POINTER(LsFilterParams),
                                        _P, _P, _P, _P, _P, _P, _P, _P, _I64, _I32, _D, _P, _P,

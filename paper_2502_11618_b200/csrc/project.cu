@@ -16,6 +16,8 @@
 #include "ls_common.cuh"
 #include "umma.cuh"
 
+#include <type_traits>
+
 namespace ls {
 
 // ---------------------------------------------------------------------------
@@ -274,11 +276,13 @@ constexpr int kPassWarps = 8;  // 256-thread CTAs
 constexpr int kPosBytes = LS_TILE_POINTS * 12, kColBytes = LS_TILE_POINTS * 3;
 constexpr int kCacheBytes = LS_TILE_POINTS * 8;  // [128 x u32 pixel][128 x f32 depth]
 // kXyz: pass 1 | kXyzRgb: pass 2 recomputing | kCacheRgb: pass 2 from the cache
-enum RingMode { kXyz = 0, kXyzRgb = 1, kCacheRgb = 2 };
+// | kRgb: colours only (multi-view pass 2, whose per-view cache blocks are read
+// straight from global memory)
+enum RingMode { kXyz = 0, kXyzRgb = 1, kCacheRgb = 2, kRgb = 3 };
 
 template <int S, int MODE>
 struct TileRing {
-    static constexpr int kMain = MODE == kCacheRgb ? kCacheBytes : kPosBytes;
+    static constexpr int kMain = MODE == kCacheRgb ? kCacheBytes : (MODE == kRgb ? 0 : kPosBytes);
     static constexpr int kStage = kMain + (MODE == kXyz ? 0 : kColBytes);
     static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8 + 4);
 };
@@ -342,16 +346,16 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         ents[q] = e;
         const bool f = full(tile);
         // the cache block is always complete (pass 1 writes all 128 slots)
-        if (!f && MODE != kCacheRgb) {
+        const bool rgb = MODE != kXyz && f && col_bulk;
+        if ((!f && MODE != kCacheRgb) || (MODE == kRgb && !rgb)) {
             umma::mbar_arrive(&bars[q]);
             return;
         }
-        const bool rgb = MODE != kXyz && f && col_bulk;
         umma::mbar_expect_tx(&bars[q], R::kMain + (rgb ? kColBytes : 0));
         uint8_t *dst = ring + q * R::kStage;
         if (MODE == kCacheRgb)
             bulk_g2s(dst, cache + (w0 + j * nw) * (kCacheBytes / 4), kCacheBytes, &bars[q]);
-        else
+        else if (MODE != kRgb)
             bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q]);
         if (rgb) bulk_g2s(dst + R::kMain, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q]);
     };
@@ -602,6 +606,233 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
     pdl_trigger();
 }
 
+// ---------------------------------------------------------------------------
+// (iii) multi-view batched passes: one read of the culled
+// scan feeds up to LS_MAX_VIEWS views.  Each view's arithmetic, culling and
+// reductions are exactly those of the single-view passes (render.py:84-143
+// run once per view), so every view's frame is bit-identical to rendering it
+// alone; what is shared is the tile stream (xyz, rgb, work list).
+// ---------------------------------------------------------------------------
+
+struct ViewCams {
+    ProjCam c[LS_MAX_VIEWS];
+};
+
+// Work list over the union of the views' keep bits, plus a status word per
+// entry: bit 2v = view v keeps some cell of the tile, bit 2v+1 = view v also
+// culls some cell of it (its points then need the per-point cell test).
+__global__ void __launch_bounds__(256) k_tile_list_views(SceneArgs s,
+                                                         const uint32_t *__restrict__ bits,
+                                                         int64_t words, int nv,
+                                                         uint32_t *__restrict__ list,
+                                                         uint32_t *__restrict__ status,
+                                                         uint32_t *__restrict__ count) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31);
+         base < s.n_tiles; base += stride) {
+        const int64_t t = base + lane;
+        uint32_t st = 0u;
+        if (t < s.n_tiles) {
+            const int c0 = __ldg(s.tile_c0 + t), c1 = __ldg(s.tile_c1 + t);
+            for (int v = 0; v < nv; ++v) {
+                const uint32_t *b = bits + v * words;
+                bool keep_any = false, cull_any = false;
+                for (int j = c0; j <= c1; ++j) {
+                    const bool k = (__ldg(b + (j >> 5)) >> (j & 31)) & 1u;
+                    keep_any |= k;
+                    cull_any |= !k;
+                }
+                if (keep_any) st |= (cull_any ? 3u : 1u) << (2 * v);
+            }
+        }
+        const uint32_t vote = __ballot_sync(0xffffffffu, st != 0u);
+        if (vote == 0u) continue;
+        uint32_t off = 0;
+        if (lane == 0) off = atomicAdd(count, (uint32_t)__popc(vote));
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (st != 0u) {
+            const uint32_t at = off + __popc(vote & ((1u << lane) - 1u));
+            list[at] = (uint32_t)t;
+            status[at] = st;
+        }
+    }
+    pdl_trigger();
+}
+
+// Status word of an item: every view keeps every point when there is no cull.
+__device__ __forceinline__ uint32_t item_status(const uint32_t *__restrict__ status,
+                                                const Item &it) {
+    return status ? __ldg(status + it.index) : 0x5555u;
+}
+
+// drop_culled against one view's keep bits (the tile straddles a culled cell).
+__device__ __forceinline__ void drop_culled_view(const SceneArgs &s,
+                                                 const uint32_t *__restrict__ bits,
+                                                 const Item &it, int64_t (&pix)[4]) {
+    const int64_t tile = it.e & ~kMixed;
+    const int c0 = __ldg(s.tile_c0 + tile), c1 = __ldg(s.tile_c1 + tile);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (pix[k] >= 0 && !point_kept(s, bits, c0, c1, it.base + k)) pix[k] = -1;
+}
+
+// The multi-view passes are instantiated for NV = 1, 2, 4, 8 view slots
+// (slots >= n_views carry status 0); the view loop is unrolled so each view's
+// camera stays constant-bank operands, exactly like the single-view passes.
+// With a cache, view v of work item i owns the 1 KB block i * n_views + v
+// (pass 1 writes it, pass 2 decides from it: the single-view cache rule).
+template <int NV>
+__global__ void __launch_bounds__(256, 3) k_frame_pass1_views(
+    SceneArgs s, const ViewCams vc, int nv, int64_t npix, const uint32_t *__restrict__ bits,
+    int64_t words, const uint32_t *__restrict__ list, const uint32_t *__restrict__ status,
+    const uint32_t *__restrict__ count, unsigned long long *__restrict__ minz,
+    uint32_t *__restrict__ cache) {
+    pdl_wait();
+    const uint32_t live = (1u << (2 * nv)) - 1u;
+    for_each_item<kPass1Stages, kXyz>(s, list, count, nullptr, [&](const Item &it, uint3) {
+        float P[12];
+        const int cnt = item_points(s, it, P);
+        const uint32_t st = item_status(status, it) & live;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t vs = (st >> (2 * v)) & 3u;
+            if (vs == 0u) continue;
+            int64_t pix[4];
+            double zc[4];
+            project4(P, cnt, vc.c[v], pix, zc);
+            if (vs == 3u) drop_culled_view(s, bits + v * words, it, pix);
+            if (cache) {
+                const int lane = threadIdx.x & 31;
+                uint32_t *blk = cache + (it.index * nv + v) * (kCacheBytes / 4);
+                reinterpret_cast<uint4 *>(blk)[lane] =
+                    make_uint4(pix[0] >= 0 ? (uint32_t)pix[0] : kNoPixel,
+                               pix[1] >= 0 ? (uint32_t)pix[1] : kNoPixel,
+                               pix[2] >= 0 ? (uint32_t)pix[2] : kNoPixel,
+                               pix[3] >= 0 ? (uint32_t)pix[3] : kNoPixel);
+                reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
+                    make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
+                                __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+            }
+            unsigned long long *mz = minz + v * npix;
+            unsigned long long key[4], cur[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) key[k] = (unsigned long long)__double_as_longlong(zc[k]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldca(mz + pix[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(mz + pix[k], key[k]);
+        }
+    });
+    pdl_trigger();
+}
+
+// Keep decision + lane fold + vector atomics of one view's 4 points (shared
+// by both multi-view pass-2 forms).
+__device__ __forceinline__ void accumulate4(int64_t (&pix)[4], const uint3 &W, float *a) {
+    uint32_t sum[4][4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        sum[k][0] = color_byte3(W, 3 * k);
+        sum[k][1] = color_byte3(W, 3 * k + 1);
+        sum[k][2] = color_byte3(W, 3 * k + 2);
+        sum[k][3] = 1u;
+    }
+    merge_lane_sum(pix, sum);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (pix[k] >= 0)
+            red_add_v4c(a + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
+                        (float)sum[k][3]);
+}
+
+template <int NV>
+__global__ void __launch_bounds__(256, 3) k_frame_pass2_views(
+    SceneArgs s, const ViewCams vc, int nv, int64_t npix, const uint32_t *__restrict__ bits,
+    int64_t words, const uint32_t *__restrict__ list, const uint32_t *__restrict__ status,
+    const uint32_t *__restrict__ count, double ope, const unsigned long long *__restrict__ minz,
+    float *__restrict__ acc) {
+    pdl_wait();
+    const uint32_t live = (1u << (2 * nv)) - 1u;
+    for_each_item<kPass2Stages, kXyzRgb>(s, list, count, nullptr, [&](const Item &it, uint3 W) {
+        float P[12];
+        const int cnt = item_points(s, it, P);
+        const uint32_t st = item_status(status, it) & live;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const uint32_t vs = (st >> (2 * v)) & 3u;
+            if (vs == 0u) continue;
+            int64_t pix[4];
+            double zc[4];
+            project4(P, cnt, vc.c[v], pix, zc);
+            if (vs == 3u) drop_culled_view(s, bits + v * words, it, pix);
+            const unsigned long long *mz = minz + v * npix;
+            unsigned long long m[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) m[k] = pix[k] >= 0 ? __ldg(mz + pix[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (pix[k] >= 0 && !(zc[k] <= dmul(__longlong_as_double((long long)m[k]), ope)))
+                    pix[k] = -1;
+            accumulate4(pix, W, acc + 4 * v * npix);
+        }
+    });
+    pdl_trigger();
+}
+
+// Pass 2 from the per-view cache (k_frame_pass2_cached's rule per view): the
+// ring carries only colours; a view's 1 KB block is one coalesced 16 B load
+// per lane for pixels and one for depths.
+template <int NV>
+__global__ void __launch_bounds__(256) k_frame_pass2_views_cached(
+    SceneArgs s, const ViewCams vc, int nv, int64_t npix, const uint32_t *__restrict__ list,
+    const uint32_t *__restrict__ status, const uint32_t *__restrict__ count,
+    const uint32_t *__restrict__ cache, double ope, const unsigned long long *__restrict__ minz,
+    float *__restrict__ acc) {
+    const int lane = threadIdx.x & 31;
+    pdl_wait();
+    const uint32_t live = (1u << (2 * nv)) - 1u;
+    for_each_item<kPass2Stages, kRgb>(s, list, count, nullptr, [&](const Item &it, uint3 W) {
+        const uint32_t st = item_status(status, it) & live;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            if (((st >> (2 * v)) & 3u) == 0u) continue;
+            const uint32_t *blk = cache + (it.index * nv + v) * (kCacheBytes / 4);
+            const uint4 pw = __ldcs(reinterpret_cast<const uint4 *>(blk) + lane);
+            const float4 zw = __ldcs(reinterpret_cast<const float4 *>(blk + LS_TILE_POINTS) + lane);
+            const uint32_t pc[4] = {pw.x, pw.y, pw.z, pw.w};
+            const float zlo[4] = {zw.x, zw.y, zw.z, zw.w};
+            const unsigned long long *mz = minz + v * npix;
+            unsigned long long m[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) m[k] = pc[k] != kNoPixel ? __ldg(mz + pc[k]) : 0ull;
+            int64_t pix[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                pix[k] = -1;
+                if (pc[k] == kNoPixel) continue;
+                const double t = dmul(__longlong_as_double((long long)m[k]), ope);
+                const float trd = __double2float_rd(t);
+                bool keep = __int_as_float(__float_as_int(zlo[k]) + 1) <= trd;
+                if (!keep && !(zlo[k] > trd)) {  // within one f32 ulp: exact depth
+                    const float *p = s.pos + 3 * (it.base + k);
+                    const double x = (double)__ldg(p), y = (double)__ldg(p + 1),
+                                 z = (double)__ldg(p + 2);
+                    const ProjCam &c = vc.c[v];
+                    const double zc =
+                        dadd(dadd(dadd(dmul(c.r[6], x), dmul(c.r[7], y)), dmul(c.r[8], z)), c.t[2]);
+                    keep = zc <= t;
+                }
+                if (keep) pix[k] = (int64_t)pc[k];
+            }
+            accumulate4(pix, W, acc + 4 * v * npix);
+        }
+    });
+    pdl_trigger();
+}
+
 // Per-scan: occupied-cell span of every warp tile.
 __global__ void k_tile_index(const int64_t *__restrict__ occ_off, int64_t n_occ, int64_t n,
                              int64_t n_tiles, int32_t *__restrict__ c0, int32_t *__restrict__ c1) {
@@ -652,7 +883,7 @@ static int ring_blocks_per_sm(const void *fn, size_t smem) {
         const void *fn;
         int blocks;
     };
-    static Entry cache[8];
+    static Entry cache[32];
     static int n = 0;
     for (int i = 0; i < n; ++i)
         if (cache[i].fn == fn) return cache[i].blocks;
@@ -664,7 +895,7 @@ static int ring_blocks_per_sm(const void *fn, size_t smem) {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, 256, smem) != cudaSuccess || b < 1)
         b = 1;
-    if (n < 8) cache[n++] = {fn, b};
+    if (n < 32) cache[n++] = {fn, b};
     return b;
 }
 
@@ -823,6 +1054,100 @@ int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
     if (rc) return rc;
     return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits, d_cache,
                           d_accum4, stream);
+}
+
+int ls_tile_worklist_views(const ls_scene *scene, const uint32_t *d_keep_bits,
+                           int64_t bits_stride, int32_t n_views, uint32_t *d_list,
+                           uint32_t *d_status, uint32_t *d_count, void *stream) {
+    if (!scene_ok(scene, d_list) || !d_keep_bits || !d_list || !d_status || !d_count ||
+        n_views < 1 || n_views > LS_MAX_VIEWS || bits_stride < (scene->n_occ + 31) / 32)
+        return LS_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = launch_pdl(k_zero_count, dim3(1), dim3(32), 0, st, d_count);
+    if (e != cudaSuccess) return (int)e;
+    if (scene->n_points == 0) return 0;
+    SceneArgs a = scene_args(*scene);
+    a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    return (int)launch_pdl(k_tile_list_views, dim3(grid_for(a.n_tiles, 256, 8)), dim3(256), 0, st,
+                           a, d_keep_bits, bits_stride, (int)n_views, d_list, d_status, d_count);
+}
+
+size_t ls_frame_views_cache_bytes(const ls_scene *scene, int32_t n_views) {
+    if (n_views < 1 || n_views > LS_MAX_VIEWS) return 0;
+    return ls_frame_cache_bytes(scene) * (size_t)n_views;
+}
+
+}  // extern "C"
+
+namespace ls {
+
+template <int NV>
+static int launch_views(const SceneArgs &a, const ViewCams &vc, int nv, int64_t npix,
+                        const uint32_t *bits, int64_t stride, const uint32_t *list,
+                        const uint32_t *status, const uint32_t *count, double ope,
+                        uint64_t *minz, uint32_t *cache, float *acc, cudaStream_t st) {
+    cudaError_t e = launch_pdl(k_frame_pass1_views<NV>,
+                               dim3(frame_grid(k_frame_pass1_views<NV>, kSmem1, a.n_tiles)),
+                               dim3(256), kSmem1, st, a, vc, nv, npix, bits, stride, list, status,
+                               count, (unsigned long long *)minz, cache);
+    if (e != cudaSuccess) return (int)e;
+    if (cache) {
+        constexpr size_t kSm = TileRing<kPass2Stages, kRgb>::kBytes;
+        return (int)launch_pdl(k_frame_pass2_views_cached<NV>,
+                               dim3(frame_grid(k_frame_pass2_views_cached<NV>, kSm, a.n_tiles)),
+                               dim3(256), kSm, st, a, vc, nv, npix, list, status, count,
+                               (const uint32_t *)cache, ope, (const unsigned long long *)minz,
+                               acc);
+    }
+    return (int)launch_pdl(k_frame_pass2_views<NV>,
+                           dim3(frame_grid(k_frame_pass2_views<NV>, kSmem2, a.n_tiles)),
+                           dim3(256), kSmem2, st, a, vc, nv, npix, bits, stride, list, status,
+                           count, ope, (const unsigned long long *)minz, acc);
+}
+
+}  // namespace ls
+
+extern "C" {
+
+int ls_frame_project_views(const ls_scene *scene, const uint32_t *d_keep_bits,
+                           int64_t bits_stride, uint32_t *d_list, uint32_t *d_status,
+                           uint32_t *d_count, const ls_camera *cams, int32_t n_views,
+                           double eps_rel, uint64_t *d_minz_bits, uint32_t *d_cache,
+                           float *d_accum4, void *stream) {
+    if (!scene_ok(scene, d_keep_bits ? d_list : nullptr) || !cams || n_views < 1 ||
+        n_views > LS_MAX_VIEWS || !d_minz_bits || !d_accum4)
+        return LS_EINVAL;
+    ViewCams vc;
+    for (int v = 0; v < n_views; ++v) {
+        if (!camera_ok(cams + v) || cams[v].width != cams[0].width ||
+            cams[v].height != cams[0].height || !cache_ok(cams + v, d_cache))
+            return LS_EINVAL;
+        vc.c[v] = make_cam(cams[v]);
+    }
+    for (int v = n_views; v < LS_MAX_VIEWS; ++v) vc.c[v] = vc.c[0];
+    if (scene->n_points == 0) return 0;
+    int rc = 0;
+    if (d_keep_bits) {
+        rc = ls_tile_worklist_views(scene, d_keep_bits, bits_stride, n_views, d_list, d_status,
+                                    d_count, stream);
+        if (rc) return rc;
+    } else {
+        d_list = d_status = d_count = nullptr;
+    }
+    SceneArgs a = scene_args(*scene);
+    a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    const int64_t npix = cams[0].width * cams[0].height;
+    const double ope = 1.0 + eps_rel;  // rounded once (_native.pyx:135)
+    cudaStream_t st = (cudaStream_t)stream;
+    auto go = [&](auto tag) {
+        return launch_views<decltype(tag)::value>(a, vc, n_views, npix, d_keep_bits, bits_stride,
+                                                  d_list, d_status, d_count, ope, d_minz_bits,
+                                                  d_cache, d_accum4, st);
+    };
+    if (n_views == 1) return go(std::integral_constant<int, 1>());
+    if (n_views == 2) return go(std::integral_constant<int, 2>());
+    if (n_views <= 4) return go(std::integral_constant<int, 4>());
+    return go(std::integral_constant<int, 8>());
 }
 
 }  // extern "C"

@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from .filtering import FilterParams
 from .frame import FrameRGBDA, RenderParams
-from .render import FrameBuffers, project_scene
+from .render import FrameBuffers, ViewBuffers, project_scene, project_scene_views
 
 # kernel launches per frame of the fused path: cull, work-list counter reset,
 # tile work list, pass 1, pass 2, assemble+pyramid, L filter steps (+ U-Net
@@ -201,3 +201,78 @@ class FrameRenderer:
         if self.unet is not None:
             return self.height * self.width * 3 * 4
         return self.height * self.width * (3 * 4 + 4 + 1)
+
+
+class ViewBatchRenderer:
+    """A batch of camera views of one resident scan per call (BASELINE
+    configs[4]: view-parallel reconstruction).  Each call culls every view,
+    runs ONE multi-view pass pair over the scan (ls_frame_project_views: a
+    tile is read once for all views), one assemble/filter per view into row v
+    of a batched U-Net input, and one batched U-Net forward.  Every view's
+    frame is identical to ``FrameRenderer`` rendering it alone."""
+
+    def __init__(self, grid, width: int, height: int, n_views: int,
+                 render_params: RenderParams | None = None,
+                 filter_params: FilterParams | None = None, unet=None):
+        import torch
+
+        self.device = _lib.device()
+        self.scene = grid.scene()
+        self.width, self.height, self.n_views = int(width), int(height), int(n_views)
+        self.rp = render_params or RenderParams()
+        self.fp = filter_params or FilterParams()
+        self.vbufs = ViewBuffers(width, height, n_views, self.device)
+        h, w, k, dev = self.height, self.width, self.n_views, self.device
+        n = _lib.load().ls_pyramid_floats(h, w, self.fp.levels_n)
+        if n < 0:
+            raise ValueError(f"image {w}x{h} too small for {self.fp.levels_n} pyramid levels")
+        self.pyramid = torch.empty(int(n), dtype=torch.float32, device=dev)
+        self.unet = unet
+        self.frgb = self.fdepth = self.falpha = None
+        self.unet_in = self.rgb_out = None
+        if unet is None:
+            self.frgb = torch.empty((k, h, w, 3), dtype=torch.float32, device=dev)
+            self.fdepth = torch.empty((k, h, w), dtype=torch.float32, device=dev)
+            self.falpha = torch.empty((k, h, w), dtype=torch.uint8, device=dev)
+        else:
+            uh = (h + unet.divisor - 1) // unet.divisor * unet.divisor
+            if w % unet.divisor:
+                raise ValueError("frame width must be divisible by 2^depth for the U-Net")
+            self.unet_in = torch.zeros((k, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
+            self.rgb_out = torch.empty((k, uh, w, 3), dtype=torch.float32, device=dev)
+
+    @property
+    def launches_per_batch(self) -> int:
+        # per view: cull, assemble+pyramid, L filter steps; per batch: count
+        # reset, work list, 2 passes (+ U-Net layers)
+        n = self.n_views * (2 + self.fp.levels_n) + 4
+        if self.unet is not None:
+            n += self.unet.launches
+        return n
+
+    def enqueue(self, cameras) -> None:
+        """Enqueue one batch (len(cameras) == n_views) on the current stream."""
+        filtered = None if self.unet is not None else (self.frgb, self.fdepth, self.falpha)
+        project_scene_views(self.scene, cameras, self.rp.zbuffer_epsilon_rel, self.vbufs,
+                            cull=True, filter_params=self.fp, filtered=filtered,
+                            unet_in=self.unet_in, pyramid=self.pyramid)
+        if self.unet is not None:
+            self.unet.forward(self.unet_in, self.rgb_out)
+
+    def check_flags(self) -> None:
+        if int(self.vbufs.flags.max().item()):
+            raise RuntimeError("f32 accumulator bound exceeded; use project_points() for "
+                               "the exact path")
+
+    def render(self, cameras):
+        """Public call: one batch, results on the host.  Returns a list of
+        (H,W,3) f32 U-Net outputs, or of filtered FrameRGBDA frames."""
+        import torch
+
+        self.enqueue(cameras)
+        if self.unet is not None:
+            out = self.rgb_out[:, : self.height].cpu().numpy()
+            return [out[v] for v in range(self.n_views)]
+        rgb, depth, alpha = (t.cpu().numpy() for t in (self.frgb, self.fdepth, self.falpha))
+        torch.cuda.current_stream().synchronize()
+        return [FrameRGBDA(rgb[v], depth[v], alpha[v]) for v in range(self.n_views)]

@@ -80,6 +80,22 @@ class DeviceScene:
                                        _lib.stream_ptr()), "cull")
         return bits
 
+    def view_buffers(self):
+        """Multi-view cull/work-list buffers (allocated on first use):
+        (LS_MAX_VIEWS, words) keep bits, work list, per-entry view status, count."""
+        vb = getattr(self, "_view_bufs", None)
+        if vb is None:
+            import torch
+
+            dev = self.keep_bits.device
+            words = int(self.keep_bits.shape[0])
+            vb = (torch.empty((_lib.LS_MAX_VIEWS, words), dtype=torch.int32, device=dev),
+                  torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev),
+                  torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev),
+                  torch.zeros(1, dtype=torch.int32, device=dev))
+            self._view_bufs = vb
+        return vb
+
     def worklist(self):
         """Frame work list of non-culled tiles from the current keep bits."""
         _lib.check(_lib.load().ls_tile_worklist(self.struct, self.keep_bits.data_ptr(),

@@ -180,6 +180,123 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
         ev[3].record()
 
 
+class ViewBuffers:
+    """Pass buffers of a batch of same-size views (ls_frame_project_views):
+    view v's minz / accum are rows v of one block, its raw frame rows v of
+    (n_views, H, W, ...) tensors."""
+
+    def __init__(self, width: int, height: int, n_views: int, device):
+        import torch
+
+        if not 1 <= n_views <= _lib.LS_MAX_VIEWS:
+            raise ValueError(f"n_views must be in [1, {_lib.LS_MAX_VIEWS}]")
+        self.width, self.height, self.n_views = int(width), int(height), int(n_views)
+        npix = self.width * self.height
+        k, h, w = self.n_views, self.height, self.width
+        self.minz = torch.full((k, npix), _lib.INF_BITS, dtype=torch.int64, device=device)
+        self.accum = torch.zeros((k, npix, 4), dtype=torch.float32, device=device)
+        self.rgb = torch.empty((k, h, w, 3), dtype=torch.float32, device=device)
+        self.depth = torch.empty((k, h, w), dtype=torch.float32, device=device)
+        self.alpha = torch.empty((k, h, w), dtype=torch.uint8, device=device)
+        self.flags = torch.zeros(k, dtype=torch.int32, device=device)
+
+
+def views_cache(scene, camera: CameraModel, n_views: int):
+    """The scene's multi-view pass-1 -> pass-2 cache (n_views KB per warp tile,
+    grown on demand), or None when disabled / the frame is too large."""
+    if not USE_FRAME_CACHE or camera.width * camera.height >= 0xFFFFFFFF:
+        return None
+    nbytes = int(_lib.load().ls_frame_views_cache_bytes(scene.struct, n_views))
+    c = getattr(scene, "_views_cache", None)
+    if c is None or c.numel() * 4 < nbytes:
+        import torch
+
+        c = torch.empty(max(nbytes // 4, 4), dtype=torch.int32, device=_lib.device())
+        scene._views_cache = c
+    return c
+
+
+def project_scene_views(scene: DeviceScene, cameras, eps_rel: float, vb: ViewBuffers,
+                        cull: bool = True, filter_params=None, filtered=None, keep=None,
+                        unet_in=None, unet_znear: float = 0.1, pyramid=None) -> None:
+    """Enqueue a batch of views on the current stream (no host sync): per-view
+    culls, ONE multi-view pass pair over the scan (each tile read once for all
+    views), then one assemble/filter per view.  ``filtered`` / ``keep`` /
+    ``unet_in``: optional per-view outputs indexed by view (row v).  Each view's
+    frame is bit-identical to ``project_scene`` of that view alone."""
+    cameras = list(cameras)
+    k = len(cameras)
+    if k != vb.n_views:
+        raise ValueError(f"{k} cameras for a batch of {vb.n_views} views")
+    if any(c.width != vb.width or c.height != vb.height for c in cameras):
+        raise ValueError("every view of a batch must have the batch's width and height")
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    cams = (_lib.LsCamera * k)(*[_lib.make_camera(c) for c in cameras])
+    bits = lst = status = cnt = None
+    stride = 0
+    if cull:
+        vbits, lst_t, status_t, cnt_t = scene.view_buffers()
+        for v, cam in enumerate(cameras):
+            scene.cull_bits(extract_frustum(cam).planes, out=vbits[v])
+        bits, stride = vbits.data_ptr(), int(vbits.shape[1])
+        lst, status, cnt = lst_t.data_ptr(), status_t.data_ptr(), cnt_t.data_ptr()
+    cache = _lib.ptr(views_cache(scene, cameras[0], k))
+    _lib.check(lib.ls_frame_project_views(scene.struct, bits, stride, lst, status, cnt, cams, k,
+                                          float(eps_rel), vb.minz.data_ptr(), cache,
+                                          vb.accum.data_ptr(), st), "frame_project_views")
+    fp = None if filter_params is None else _lib.make_filter(filter_params)
+    for v in range(k):
+        frgb = fdepth = falpha = None
+        if filtered is not None:
+            frgb, fdepth, falpha = (None if t is None else t[v] for t in filtered)
+        uin = None if unet_in is None else unet_in[v]
+        unet_h, unet_c = (0, 0) if uin is None else (int(uin.shape[-3]), int(uin.shape[-1]))
+        _lib.check(lib.ls_frame_finish(vb.minz[v].data_ptr(), vb.accum[v].data_ptr(), vb.width,
+                                       vb.height, fp, vb.rgb[v].data_ptr(),
+                                       vb.depth[v].data_ptr(), vb.alpha[v].data_ptr(),
+                                       _lib.ptr(frgb), _lib.ptr(fdepth), _lib.ptr(falpha),
+                                       _lib.ptr(None if keep is None else keep[v]),
+                                       _lib.ptr(uin), unet_h, unet_c, float(unet_znear),
+                                       _lib.ptr(pyramid), vb.flags[v:].data_ptr(), st),
+                   "frame_finish")
+
+
+def project_points_views(cloud: PointCloud, grid: UniformGrid | None, cameras,
+                         params: RenderParams | None = None) -> list[FrameRGBDA]:
+    """``project_points`` for a batch of same-size cameras in one multi-view
+    pass pair (at most LS_MAX_VIEWS per batch; longer lists run in batches).
+    Returns one frame per camera, each identical to ``project_points``."""
+    params = params or RenderParams()
+    cameras = list(cameras)
+    if not cameras:
+        return []
+    dev = _lib.device()
+    if grid is None:
+        pos, col = cloud.device_arrays()
+        scene = _brute_scene(cloud, pos, col)
+        cull = False
+    else:
+        scene = grid.scene()
+        cull = True
+    out = []
+    for b0 in range(0, len(cameras), _lib.LS_MAX_VIEWS):
+        batch = cameras[b0:b0 + _lib.LS_MAX_VIEWS]
+        if not scene.n_points:
+            out += [FrameRGBDA.empty(c.width, c.height) for c in batch]
+            continue
+        vb = ViewBuffers(batch[0].width, batch[0].height, len(batch), dev)
+        project_scene_views(scene, batch, params.zbuffer_epsilon_rel, vb, cull=cull)
+        flags = vb.flags.cpu().numpy()
+        rgb, depth, alpha = vb.rgb.cpu().numpy(), vb.depth.cpu().numpy(), vb.alpha.cpu().numpy()
+        for v, cam in enumerate(batch):
+            if flags[v] & 1:
+                out.append(_exact_frame(cloud, grid, cam, params))
+            else:
+                out.append(FrameRGBDA(rgb[v], depth[v], alpha[v]))
+    return out
+
+
 def _exact_frame(cloud, grid, camera, params):
     """Exact (u64 x 4) path, used if a pixel may exceed the f32 accumulator bound."""
     cands = candidates(cloud, grid, camera)
