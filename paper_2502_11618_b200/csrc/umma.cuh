@@ -104,6 +104,22 @@ __device__ __forceinline__ void fence_after_sync() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// One elected lane of a fully active warp (elect.sync): the single-thread
+// roles (TMA producer, MMA issuer) run under it so ptxas knows exactly one
+// thread issues the uniform-datapath instructions (with a plain lane == 0 test
+// every tcgen05.mma / TMA issue gets an ELECT serialisation loop around it).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t"
+        "}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void fence_before_sync() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }

@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
     const uint32_t tmem = *tslot;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elect_one()) {
             // ------------------------------ TMA producer ------------------------------
             if (p.resident) {
                 mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk);
@@ -234,16 +234,15 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
             // the previous layer's activations are complete and visible past here;
             // every global write of this kernel depends on loads issued after it
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            uint32_t it = 0;
+            int s = 0;
+            uint32_t ph = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
                 const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
                 for (int q = 0; q < p.nq; ++q) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
                     const CUtensorMap *ma = second ? &mA1 : &mA0;
-                    for (int kg = 0; kg < n_kg; ++kg, ++it) {
-                        const int s = (int)(it % (uint32_t)S);
-                        const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    for (int kg = 0; kg < n_kg; ++kg, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                         mbar_wait(empty + s, ph ^ 1u);
                         uint8_t *st = smem + (size_t)s * p.stage_bytes;
                         mbar_expect_tx(full + s, p.kxps * (p.a_tx + (p.resident ? 0u : p.b_blk)));
@@ -260,23 +259,22 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
             const uint32_t idesc = idesc_bf16(128, BN);
             const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
             const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
             if (p.resident) mbar_wait(bres, 0);
             const uint32_t a_box16 = p.a_bytes >> 4, b_blk16 = p.b_blk >> 4;
-            uint32_t it = 0, acc = 0;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
-                const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
+            int s = 0;
+            uint32_t ph = 0, ab = 0, aph = 0;
+            for (int item = blockIdx.x; item < p.n_items;
+                 item += gridDim.x, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
                 mbar_wait(tempty + ab, aph ^ 1u);
                 fence_after_sync();
                 const uint32_t d0 = tmem + ab * C::kItemCols;
                 for (int q = 0; q < p.nq; ++q) {
-                    for (int kg = 0; kg < n_kg; ++kg, ++it) {
-                        const int s = (int)(it % (uint32_t)S);
-                        const uint32_t ph = (it / (uint32_t)S) & 1u;
+                    for (int kg = 0; kg < n_kg; ++kg, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                         mbar_wait(full + s, ph);
                         fence_after_sync();
                         const uint32_t st = sbase + (uint32_t)s * p.stage_bytes;
@@ -546,7 +544,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
     const uint32_t tmem = *tslot;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elect_one()) {
             // ------------------------------ TMA producer ------------------------------
             // resident weights: block (q, ky) = 3*COUT rows [kx][co], from taps kx*3+ky
             mbar_expect_tx(bres, (uint32_t)(9 * p.nq) * p.b_blk);
@@ -559,15 +557,14 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
                                     kx * 3 + ky, bres);
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
-            uint32_t it = 0;
+            int s = 0;
+            uint32_t ph = 0;
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
                 int img, x0, y0;
                 pos(item, img, x0, y0);
-                for (int q = 0; q < p.nq; ++q, ++it) {
+                for (int q = 0; q < p.nq; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
-                    const int s = (int)(it % (uint32_t)S);
-                    const uint32_t ph = (it / (uint32_t)S) & 1u;
                     mbar_wait(empty + s, ph ^ 1u);
                     mbar_expect_tx(full + s, p.a_tx);
                     tma_load_4d(smem + (size_t)s * p.stage_bytes, second ? &mA1 : &mA0, c, x0 - 1,
@@ -576,21 +573,20 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        if (elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
             const uint32_t idesc = idesc_bf16(128, C::kN);
             const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
             const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
             mbar_wait(bres, 0);
-            uint32_t it = 0, acc = 0;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++acc) {
-                const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
+            int s = 0;
+            uint32_t ph = 0, ab = 0, aph = 0;
+            for (int item = blockIdx.x; item < p.n_items;
+                 item += gridDim.x, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
                 mbar_wait(tempty + ab, aph ^ 1u);
                 fence_after_sync();
                 const uint32_t d0 = tmem + ab * C::kN;
-                for (int q = 0; q < p.nq; ++q, ++it) {
-                    const int s = (int)(it % (uint32_t)S);
-                    const uint32_t ph = (it / (uint32_t)S) & 1u;
+                for (int q = 0; q < p.nq; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     mbar_wait(full + s, ph);
                     fence_after_sync();
                     const uint32_t a_lo = dlo + ((sbase + (uint32_t)s * p.stage_bytes) >> 4);

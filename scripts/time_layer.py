@@ -37,7 +37,8 @@ def layer(c0, c1, cout, h, w, pool=False, transposed=False, reps=10):
     return e0.elapsed_time(e1) / reps * 1e3
 
 H, W = 1088, 1920
-print(os.environ.get("LS_CONV_MAX_STAGES"), os.environ.get("LS_CONV_CTAS_PER_SM"),
+if os.environ.get("LS_TIME_LAYER_NO_MAIN") != "1":
+  print(os.environ.get("LS_CONV_MAX_STAGES"), os.environ.get("LS_CONV_CTAS_PER_SM"),
       "e0c2 %.1f us" % layer(32, 0, 32, H, W, pool=True),
       "d0c1 %.1f us" % layer(32, 32, 32, H, W),
       "e1c2 %.1f us" % layer(64, 0, 64, H // 2, W // 2, pool=True),
