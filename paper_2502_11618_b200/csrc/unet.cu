@@ -40,6 +40,14 @@ namespace unet {
 
 using namespace ls::umma;
 
+// sub-tiles per work item of the 128 / 256-column tiles (A/B build switches)
+#ifndef LS_MT128
+#define LS_MT128 1
+#endif
+#ifndef LS_MT256
+#define LS_MT256 1
+#endif
+
 constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
 constexpr size_t kSmemBudget = 222 * 1024;
@@ -77,7 +85,7 @@ struct CfgP {
     static constexpr uint32_t kRow = CHUNK * 2;  // bytes per operand row
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
-    static constexpr int kMT = BN <= 32 ? 4 : (BN <= 64 ? 2 : 1);      // sub-tiles per item
+    static constexpr int kMT = BN <= 32 ? 4 : (BN <= 64 ? 2 : (BN <= 128 ? LS_MT128 : LS_MT256));
     static constexpr int kItemCols = kMT * BN;                          // TMEM columns per item
     static constexpr int kAcc = 512 / kItemCols >= 4 ? 4 : 512 / kItemCols;
     static constexpr int kEpiGroups = kAcc >= 4 ? 3 : (kAcc >= 3 ? 2 : 1);
@@ -100,6 +108,42 @@ __device__ __forceinline__ float act_slope(int act, float alpha) {
 
 __device__ __forceinline__ float apply_act(float v, float slope) { return fmaxf(v, slope * v); }
 
+// Packed f32x2 arithmetic (FADD2 / FFMA2 / FMUL2 on sm_100): two channels per
+// instruction with exactly the scalar ops' IEEE results, so the packed
+// epilogue computes bit-identical values with fewer issue slots.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 f2(float lo, float hi) {
+    f32x2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void unf2(f32x2 v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f32x2 add2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f32x2 fma2(f32x2 a, f32x2 b, f32x2 c) {
+    f32x2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f32x2 mul2(f32x2 a, f32x2 b) {
+    f32x2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+// apply_act on a channel pair: max(v, slope * v)
+__device__ __forceinline__ void act2(f32x2 y, f32x2 slope2, float &a, float &b) {
+    float c, d;
+    unf2(y, a, b);
+    unf2(mul2(y, slope2), c, d);
+    a = fmaxf(a, c);
+    b = fmaxf(b, d);
+}
+
 __device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
     __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162 *>(&a);
     __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162 *>(&b);
@@ -119,6 +163,25 @@ __device__ __forceinline__ uint32_t hmax4(uint32_t a, uint32_t b, uint32_t c, ui
     __nv_bfloat162 w = *reinterpret_cast<__nv_bfloat162 *>(&d);
     __nv_bfloat162 m = __hmax2(__hmax2(x, y), __hmax2(z, w));
     return *reinterpret_cast<uint32_t *>(&m);
+}
+
+// Final 1x1 conv partial sums over 16 channels (same sequential FMA order
+// per output as a scalar loop; weights read as float4 broadcasts).
+__device__ __forceinline__ void head_accumulate(const float *s_hw, int cout, int head_c, int n,
+                                                const float (&v)[16], float (&hacc)[4]) {
+#pragma unroll
+    for (int j2 = 0; j2 < 4; ++j2) {
+        if (j2 >= head_c) break;
+        const float4 *w4 = reinterpret_cast<const float4 *>(s_hw + j2 * cout + n);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 w = w4[q];
+            hacc[j2] = fmaf(w.x, v[4 * q], hacc[j2]);
+            hacc[j2] = fmaf(w.y, v[4 * q + 1], hacc[j2]);
+            hacc[j2] = fmaf(w.z, v[4 * q + 2], hacc[j2]);
+            hacc[j2] = fmaf(w.w, v[4 * q + 3], hacc[j2]);
+        }
+    }
 }
 
 // floor(a / b) for 0 <= a < 2^24, b >= 1 via one f32 reciprocal + correction
@@ -320,6 +383,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
         const int m = quarter * 32 + lane;
         const int tx = m % kTW, ty = m / kTW;
         const float slope = act_slope(p.act, p.alpha);
+        const f32x2 slope2 = f2(slope, slope);
         uint32_t acc = (uint32_t)eg;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
@@ -351,20 +415,18 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
 #pragma unroll
                     for (int i4 = 0; i4 < 4; ++i4) {
                         const float4 sc = sc4[i4], sh = sh4[i4];
-                        const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
-                        const float shv[4] = {sh.x, sh.y, sh.z, sh.w};
+                        const f32x2 sc2[2] = {f2(sc.x, sc.y), f2(sc.z, sc.w)};
+                        const f32x2 sh2[2] = {f2(sh.x, sh.y), f2(sh.z, sh.w)};
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            v[4 * i4 + j] = apply_act(
-                                fmaf(__uint_as_float(rr[h2 * 16 + 4 * i4 + j]), scv[j], shv[j]),
-                                slope);
+                        for (int jp = 0; jp < 2; ++jp) {
+                            const int i = 4 * i4 + 2 * jp;
+                            const f32x2 x = f2(__uint_as_float(rr[h2 * 16 + i]),
+                                               __uint_as_float(rr[h2 * 16 + i + 1]));
+                            act2(fma2(x, sc2[jp], sh2[jp]), slope2, v[i], v[i + 1]);
+                        }
                     }
                     if (MODE == kHead) {
-                        for (int j2 = 0; j2 < p.head_c; ++j2) {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
-                        }
+                        head_accumulate(s_hw, p.cout, p.head_c, n, v, hacc);
                         if (!p.y && !p.y_f32) continue;  // head input not materialised
                     }
                     uint32_t pk[8];
@@ -614,6 +676,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
         const int m = quarter * 32 + lane;
         const int tx = m % kTW, ty = m / kTW;  // input pixel of this lane
         const float slope = act_slope(p.act, p.alpha);
+        const f32x2 slope2 = f2(slope, slope);
         uint32_t acc = (uint32_t)eg;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
@@ -646,24 +709,25 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
 #pragma unroll
                 for (int i4 = 0; i4 < 4; ++i4) {
                     const float4 sc = sc4[i4], sh = sh4[i4];
-                    const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
-                    const float shv[4] = {sh.x, sh.y, sh.z, sh.w};
+                    const f32x2 sc2[2] = {f2(sc.x, sc.y), f2(sc.z, sc.w)};
+                    const f32x2 sh2[2] = {f2(sh.x, sh.y), f2(sh.z, sh.w)};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int i = 4 * i4 + j;
-                        // T0 of the left neighbour, T2 of the right one
-                        const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(t0[i]), 1);
-                        const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(t2[i]), 1);
-                        const float d = (left + __uint_as_float(t1[i])) + right;
-                        v[i] = apply_act(fmaf(d, scv[j], shv[j]), slope);
+                    for (int jp = 0; jp < 2; ++jp) {
+                        const int i = 4 * i4 + 2 * jp;
+                        // T0 of the left neighbour, T2 of the right one, two channels at a time
+                        const f32x2 left =
+                            f2(__shfl_up_sync(0xffffffffu, __uint_as_float(t0[i]), 1),
+                               __shfl_up_sync(0xffffffffu, __uint_as_float(t0[i + 1]), 1));
+                        const f32x2 right =
+                            f2(__shfl_down_sync(0xffffffffu, __uint_as_float(t2[i]), 1),
+                               __shfl_down_sync(0xffffffffu, __uint_as_float(t2[i + 1]), 1));
+                        const f32x2 mid = f2(__uint_as_float(t1[i]), __uint_as_float(t1[i + 1]));
+                        const f32x2 d = add2(add2(left, mid), right);
+                        act2(fma2(d, sc2[jp], sh2[jp]), slope2, v[i], v[i + 1]);
                     }
                 }
                 if (MODE == kHead) {
-                    for (int j2 = 0; j2 < p.head_c; ++j2) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            hacc[j2] = fmaf(s_hw[j2 * p.cout + n + i], v[i], hacc[j2]);
-                    }
+                    head_accumulate(s_hw, p.cout, p.head_c, n, v, hacc);
                     if (!p.y && !p.y_f32) continue;
                 }
                 uint32_t pk[8];
@@ -868,7 +932,7 @@ static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
     }
 }
 
-static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : 1); }
+static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : (bn <= 128 ? LS_MT128 : LS_MT256)); }
 
 }  // namespace unet
 }  // namespace ls
