@@ -5,7 +5,8 @@ os.environ.setdefault("LS_TIME_LAYER_NO_MAIN", "1")
 from time_layer import layer, H, W  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "d0c1"
-cfg = {"e0c2": dict(c0=32, c1=0, cout=32, h=H, w=W, pool=True),
+cfg = {"e0c1": dict(c0=8, c1=0, cout=32, h=H, w=W),
+       "e0c2": dict(c0=32, c1=0, cout=32, h=H, w=W, pool=True),
        "d0c1": dict(c0=32, c1=32, cout=32, h=H, w=W),
        "e1c2": dict(c0=64, c1=0, cout=64, h=H // 2, w=W // 2, pool=True),
        "d0up": dict(c0=64, c1=0, cout=32, h=H // 2, w=W // 2, transposed=True)}[name]
