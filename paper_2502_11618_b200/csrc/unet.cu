@@ -772,6 +772,304 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// cout = 32 convolutions over pixel PAIRS (the full-resolution e0c2, d0c1,
+// d0c2 + head layers; sources of 32 channels).  The NHWC input is read as
+// (W/2) "pair pixels" of 64 channels P(j) = [x(2j), x(2j+1)] (one 128 B
+// swizzled operand row), so a 128-row A tile is 8 rows x 16 pairs and TMEM
+// lane j holds both outputs of its pair, N = 64 = [out(2j) | out(2j+1)]:
+//   MMA_0  (N=64)  A = P(j),   B rows [W(kx=1+e) ; W(kx=e)] for element e
+//                  -- every tap whose input and output share the pair
+//   MMA_-1 (N=32)  A = P(j-1) element 1 = x(2j-1), B = W(kx=0) -> out(2j)
+//   MMA_+1 (N=32)  A = P(j+1) element 0 = x(2j+2), B = W(kx=2) -> out(2j+1)
+// MMA_-1 / MMA_+1 address the neighbouring pair through a descriptor start
+// one operand row earlier / later (tcgen05 descriptors may start at any row
+// of a swizzled tile, scripts/umma_shift_test.cu), so the kx sum happens in
+// the tensor core: the epilogue has no cross-lane shuffles and reads 32 TMEM
+// columns per output pixel instead of 96 (k_conv_kx).  Lanes of pair columns
+// 0 and 15 of a tile row see the wrong neighbour: tiles advance by 14 pairs.
+// Weights stay resident, loaded from the ABI's [tap][n][c] layout as
+// 16-channel x 32-row boxes into 32 B-swizzled B tiles.
+constexpr int kPxCols = 14;  // output pairs per tile row
+
+struct CfgPx {
+    static constexpr uint32_t kRow = 128;        // A operand row: 64 bf16 channels
+    static constexpr int kN = 64;                // [out(2j) | out(2j+1)] x 32
+    static constexpr int kAcc = 7;               // TMEM buffers of 64 columns
+    static constexpr int kEpiGroups = 4;
+    static constexpr int kThreads = 64 + 128 * kEpiGroups;
+    static constexpr int kTmemCols = 512;
+    static constexpr uint32_t kBTile = 2048;     // 64 rows x 32 B
+    static constexpr uint32_t kRingPad = 1024;   // MMA_-1 of stage 0 reads one row before it
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
+    const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+    const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
+    using C = CfgPx;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    const int S = p.stages;
+    float *sconst = reinterpret_cast<float *>(smem + p.off_const);
+    const float *s_scale = sconst;
+    const float *s_shift = sconst + p.n_total;
+    const float *s_hw = sconst + 2 * p.n_total;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + C::kAcc;
+    uint64_t *bres = tempty + C::kAcc;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
+    const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
+    const float r_tx = 1.0f / (float)p.tiles_x;
+    // item -> (image, first loaded pair column, first row)
+    auto pos = [&](int item, int &img, int &px0, int &y0) {
+        img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
+        const int r = item - img * p.tiles_x * p.tiles_y;
+        const int ty = fdiv(r, p.tiles_x, r_tx);
+        y0 = ty * kTH;
+        px0 = (r - ty * p.tiles_x) * kPxCols - 1;
+    };
+    const int nsrc = p.nq;  // 1 or 2 sources of 32 channels, one 64-channel pair chunk each
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, 1);
+            }
+            for (int a = 0; a < C::kAcc; ++a) {
+                mbar_init(tfull + a, 1);
+                mbar_init(tempty + a, 4);
+            }
+            mbar_init(bres, 1);
+            fence_barrier_init();
+            tma_prefetch(&mA0);
+            if (nsrc > 1) tma_prefetch(&mA1);
+            tma_prefetch(&mB);
+        }
+        __syncwarp();
+        tmem_alloc(tslot, C::kTmemCols);
+    } else if (warp >= 2) {
+        const int t = threadIdx.x - 64;
+        constexpr int kEpiThreads = 128 * C::kEpiGroups;
+        for (int i = t; i < p.n_total; i += kEpiThreads) {
+            sconst[i] = p.scale[i];
+            sconst[p.n_total + i] = p.shift[i];
+        }
+        if (MODE == kHead)
+            for (int i = t; i < p.head_c * p.cout; i += kEpiThreads)
+                sconst[2 * p.n_total + i] = p.head_w[i];
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tslot;
+    // B tile (source s, ky, element e, channel block t): rows 0-31 = W(kx=1+e),
+    // rows 32-63 = W(kx=e), 16 channels each
+    auto btile = [&](int src, int ky, int e, int t) -> uint32_t {
+        return p.off_b + (uint32_t)((((src * 3 + ky) * 2 + e) * 2 + t)) * C::kBTile;
+    };
+
+    if (warp == 0) {
+        if (elect_one()) {
+            // ------------------------------ TMA producer ------------------------------
+            mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
+            for (int src = 0; src < nsrc; ++src)
+                for (int ky = 0; ky < 3; ++ky)
+                    for (int e = 0; e < 2; ++e)
+                        for (int t = 0; t < 2; ++t)
+                            for (int r = 0; r < 2; ++r) {
+                                const int kx = r == 0 ? 1 + e : e;
+                                tma_load_3d(smem + btile(src, ky, e, t) + r * (C::kBTile / 2), &mB,
+                                            src * 32 + 16 * t, 0, kx * 3 + ky, bres);
+                            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            int s = 0;
+            uint32_t ph = 0;
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+                int img, px0, y0;
+                pos(item, img, px0, y0);
+                for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
+                    mbar_wait(empty + s, ph ^ 1u);
+                    mbar_expect_tx(full + s, p.a_tx);
+                    tma_load_4d(smem + C::kRingPad + (size_t)s * p.stage_bytes, q ? &mA1 : &mA0, 0,
+                                px0, y0 - 1, img, full + s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            // ------------------------------- MMA issuer -------------------------------
+            const uint32_t id64 = idesc_bf16(128, 64), id32 = idesc_bf16(128, 32);
+            const uint64_t aproto = smem_desc(0, C::kRow, kSwizzle128B);
+            const uint64_t bproto = smem_desc(0, 32, kSwizzle32B);
+            const uint32_t ahi = (uint32_t)(aproto >> 32), alo = (uint32_t)aproto;
+            const uint32_t bhi = (uint32_t)(bproto >> 32), blo = (uint32_t)bproto;
+            mbar_wait(bres, 0);
+            int s = 0;
+            uint32_t ph = 0, ab = 0, aph = 0;
+            for (int item = blockIdx.x; item < p.n_items;
+                 item += gridDim.x, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
+                mbar_wait(tempty + ab, aph ^ 1u);
+                fence_after_sync();
+                const uint32_t d0 = tmem + ab * C::kN;
+                for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
+                    mbar_wait(full + s, ph);
+                    fence_after_sync();
+                    const uint32_t a_lo =
+                        alo + ((sbase + C::kRingPad + (uint32_t)s * p.stage_bytes) >> 4);
+                    const uint32_t b_lo = blo + ((sbase + btile(q, 0, 0, 0)) >> 4);
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {
+                            // A: operand row (ky*16 + pair), K offset e*64 B + t*32 B
+                            const uint32_t arow = (uint32_t)(ky * kTW) * C::kRow;
+                            const uint32_t a_e0 = (arow + 32 * t) / 16, a_e1 = (arow + 64 + 32 * t) / 16;
+                            const uint32_t b_e0 = ((ky * 2 + 0) * 2 + t) * C::kBTile / 16;
+                            const uint32_t b_e1 = ((ky * 2 + 1) * 2 + t) * C::kBTile / 16;
+                            const uint32_t first = (q | ky | t) == 0 ? 0u : 1u;
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e0),
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e0), id64, first);
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), id64, 1u);
+                            // x(2j-1) -> out(2j): previous row's element 1, W(kx=0)
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e1 - C::kRow / 16),
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e0 + C::kBTile / 32), id32, 1u);
+                            // x(2j+2) -> out(2j+1): next row's element 0, W(kx=2)
+                            mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e0 + C::kRow / 16),
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), id32, 1u);
+                        }
+                    }
+                    mma_commit(empty + s);
+                }
+                mma_commit(tfull + ab);
+            }
+        }
+    } else {
+        // --------------------------------- epilogue ---------------------------------
+        const int eg = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + lane;
+        const int tp = m % kTW, ty = m / kTW;  // pair column / row of this lane
+        const float slope = act_slope(p.act, p.alpha);
+        const f32x2 slope2 = f2(slope, slope);
+        const int wp = p.w >> 1;
+        uint32_t ab = (uint32_t)eg % C::kAcc, aph = ((uint32_t)eg / C::kAcc) & 1u;
+        for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
+             item += C::kEpiGroups * gridDim.x) {
+            int img, px0, y0;
+            pos(item, img, px0, y0);
+            mbar_wait(tfull + ab, aph);
+            fence_after_sync();
+            const uint32_t tbase = tmem + ab * C::kN + ((uint32_t)(quarter * 32) << 16);
+            const int gp = px0 + tp, gy = y0 + ty;
+            const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
+            float hacc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+            uint32_t keep[8];  // pixel 2j's packed half for the horizontal pool
+            // 16-column groups in the order (px0, ch 0-15), (px1, 0-15), (px0, 16-31),
+            // (px1, 16-31); group g+1's tcgen05.ld is in flight while g is processed
+            uint32_t ra[16], rb[16];
+            auto col = [&](int g) -> uint32_t { return tbase + (uint32_t)((g & 1) * 32 + (g >> 1) * 16); };
+            auto process = [&](int g, const uint32_t(&rr)[16]) {
+                const int px = g & 1, n = (g >> 1) * 16;
+                const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
+                const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
+                float v[16];
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                    const float4 sc = sc4[i4], sh = sh4[i4];
+                    const f32x2 sc2[2] = {f2(sc.x, sc.y), f2(sc.z, sc.w)};
+                    const f32x2 sh2[2] = {f2(sh.x, sh.y), f2(sh.z, sh.w)};
+#pragma unroll
+                    for (int jp = 0; jp < 2; ++jp) {
+                        const int i = 4 * i4 + 2 * jp;
+                        act2(fma2(f2(__uint_as_float(rr[i]), __uint_as_float(rr[i + 1])), sc2[jp],
+                                  sh2[jp]),
+                             slope2, v[i], v[i + 1]);
+                    }
+                }
+                if (MODE == kHead) {
+                    head_accumulate(s_hw, p.cout, p.head_c, n, v, hacc[px]);
+                    if (!p.y && !p.y_f32) return;
+                }
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp + px;
+                if (valid) {
+                    if (p.y) st_global_v8(p.y + pix * p.cout + n, pk);
+                    if (p.y_f32) {
+                        float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + n);
+                        dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+                        dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+                        dst[2] = make_float4(v[8], v[9], v[10], v[11]);
+                        dst[3] = make_float4(v[12], v[13], v[14], v[15]);
+                    }
+                }
+                if (MODE == kPool) {
+                    if (px == 0) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) keep[i] = pk[i];
+                    } else {
+                        // horizontal partner in-lane, vertical partner 16 lanes away
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t a = hmax2u(keep[i], pk[i]);
+                            pk[i] = hmax2u(a, __shfl_xor_sync(0xffffffffu, a, 16));
+                        }
+                        if (valid && !(ty & 1)) {
+                            const int64_t pp =
+                                ((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp;
+                            st_global_v8(p.pool + pp * p.cout + n, pk);
+                        }
+                    }
+                }
+            };
+            tmem_ld16_async(col(0), ra);
+            tmem_ld_wait16(ra);
+            tmem_ld16_async(col(1), rb);
+            process(0, ra);
+            tmem_ld_wait16(rb);
+            tmem_ld16_async(col(2), ra);
+            process(1, rb);
+            tmem_ld_wait16(ra);
+            tmem_ld16_async(col(3), rb);
+            process(2, ra);
+            tmem_ld_wait16(rb);
+            // item fully read -> hand the TMEM buffer back
+            fence_before_sync();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + ab);
+            process(3, rb);
+            if (MODE == kHead && valid) {
+#pragma unroll
+                for (int px = 0; px < 2; ++px) {
+                    const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp + px;
+                    for (int j2 = 0; j2 < p.head_c; ++j2) {
+                        const float z = hacc[px][j2] + __ldg(p.head_b + j2);
+                        p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                    }
+                }
+            }
+            // next item of this group: kEpiGroups buffers further on
+#pragma unroll 1
+            for (int k = 0; k < C::kEpiGroups; ++k) {
+                ab = ab + 1 == C::kAcc ? 0 : ab + 1;
+                aph ^= ab == 0;
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+}
+
 // ------------------------------------------------------------------ host ---
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -834,7 +1132,7 @@ struct ls_conv_plan {
     CUtensorMap a0, a1, b;
     ConvParamsP p;
     int bn, chunk, grid, mode;
-    int kind;  // 0: k_conv_p, 1: k_conv_kx (cout = 32, kx taps stacked along N)
+    int kind;  // 0: k_conv_p, 1: k_conv_kx (kx taps stacked along N), 2: k_conv_px2 (pixel pairs)
     size_t smem;
 };
 
@@ -912,6 +1210,47 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
     return pl->p.cout == 32 ? launch_kx_c<CHUNK, 32>(pl, st) : launch_kx_c<CHUNK, 64>(pl, st);
 }
 
+template <int MODE>
+static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
+    static int attr_done = 0;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)(kSmemBudget + 2048));
+        if (e != cudaSuccess) return (int)e;
+        attr_done = 1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl->grid);
+    cfg.blockDim = dim3((unsigned)CfgPx::kThreads);
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE>, pl->a0, pl->a1, pl->b, pl->p);
+}
+
+static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
+    switch (pl->mode) {
+        case kPlain: return launch_px2_m<kPlain>(pl, st);
+        case kPool: return launch_px2_m<kPool>(pl, st);
+        default: return launch_px2_m<kHead>(pl, st);
+    }
+}
+
+// LS_CONV_PX2=0 keeps the 32-channel full-resolution layers on k_conv_kx (A/B).
+static bool px2_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_CONV_PX2");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // LS_CONV_KX=0 keeps cout = 32 layers on the generic kernel (A/B measurements).
 static bool kx_enabled() {
     static int v = -1;
@@ -938,6 +1277,87 @@ static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : (bn <= 128 ? L
 }  // namespace ls
 
 static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0); }
+
+// Plan of a 32 -> 32 (or [32, 32] -> 32) 3x3 layer on k_conv_px2 (null when
+// it does not apply: odd width).
+static ls_conv_plan *plan_px2(const uint16_t *d_x0, const uint16_t *d_x1, int c1, int batch,
+                              int h, int w, const uint16_t *d_w, const float *d_scale,
+                              const float *d_shift, int act, float alpha, uint16_t *d_y,
+                              float *d_y_f32, uint16_t *d_pool, const float *d_head_w,
+                              const float *d_head_b, int head_c, float *d_head_out) {
+    using namespace ls::unet;
+    if (w % 2) return nullptr;
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
+    if (!pl) return nullptr;
+    ConvParamsP &p = pl->p;
+    p = ConvParamsP{};
+    p.batch = batch;
+    p.h = h;
+    p.w = w;
+    p.c0 = 32;
+    p.c1 = c1;
+    p.ctot = 32 + c1;
+    p.kxs = 3;
+    p.kxps = 1;
+    p.pad = 1;
+    p.n_total = 32;
+    p.cout = 32;
+    p.act = act;
+    p.alpha = alpha;
+    p.scale = d_scale;
+    p.shift = d_shift;
+    p.y = reinterpret_cast<__nv_bfloat16 *>(d_y);
+    p.y_f32 = d_y_f32;
+    p.pool = reinterpret_cast<__nv_bfloat16 *>(d_pool);
+    p.head_w = d_head_w;
+    p.head_b = d_head_b;
+    p.head_c = head_c;
+    p.head_out = d_head_out;
+    p.tiles_x = (w / 2 + kPxCols - 1) / kPxCols;
+    p.tiles_y = (h + kTH - 1) / kTH;
+    p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
+    p.n_tiles_n = 1;
+    p.n_items = p.n_tiles_m;
+    p.nq0 = 1;
+    p.nq = c1 > 0 ? 2 : 1;
+    p.a_tx = (uint32_t)(kTW * (kTH + 2)) * CfgPx::kRow;
+    p.a_bytes = (p.a_tx + 1023u) & ~1023u;
+    p.b_blk = CfgPx::kBTile;
+    p.resident = 1;
+    const size_t res_bytes = (size_t)p.nq * 12 * CfgPx::kBTile;
+    const size_t const_bytes =
+        ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
+    const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
+    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.a_bytes) : 0;
+    if (stages < 3) {
+        delete pl;
+        return nullptr;
+    }
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    p.stage_bytes = p.a_bytes;
+    p.off_b = (uint32_t)(CfgPx::kRingPad + stages * p.stage_bytes);
+    p.off_const = (uint32_t)(p.off_b + res_bytes);
+    p.off_pool = (uint32_t)(p.off_const + const_bytes);
+    p.off_bar = p.off_pool;
+    pl->smem = 1024 + p.off_bar + 512;
+    pl->bn = 32;
+    pl->chunk = 64;
+    pl->kind = 2;
+    pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    // the NHWC tensors read as (W/2) pair pixels of 64 channels
+    bool ok = encode_act(&pl->a0, d_x0, 64, w / 2, h, batch, 64, kTH + 2);
+    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, 64, w / 2, h, batch, 64, kTH + 2);
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, 32, 9, 16, 32, 1);
+    if (!ok) {
+        delete pl;
+        return nullptr;
+    }
+    return pl;
+}
 
 // Plan of a cout = 32 / 64, 3x3 layer on k_conv_kx (null when it does not
 // fit).  c0 is the K-chunk channel count of source 0 (8 -> 16), c0_tensor
@@ -1059,6 +1479,19 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     // cout = 64 items hold 192 TMEM columns (2 buffers): worth it only when the
     // K loop is long enough to cover the buffer round trip (measured: K = 128
     // 94 -> 66 us, K = 32 / 64 slower)
+    // k_conv_px2 trades epilogue work (no shuffles) for ~1.6x the SMEM operand
+    // reads of k_conv_kx: it wins on single-source layers whose epilogue bounds
+    // them (e0c2 91 -> 67 us, d0c2 + head 96 -> 81 us) and loses on the two-source
+    // d0c1 (K = 64: 99 -> 119 us, operand-bound), which stays on k_conv_kx
+    if (!transposed && cout == 32 && c0 == 32 && c1 == 0 && px2_enabled()) {
+        ls_conv_plan *pp = plan_px2(d_x0, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
+                                    alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
+                                    d_head_out);
+        if (pp) {
+            if (status) *status = 0;
+            return pp;
+        }
+    }
     const bool kx_fit = cout == 32 || (cout == 64 && c0 + c1 >= 128 && !d_head_w);
     if (!transposed && kx_fit && kx_enabled()) {
         ls_conv_plan *pk = plan_kx(d_x0, c0_tensor, c0, d_x1, c1, cout, batch, h, w, d_w, d_scale,
@@ -1179,6 +1612,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
 int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     if (!pl) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
+    if (pl->kind == 2) return launch_px2(pl, st);
     if (pl->kind == 1) {
         if (pl->chunk == 16) return launch_kx<16>(pl, st);
         if (pl->chunk == 32) return launch_kx<32>(pl, st);

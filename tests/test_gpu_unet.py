@@ -25,6 +25,14 @@ LAYER_CASES = [
     dict(c0=64, c1=0, cout=64, h=20, w=120, act=1, pool=True),
     dict(c0=64, c1=0, cout=16, h=16, w=16, act=0, batch=2),
     dict(c0=512, c1=0, cout=512, h=4, w=8, act=1),
+    # k_conv_px2 (pixel pairs): ragged tiles (50 pairs = 3.6 tiles of 14), rows
+    # not a multiple of 8, batches, pool and head epilogues
+    dict(c0=32, c1=0, cout=32, h=20, w=100, act=2, batch=2),
+    dict(c0=32, c1=32, cout=32, h=13, w=60, act=1),  # two sources: k_conv_kx
+    dict(c0=32, c1=0, cout=32, h=10, w=36, act=1, pool=True, batch=3),
+    dict(c0=32, c1=0, cout=32, h=18, w=58, act=2, head=True),
+    # odd width: k_conv_px2 does not apply (falls back to k_conv_kx)
+    dict(c0=32, c1=0, cout=32, h=9, w=31, act=1),
 ]
 
 
