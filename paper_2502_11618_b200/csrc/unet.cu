@@ -47,6 +47,11 @@ using namespace ls::umma;
 #ifndef LS_MT256
 #define LS_MT256 1
 #endif
+// k_conv_kx (cout = 32): issue the second 16-channel half's TMEM loads before
+// processing the first (A/B build switch)
+#ifndef LS_KX_PIPE
+#define LS_KX_PIPE 0
+#endif
 
 constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
@@ -68,6 +73,7 @@ struct ConvParamsP {
     const float *head_w, *head_b;
     int head_c;
     float *head_out;
+    const void *wts;        // weights [tap][n][c] (k_conv_px2 C8 builds its B tiles from it)
     int resident;           // weights resident in smem
     int stages;
     uint32_t a_bytes;       // one A box footprint (1024-aligned)
@@ -535,7 +541,9 @@ struct CfgKx {
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
     static constexpr int kN = 3 * COUT;                  // [kx][co]: 96 or 192 columns
     static constexpr int kAcc = 480 / kN;                // TMEM buffers: 5 or 2
-    static constexpr int kEpiGroups = kAcc >= 4 ? 4 : kAcc;
+    // (LS_KX_PIPE: 48 more live registers per thread -> at most 3 groups)
+    static constexpr int kEpiGroups = (LS_KX_PIPE == 1 && COUT == 32) ? (kAcc >= 3 ? 3 : kAcc)
+                                                                      : (kAcc >= 4 ? 4 : kAcc);
     static constexpr int kThreads = 64 + 128 * kEpiGroups;
     static constexpr int kTmemCols = 512;
 };
@@ -690,19 +698,15 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
             const bool inner = tx >= 1 && tx <= kKxCols;
             const bool valid = inner && gx < p.w && gy < p.h;
             float hacc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll(COUT == 32 ? 2 : 1)
-            for (int h2 = 0; h2 < COUT / 16; ++h2) {
+            auto release = [&]() {  // item fully read -> hand the TMEM buffer back
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + ab);
+            };
+            // one 16-channel half: kx sum, BN fold, activation, stores / pool / head
+            auto half = [&](int h2, const uint32_t(&t0)[16], const uint32_t(&t1)[16],
+                            const uint32_t(&t2)[16]) {
                 const int n = h2 * 16;
-                uint32_t t0[16], t1[16], t2[16];
-                tmem_ld16_async(tbase + (uint32_t)(0 * COUT + n), t0);
-                tmem_ld16_async(tbase + (uint32_t)(1 * COUT + n), t1);
-                tmem_ld16_async(tbase + (uint32_t)(2 * COUT + n), t2);
-                tmem_ld_wait3(t0, t1, t2);
-                if (h2 == COUT / 16 - 1) {  // item fully read -> hand the TMEM buffer back
-                    fence_before_sync();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(tempty + ab);
-                }
                 const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
                 const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
                 float v[16];
@@ -728,7 +732,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
                 }
                 if (MODE == kHead) {
                     head_accumulate(s_hw, p.cout, p.head_c, n, v, hacc);
-                    if (!p.y && !p.y_f32) continue;
+                    if (!p.y && !p.y_f32) return;
                 }
                 uint32_t pk[8];
 #pragma unroll
@@ -756,6 +760,33 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
                         const int64_t pp = ((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gx / 2;
                         st_global_v8(p.pool + pp * p.cout + n, pk);
                     }
+                }
+            };
+            if (LS_KX_PIPE && COUT == 32) {
+                // both halves' loads in flight before the first half is processed
+                uint32_t a0[16], a1[16], a2[16], b0[16], b1[16], b2[16];
+                tmem_ld16_async(tbase + 0u, a0);
+                tmem_ld16_async(tbase + (uint32_t)COUT, a1);
+                tmem_ld16_async(tbase + (uint32_t)(2 * COUT), a2);
+                tmem_ld_wait3(a0, a1, a2);
+                tmem_ld16_async(tbase + 16u, b0);
+                tmem_ld16_async(tbase + (uint32_t)(COUT + 16), b1);
+                tmem_ld16_async(tbase + (uint32_t)(2 * COUT + 16), b2);
+                half(0, a0, a1, a2);
+                tmem_ld_wait3(b0, b1, b2);
+                release();
+                half(1, b0, b1, b2);
+            } else {
+#pragma unroll(COUT == 32 ? 2 : 1)
+                for (int h2 = 0; h2 < COUT / 16; ++h2) {
+                    const int n = h2 * 16;
+                    uint32_t t0[16], t1[16], t2[16];
+                    tmem_ld16_async(tbase + (uint32_t)(0 * COUT + n), t0);
+                    tmem_ld16_async(tbase + (uint32_t)(1 * COUT + n), t1);
+                    tmem_ld16_async(tbase + (uint32_t)(2 * COUT + n), t2);
+                    tmem_ld_wait3(t0, t1, t2);
+                    if (h2 == COUT / 16 - 1) release();
+                    half(h2, t0, t1, t2);
                 }
             }
             if (MODE == kHead && valid) {
@@ -803,7 +834,13 @@ struct CfgPx {
     static constexpr uint32_t kRingPad = 1024;   // MMA_-1 of stage 0 reads one row before it
 };
 
-template <int MODE>
+// C8: the network's 8-channel input layer (e0c1).  A pair row is then 16
+// channels (32 B, 32 B swizzle), one K16 step per ky covers both elements, and
+// the three B tiles per ky ([W(1)|W(2)] ; [W(0)|W(1)] for N=64, [0|W(0)] and
+// [W(2)|0] for the N=32 neighbour MMAs) mix 8-channel halves of two taps, so
+// the epilogue warps assemble them in shared memory (manual 32 B swizzle)
+// instead of TMA.
+template <int MODE, bool C8>
 __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
@@ -864,6 +901,24 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         if (MODE == kHead)
             for (int i = t; i < p.head_c * p.cout; i += kEpiThreads)
                 sconst[2 * p.n_total + i] = p.head_w[i];
+        if (C8) {
+            // per ky 4 KB: [0, 2 KB) the N=64 tile, [2, 3) [0|W0], [3, 4) [W2|0];
+            // one thread per (ky, row, 16 B half); W is [tap][32][16] bf16
+            const uint16_t *wg = reinterpret_cast<const uint16_t *>(p.wts);
+            for (int i = t; i < 3 * 128 * 2; i += kEpiThreads) {
+                const int ky = i / 256, r = (i >> 1) & 127, hf = i & 1;
+                int kx = -1, co = r & 31;
+                if (r < 32) kx = hf ? 2 : 1;          // out(2j)   <- [x(2j) | x(2j+1)]
+                else if (r < 64) kx = hf ? 1 : 0;     // out(2j+1) <- [x(2j) | x(2j+1)]
+                else if (r < 96) kx = hf ? 0 : -1;    // out(2j)   <- x(2j-1) (element 1)
+                else kx = hf ? -1 : 2;                // out(2j+1) <- x(2j+2) (element 0)
+                uint4 v = make_uint4(0u, 0u, 0u, 0u);
+                if (kx >= 0) v = *reinterpret_cast<const uint4 *>(wg + ((kx * 3 + ky) * 32 + co) * 16);
+                const uint32_t a = (uint32_t)(r * 32 + hf * 16);
+                *reinterpret_cast<uint4 *>(smem + p.off_b + ky * 4096 + (a ^ (((a >> 7) & 1u) << 4))) = v;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
     }
     fence_before_sync();
     __syncthreads();
@@ -874,12 +929,14 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
     auto btile = [&](int src, int ky, int e, int t) -> uint32_t {
         return p.off_b + (uint32_t)((((src * 3 + ky) * 2 + e) * 2 + t)) * C::kBTile;
     };
+    constexpr uint32_t kARow = C8 ? 32u : C::kRow;
 
     if (warp == 0) {
         if (elect_one()) {
             // ------------------------------ TMA producer ------------------------------
-            mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
-            for (int src = 0; src < nsrc; ++src)
+            if (C8) mbar_arrive(bres);  // B tiles were built before the block barrier
+            else mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
+            for (int src = 0; src < (C8 ? 0 : nsrc); ++src)
                 for (int ky = 0; ky < 3; ++ky)
                     for (int e = 0; e < 2; ++e)
                         for (int t = 0; t < 2; ++t)
@@ -906,7 +963,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         if (elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
             const uint32_t id64 = idesc_bf16(128, 64), id32 = idesc_bf16(128, 32);
-            const uint64_t aproto = smem_desc(0, C::kRow, kSwizzle128B);
+            const uint64_t aproto = smem_desc(0, kARow, C8 ? kSwizzle32B : kSwizzle128B);
             const uint64_t bproto = smem_desc(0, 32, kSwizzle32B);
             const uint32_t ahi = (uint32_t)(aproto >> 32), alo = (uint32_t)aproto;
             const uint32_t bhi = (uint32_t)(bproto >> 32), blo = (uint32_t)bproto;
@@ -924,6 +981,19 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                     const uint32_t a_lo =
                         alo + ((sbase + C::kRingPad + (uint32_t)s * p.stage_bytes) >> 4);
                     const uint32_t b_lo = blo + ((sbase + btile(q, 0, 0, 0)) >> 4);
+                    if constexpr (C8) {
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) {
+                            const uint32_t ar = (uint32_t)(ky * kTW) * kARow / 16;
+                            const uint32_t bt = (uint32_t)ky * 4096 / 16;
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + ar),
+                                     ((uint64_t)bhi << 32) | (b_lo + bt), id64, ky ? 1u : 0u);
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + ar - kARow / 16),
+                                     ((uint64_t)bhi << 32) | (b_lo + bt + 2048 / 16), id32, 1u);
+                            mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + ar + kARow / 16),
+                                     ((uint64_t)bhi << 32) | (b_lo + bt + 3072 / 16), id32, 1u);
+                        }
+                    } else {
 #pragma unroll
                     for (int ky = 0; ky < 3; ++ky) {
 #pragma unroll
@@ -945,6 +1015,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                             mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e0 + C::kRow / 16),
                                      ((uint64_t)bhi << 32) | (b_lo + b_e1), id32, 1u);
                         }
+                    }
                     }
                     mma_commit(empty + s);
                 }
@@ -1210,11 +1281,11 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
     return pl->p.cout == 32 ? launch_kx_c<CHUNK, 32>(pl, st) : launch_kx_c<CHUNK, 64>(pl, st);
 }
 
-template <int MODE>
+template <int MODE, bool C8>
 static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE>,
+        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE, C8>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
@@ -1230,25 +1301,27 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE>, pl->a0, pl->a1, pl->b, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8>, pl->a0, pl->a1, pl->b, pl->p);
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
+    if (pl->chunk == 16) return launch_px2_m<kPlain, true>(pl, st);  // e0c1: plain only
     switch (pl->mode) {
-        case kPlain: return launch_px2_m<kPlain>(pl, st);
-        case kPool: return launch_px2_m<kPool>(pl, st);
-        default: return launch_px2_m<kHead>(pl, st);
+        case kPlain: return launch_px2_m<kPlain, false>(pl, st);
+        case kPool: return launch_px2_m<kPool, false>(pl, st);
+        default: return launch_px2_m<kHead, false>(pl, st);
     }
 }
 
-// LS_CONV_PX2=0 keeps the 32-channel full-resolution layers on k_conv_kx (A/B).
-static bool px2_enabled() {
+// LS_CONV_PX2 (A/B switch, bit mask, default 3): bit 0 = 32-channel
+// single-source layers on k_conv_px2, bit 1 = the 8-channel input layer.
+static int px2_mask() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("LS_CONV_PX2");
-        v = (e && e[0] == '0') ? 0 : 1;
+        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
     }
-    return v == 1;
+    return v;
 }
 
 // LS_CONV_KX=0 keeps cout = 32 layers on the generic kernel (A/B measurements).
@@ -1280,7 +1353,7 @@ static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0
 
 // Plan of a 32 -> 32 (or [32, 32] -> 32) 3x3 layer on k_conv_px2 (null when
 // it does not apply: odd width).
-static ls_conv_plan *plan_px2(const uint16_t *d_x0, const uint16_t *d_x1, int c1, int batch,
+static ls_conv_plan *plan_px2(const uint16_t *d_x0, int c0, const uint16_t *d_x1, int c1, int batch,
                               int h, int w, const uint16_t *d_w, const float *d_scale,
                               const float *d_shift, int act, float alpha, uint16_t *d_y,
                               float *d_y_f32, uint16_t *d_pool, const float *d_head_w,
@@ -1294,9 +1367,11 @@ static ls_conv_plan *plan_px2(const uint16_t *d_x0, const uint16_t *d_x1, int c1
     p.batch = batch;
     p.h = h;
     p.w = w;
-    p.c0 = 32;
+    const bool c8 = c0 == 8;
+    p.c0 = c8 ? 16 : 32;
     p.c1 = c1;
-    p.ctot = 32 + c1;
+    p.ctot = p.c0 + c1;
+    p.wts = d_w;
     p.kxs = 3;
     p.kxps = 1;
     p.pad = 1;
@@ -1320,11 +1395,12 @@ static ls_conv_plan *plan_px2(const uint16_t *d_x0, const uint16_t *d_x1, int c1
     p.n_items = p.n_tiles_m;
     p.nq0 = 1;
     p.nq = c1 > 0 ? 2 : 1;
-    p.a_tx = (uint32_t)(kTW * (kTH + 2)) * CfgPx::kRow;
+    const uint32_t arow = c8 ? 32u : CfgPx::kRow;
+    p.a_tx = (uint32_t)(kTW * (kTH + 2)) * arow;
     p.a_bytes = (p.a_tx + 1023u) & ~1023u;
     p.b_blk = CfgPx::kBTile;
     p.resident = 1;
-    const size_t res_bytes = (size_t)p.nq * 12 * CfgPx::kBTile;
+    const size_t res_bytes = c8 ? (size_t)3 * 4096 : (size_t)p.nq * 12 * CfgPx::kBTile;
     const size_t const_bytes =
         ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
     const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
@@ -1342,15 +1418,16 @@ static ls_conv_plan *plan_px2(const uint16_t *d_x0, const uint16_t *d_x1, int c1
     p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = 32;
-    pl->chunk = 64;
+    pl->chunk = c8 ? 16 : 64;
     pl->kind = 2;
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
-    // the NHWC tensors read as (W/2) pair pixels of 64 channels
-    bool ok = encode_act(&pl->a0, d_x0, 64, w / 2, h, batch, 64, kTH + 2);
-    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, 64, w / 2, h, batch, 64, kTH + 2);
+    // the NHWC tensors read as (W/2) pair pixels of 2*c channels
+    const int pc = c8 ? 16 : 64;
+    bool ok = encode_act(&pl->a0, d_x0, pc, w / 2, h, batch, pc, kTH + 2);
+    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, pc, w / 2, h, batch, pc, kTH + 2);
     ok = ok && encode_wts(&pl->b, d_w, p.ctot, 32, 9, 16, 32, 1);
     if (!ok) {
         delete pl;
@@ -1483,8 +1560,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     // reads of k_conv_kx: it wins on single-source layers whose epilogue bounds
     // them (e0c2 91 -> 67 us, d0c2 + head 96 -> 81 us) and loses on the two-source
     // d0c1 (K = 64: 99 -> 119 us, operand-bound), which stays on k_conv_kx
-    if (!transposed && cout == 32 && c0 == 32 && c1 == 0 && px2_enabled()) {
-        ls_conv_plan *pp = plan_px2(d_x0, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
+    const bool px2_fit = cout == 32 && c1 == 0 &&
+                         ((c0_tensor == 32 && (px2_mask() & 1)) ||
+                          (c0_tensor == 8 && !d_pool && !d_head_w && (px2_mask() & 2)));
+    if (!transposed && px2_fit) {
+        ls_conv_plan *pp = plan_px2(d_x0, c0_tensor, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
                                     alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
                                     d_head_out);
         if (pp) {

@@ -123,14 +123,16 @@ def test_unet_vs_f64_oracle(name, h, w):
     assert err <= 2 * max(floor, 1e-3)
 
 
-def test_eight_channel_input_identical():
-    """The engine's 8-channel input (TMA zero-fills channels 8..15 of the first
-    layer's K chunk) gives bit-identical outputs to the 16-channel layout."""
+def test_eight_channel_input_matches_sixteen():
+    """The engine's 8-channel input (first layer on pixel pairs, k_conv_px2 C8)
+    and the 16-channel layout (k_conv_kx, TMA zero-fills channels 8..15) are two
+    kernels for the same layer: outputs agree within the U-Net tolerance."""
     from paper_2502_11618_b200.unet import UNet
 
     net = UNet.from_config("default", seed=5)
     x = _input(np.random.default_rng(3), 64, 96)
-    assert np.array_equal(_run_device(net, x, 8), _run_device(net, x, 16))
+    a, b = _run_device(net, x, 8), _run_device(net, x, 16)
+    assert np.abs(a - b).max() <= 5e-3
 
 
 def test_divisibility_rejected():
