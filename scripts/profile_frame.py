@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch
 
-from paper_2502_11618_b200 import PointCloud, build_grid
+from paper_2502_11618_b200 import PointCloud, build_grid, cull_cells, extract_frustum
 from paper_2502_11618_b200.engine import FrameRenderer
 from paper_2502_11618_b200.scenes import hall_cameras, multi_station_hall
 
@@ -27,9 +27,13 @@ if a.unet != "none":
 
     unet = UNet.from_config(a.unet, seed=7, device=torch.device("cuda"))
 cams = hall_cameras(8)
-r = FrameRenderer(grid, 1920, 1080, unet=unet)
+r = FrameRenderer(grid, 1920, 1080, unet=unet, filtered_outputs=unet is None)
 for i in range(a.frames):
     r.enqueue(cams[i % len(cams)])
 torch.cuda.synchronize()
 r.check_flags()
-print("done")
+cand = []
+for i in range(a.frames):
+    s, e = grid.cell_ranges(cull_cells(grid, extract_frustum(cams[i % len(cams)])))
+    cand.append(int((e - s).sum()))
+print("candidates per frame:", cand)
