@@ -1041,7 +1041,8 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             const uint32_t tbase = tmem + ab * C::kN + ((uint32_t)(quarter * 32) << 16);
             const int gp = px0 + tp, gy = y0 + ty;
             const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
-            float hacc[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+            f32x2 hacc2[4] = {0ull, 0ull, 0ull, 0ull};  // head sums {pixel 2j, 2j+1}
+            float vkeep[16];   // pixel 2j's activations for the pair-wise head
             uint32_t keep[8];  // pixel 2j's packed half for the horizontal pool
             // 16-column groups in the order (px0, ch 0-15), (px1, 0-15), (px0, 16-31),
             // (px1, 16-31); group g+1's tcgen05.ld is in flight while g is processed
@@ -1066,7 +1067,28 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                     }
                 }
                 if (MODE == kHead) {
-                    head_accumulate(s_hw, p.cout, p.head_c, n, v, hacc[px]);
+                    // both pixels of the pair at once: one FFMA2 per channel and
+                    // head output, weights read once (each pixel's sum keeps the
+                    // scalar loop's order)
+                    if (px == 0) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) vkeep[i] = v[i];
+                    } else {
+#pragma unroll
+                        for (int j2 = 0; j2 < 4; ++j2) {
+                            if (j2 >= p.head_c) break;
+                            const float4 *w4 = reinterpret_cast<const float4 *>(s_hw + j2 * p.cout + n);
+#pragma unroll
+                            for (int q4 = 0; q4 < 4; ++q4) {
+                                const float4 w = w4[q4];
+                                const float wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    hacc2[j2] = fma2(f2(wv[k], wv[k]),
+                                                     f2(vkeep[4 * q4 + k], v[4 * q4 + k]), hacc2[j2]);
+                            }
+                        }
+                    }
                     if (!p.y && !p.y_f32) return;
                 }
                 uint32_t pk[8];
@@ -1119,13 +1141,15 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             if (lane == 0) mbar_arrive(tempty + ab);
             process(3, rb);
             if (MODE == kHead && valid) {
+                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
 #pragma unroll
-                for (int px = 0; px < 2; ++px) {
-                    const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp + px;
-                    for (int j2 = 0; j2 < p.head_c; ++j2) {
-                        const float z = hacc[px][j2] + __ldg(p.head_b + j2);
-                        p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
-                    }
+                for (int j2 = 0; j2 < 4; ++j2) {
+                    if (j2 >= p.head_c) break;
+                    float h0, h1;
+                    unf2(hacc2[j2], h0, h1);
+                    const float b = __ldg(p.head_b + j2);
+                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-(h0 + b)));
+                    p.head_out[(pix + 1) * p.head_c + j2] = 1.0f / (1.0f + expf(-(h1 + b)));
                 }
             }
             // next item of this group: kEpiGroups buffers further on
