@@ -249,6 +249,10 @@ int64_t ls_pyramid_floats(int64_t height, int64_t width, int32_t levels_n);
  *        d_unet_in (may be NULL): bf16 NHWC, unet_h rows x W x unet_c channels
  *          [r,g,b,zNear/max(d,zNear),alpha, 0...] of the FILTERED frame,
  *          rows >= H left untouched (caller zero-fills once).
+ *   U-Net-only frames: with a filter and d_unet_in, d_rgb / d_alpha may be
+ *     NULL when no filtered output is requested either -- the assembly then
+ *     writes every pixel's U-Net input and the final filter step clears the
+ *     rejected ones (same input, no f32 rgb round trip); d_depth stays required.
  *   d_pyramid: ls_pyramid_floats(H,W,L) floats of scratch.
  *   d_flags: 1 int32; bit0 set if a pixel's accumulator may have lost exactness.
  * filter==NULL skips the filter (raw frame only). */

@@ -161,11 +161,35 @@ struct Levels {
     int L;
 };
 
+// Writes one filtered pixel's U-Net input channels [r g b d' a 0 ...].
+__device__ __forceinline__ void store_unet_px(__nv_bfloat16 *__restrict__ dst, int unet_c, float r,
+                                              float g, float b, float dd, float a, double znear) {
+    // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
+    const float dn = dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear))) : 0.0f;
+    __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
+    __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
+    __nv_bfloat162 v45 = __floats2bfloat162_rn(a, 0.0f);
+    if ((unet_c & 7) == 0) {  // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
+        uint4 *o4 = reinterpret_cast<uint4 *>(dst);
+        o4[0] = make_uint4(*reinterpret_cast<uint32_t *>(&v01), *reinterpret_cast<uint32_t *>(&v23),
+                           *reinterpret_cast<uint32_t *>(&v45), 0u);
+        for (int c = 1; c < unet_c / 8; ++c) o4[c] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+        __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(dst);
+        const __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
+        o2[0] = v01;
+        o2[1] = v23;
+        o2[2] = v45;
+        for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
+    }
+}
+
 // 32x32 pixel block per CTA, 256 threads, 2x2 pixels per thread.
 __global__ void __launch_bounds__(256) k_assemble_pyramid(
     unsigned long long *__restrict__ minz, float4 *__restrict__ acc, int64_t H,
     int64_t W, Levels lv, int pool_levels, float *__restrict__ rgb, float *__restrict__ depth,
-    uint8_t *__restrict__ alpha, int *__restrict__ flags) {
+    uint8_t *__restrict__ alpha, int *__restrict__ flags, __nv_bfloat16 *__restrict__ unet_in,
+    int unet_c, double znear) {
     pdl_wait();  // launched with PDL after pass 2; its trigger is completion
     __shared__ float s1[16][17];
     __shared__ float s2[8][9];
@@ -228,13 +252,24 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
                 m = sv < m ? sv : m;
             }
         }
+        if (unet_in) {
+            // U-Net-only frames: the input of every pixel as if kept (the
+            // final filter step clears the rejected ones) -- no f32 rgb round trip
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx)
+                if (ok[dy][dx])
+                    store_unet_px(unet_in + (p + dx) * unet_c, unet_c, c[dx][0], c[dx][1], c[dx][2],
+                                  d[dx], (float)al[dx], znear);
+        }
         if (ok[dy][1] && (W & 1) == 0) {
-            float2 *r2 = reinterpret_cast<float2 *>(rgb + 3 * p);
-            r2[0] = make_float2(c[0][0], c[0][1]);
-            r2[1] = make_float2(c[0][2], c[1][0]);
-            r2[2] = make_float2(c[1][1], c[1][2]);
+            if (rgb) {
+                float2 *r2 = reinterpret_cast<float2 *>(rgb + 3 * p);
+                r2[0] = make_float2(c[0][0], c[0][1]);
+                r2[1] = make_float2(c[0][2], c[1][0]);
+                r2[2] = make_float2(c[1][1], c[1][2]);
+            }
             *reinterpret_cast<float2 *>(depth + p) = make_float2(d[0], d[1]);
-            *reinterpret_cast<uchar2 *>(alpha + p) = make_uchar2(al[0], al[1]);
+            if (alpha) *reinterpret_cast<uchar2 *>(alpha + p) = make_uchar2(al[0], al[1]);
             // consume-and-reset for the next frame
             *reinterpret_cast<ulonglong2 *>(minz + p) = make_ulonglong2(kInfBits, kInfBits);
             acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -244,11 +279,13 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
             for (int dx = 0; dx < 2; ++dx) {
                 if (!ok[dy][dx]) continue;
                 const int64_t q = p + dx;
-                rgb[3 * q] = c[dx][0];
-                rgb[3 * q + 1] = c[dx][1];
-                rgb[3 * q + 2] = c[dx][2];
+                if (rgb) {
+                    rgb[3 * q] = c[dx][0];
+                    rgb[3 * q + 1] = c[dx][1];
+                    rgb[3 * q + 2] = c[dx][2];
+                }
                 depth[q] = d[dx];
-                alpha[q] = al[dx];
+                if (alpha) alpha[q] = al[dx];
                 minz[q] = kInfBits;
                 acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
@@ -300,29 +337,6 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     }
 }
 
-// Writes one filtered pixel's U-Net input channels [r g b d' a 0 ...].
-__device__ __forceinline__ void store_unet_px(__nv_bfloat16 *__restrict__ dst, int unet_c, float r,
-                                              float g, float b, float dd, float a, double znear) {
-    // weights.ts:90-95: d' = zNear/max(d, zNear) (f64 -> f32), 0 if empty
-    const float dn = dd > 0.0f ? __double2float_rn(ddiv(znear, fmax((double)dd, znear))) : 0.0f;
-    __nv_bfloat162 v01 = __floats2bfloat162_rn(r, g);
-    __nv_bfloat162 v23 = __floats2bfloat162_rn(b, dn);
-    __nv_bfloat162 v45 = __floats2bfloat162_rn(a, 0.0f);
-    if ((unet_c & 7) == 0) {  // 16 B vector stores: [r g b d' | a 0 0 0 | 0 ...]
-        uint4 *o4 = reinterpret_cast<uint4 *>(dst);
-        o4[0] = make_uint4(*reinterpret_cast<uint32_t *>(&v01), *reinterpret_cast<uint32_t *>(&v23),
-                           *reinterpret_cast<uint32_t *>(&v45), 0u);
-        for (int c = 1; c < unet_c / 8; ++c) o4[c] = make_uint4(0u, 0u, 0u, 0u);
-    } else {
-        __nv_bfloat162 *o2 = reinterpret_cast<__nv_bfloat162 *>(dst);
-        const __nv_bfloat162 z = __floats2bfloat162_rn(0.0f, 0.0f);
-        o2[0] = v01;
-        o2[1] = v23;
-        o2[2] = v45;
-        for (int c = 3; c < unet_c / 2; ++c) o2[c] = z;
-    }
-}
-
 // One thread per COARSE pixel on a 2-D grid (32 x 8 threads per CTA, no
 // index division); FINAL reads the full-resolution frame and, where the
 // thread's two children of a fine row are both inside an even-width image,
@@ -365,7 +379,11 @@ __global__ void __launch_bounds__(256) k_filter_step(
                 const float dq = fine[q];  // frame depth (0 = empty)
                 const bool kq = keep_test(sentinel(dq), ref, fs);
                 if (keep_out) keep_out[q] = (uint8_t)kq;
-                if (!rgb) continue;  // mask-only (filter_depth_image)
+                if (!rgb) {  // mask-only, or U-Net-only: clear a rejected non-empty pixel
+                    if (unet_in && !kq && dq > 0.0f)
+                        store_unet_px(unet_in + q * unet_c, unet_c, 0.f, 0.f, 0.f, 0.f, 0.f, znear);
+                    continue;
+                }
                 const float m = kq ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
                 const float r = rgb[3 * q] * m, g = rgb[3 * q + 1] * m, b = rgb[3 * q + 2] * m,
                             dd = dq * m;
@@ -391,7 +409,16 @@ __global__ void __launch_bounds__(256) k_filter_step(
             mk[dx] = k[dx] ? 1.0f : 0.0f;
         }
         if (keep_out) *reinterpret_cast<uchar2 *>(keep_out + p) = make_uchar2(k[0], k[1]);
-        if (!rgb) continue;
+        if (!rgb) {
+            if (unet_in) {
+#pragma unroll
+                for (int dx = 0; dx < 2; ++dx)
+                    if (!k[dx] && d[dx] > 0.0f)
+                        store_unet_px(unet_in + (p + dx) * unet_c, unet_c, 0.f, 0.f, 0.f, 0.f, 0.f,
+                                      znear);
+            }
+            continue;
+        }
         const float2 *r2 = reinterpret_cast<const float2 *>(rgb + 3 * p);
         const float2 a0 = r2[0], a1 = r2[1], a2 = r2[2];
         const float c[2][3] = {{a0.x, a0.y, a1.x}, {a1.y, a2.x, a2.y}};
@@ -569,7 +596,13 @@ int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64
                     uint8_t *d_alpha, float *d_frgb, float *d_fdepth, uint8_t *d_falpha,
                     uint8_t *d_keep, uint16_t *d_unet_in, int64_t unet_h, int32_t unet_c,
                     double unet_znear, float *d_pyramid, int32_t *d_flags, void *stream) {
-    if (width <= 0 || height <= 0 || !d_rgb || !d_depth || !d_alpha || !d_flags) return LS_EINVAL;
+    // U-Net-only frames (a filter, a U-Net input, no raw rgb/alpha and no
+    // filtered outputs): the assembly writes the U-Net input of every pixel and
+    // the final filter step only clears the rejected ones
+    const bool unet_only = filter && d_unet_in && !d_rgb && !d_alpha && !d_frgb && !d_fdepth &&
+                           !d_falpha;
+    if (width <= 0 || height <= 0 || !d_depth || !d_flags) return LS_EINVAL;
+    if (!unet_only && (!d_rgb || !d_alpha)) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     Levels lv{};
     float *up_base = nullptr;
@@ -587,7 +620,9 @@ int ls_frame_finish(uint64_t *d_minz_bits, float *d_accum4, int64_t width, int64
     cudaError_t e = launch_pdl(k_assemble_pyramid, grid, dim3(256), 0, st,
                                (unsigned long long *)d_minz_bits,
                                reinterpret_cast<float4 *>(d_accum4), height, width, lv, in_block,
-                               d_rgb, d_depth, d_alpha, d_flags);
+                               d_rgb, d_depth, d_alpha, d_flags,
+                               unet_only ? reinterpret_cast<__nv_bfloat16 *>(d_unet_in) : nullptr,
+                               (int)unet_c, unet_znear);
     if (e != cudaSuccess) return (int)e;
     if (!filter) return 0;
     for (int k = 6; k <= L; ++k) {  // levels beyond the in-block five

@@ -101,7 +101,8 @@ class FrameRenderer:
         project_scene(self.scene, camera, self.rp.zbuffer_epsilon_rel, self.bufs, cull=True,
                       filter_params=self.fp, filtered=filtered,
                       unet_in=None if self.unet is None else self.unet_in[0],
-                      pyramid=self.pyramid, stage_events=events)
+                      pyramid=self.pyramid, stage_events=events,
+                      raw=self.unet is None or self.filtered_outputs)
         if self.unet is not None:
             self.unet.forward(self.unet_in, outs[0])
         if events is not None:
@@ -255,7 +256,8 @@ class ViewBatchRenderer:
         filtered = None if self.unet is not None else (self.frgb, self.fdepth, self.falpha)
         project_scene_views(self.scene, cameras, self.rp.zbuffer_epsilon_rel, self.vbufs,
                             cull=True, filter_params=self.fp, filtered=filtered,
-                            unet_in=self.unet_in, pyramid=self.pyramid)
+                            unet_in=self.unet_in, pyramid=self.pyramid,
+                            raw=self.unet is None)
         if self.unet is not None:
             self.unet.forward(self.unet_in, self.rgb_out)
 

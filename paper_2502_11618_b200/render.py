@@ -138,11 +138,14 @@ def frame_cache(scene, camera: CameraModel):
 def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs: FrameBuffers,
                   cull: bool = True, filter_params=None, filtered=None, keep=None,
                   unet_in=None, unet_znear: float = 0.1, pyramid=None,
-                  stage_events=None) -> None:
+                  stage_events=None, raw: bool = True) -> None:
     """Enqueue one fused frame on the current stream (no host sync):
     cull -> pass 1 -> pass 2 -> assemble (+ filter / U-Net input).
     ``stage_events``: optional CUDA events recorded after cull, pass 1,
-    pass 2 and assemble/filter."""
+    pass 2 and assemble/filter.  ``raw=False`` (U-Net-only frames: a filter,
+    ``unet_in`` and no filtered outputs) skips the raw f32 rgb / alpha frame:
+    the assembly writes the U-Net input directly (bufs.rgb / bufs.alpha are
+    then not updated)."""
     lib = _lib.load()
     st = _lib.stream_ptr()
     cam = _lib.make_camera(camera)
@@ -171,9 +174,10 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
                                 _lib.ptr(filtered[2]))
     unet_h, unet_c = (0, 0) if unet_in is None else (int(unet_in.shape[-3]),
                                                       int(unet_in.shape[-1]))
+    raw_rgb, raw_alpha = (bufs.rgb.data_ptr(), bufs.alpha.data_ptr()) if raw else (None, None)
     _lib.check(lib.ls_frame_finish(bufs.minz.data_ptr(), bufs.accum.data_ptr(), bufs.width,
-                                   bufs.height, fp, bufs.rgb.data_ptr(), bufs.depth.data_ptr(),
-                                   bufs.alpha.data_ptr(), frgb, fdepth, falpha, _lib.ptr(keep),
+                                   bufs.height, fp, raw_rgb, bufs.depth.data_ptr(),
+                                   raw_alpha, frgb, fdepth, falpha, _lib.ptr(keep),
                                    _lib.ptr(unet_in), unet_h, unet_c, float(unet_znear),
                                    _lib.ptr(pyramid), bufs.flags.data_ptr(), st), "frame_finish")
     if ev[3] is not None:
@@ -218,7 +222,8 @@ def views_cache(scene, camera: CameraModel, n_views: int):
 
 def project_scene_views(scene: DeviceScene, cameras, eps_rel: float, vb: ViewBuffers,
                         cull: bool = True, filter_params=None, filtered=None, keep=None,
-                        unet_in=None, unet_znear: float = 0.1, pyramid=None) -> None:
+                        unet_in=None, unet_znear: float = 0.1, pyramid=None,
+                        raw: bool = True) -> None:
     """Enqueue a batch of views on the current stream (no host sync): per-view
     culls, ONE multi-view pass pair over the scan (each tile read once for all
     views), then one assemble/filter per view.  ``filtered`` / ``keep`` /
@@ -253,8 +258,9 @@ def project_scene_views(scene: DeviceScene, cameras, eps_rel: float, vb: ViewBuf
         uin = None if unet_in is None else unet_in[v]
         unet_h, unet_c = (0, 0) if uin is None else (int(uin.shape[-3]), int(uin.shape[-1]))
         _lib.check(lib.ls_frame_finish(vb.minz[v].data_ptr(), vb.accum[v].data_ptr(), vb.width,
-                                       vb.height, fp, vb.rgb[v].data_ptr(),
-                                       vb.depth[v].data_ptr(), vb.alpha[v].data_ptr(),
+                                       vb.height, fp, vb.rgb[v].data_ptr() if raw else None,
+                                       vb.depth[v].data_ptr(),
+                                       vb.alpha[v].data_ptr() if raw else None,
                                        _lib.ptr(frgb), _lib.ptr(fdepth), _lib.ptr(falpha),
                                        _lib.ptr(None if keep is None else keep[v]),
                                        _lib.ptr(uin), unet_h, unet_c, float(unet_znear),

@@ -82,3 +82,6 @@ def test_unfiltered_outputs_same_reconstruction():
     b = FrameRenderer(grid, 256, 192, unet=unet, filtered_outputs=False)
     for v in views:
         assert np.array_equal(a.render(v), b.render(v))
+        # b's assembly writes the U-Net input directly (no raw f32 rgb) and its
+        # final filter step clears the rejected pixels: the same input tensor
+        assert bool((a.unet_in == b.unet_in).all())
