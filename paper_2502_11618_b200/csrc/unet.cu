@@ -86,12 +86,20 @@ struct ConvParamsP {
     uint32_t off_bar;       // barriers
 };
 
-template <int BN, int CHUNK>
+// 128-pixel sub-tiles per work item: more sub-tiles share each streamed
+// weight stage (a 256-column layer reads 48 KB of weights per 10 KB of
+// activations), fewer items fill the 148 SMs -- the plan picks 2 for
+// 256-column tiles when that still leaves >= ~0.8 items per SM
+constexpr int default_mt(int bn) {
+    return bn <= 32 ? 4 : (bn <= 64 ? 2 : (bn <= 128 ? LS_MT128 : LS_MT256));
+}
+
+template <int BN, int CHUNK, int MT = default_mt(BN)>
 struct CfgP {
     static constexpr uint32_t kRow = CHUNK * 2;  // bytes per operand row
     static constexpr uint32_t kLayout =
         CHUNK == 64 ? kSwizzle128B : (CHUNK == 32 ? kSwizzle64B : kSwizzle32B);
-    static constexpr int kMT = BN <= 32 ? 4 : (BN <= 64 ? 2 : (BN <= 128 ? LS_MT128 : LS_MT256));
+    static constexpr int kMT = MT;
     static constexpr int kItemCols = kMT * BN;                          // TMEM columns per item
     static constexpr int kAcc = 512 / kItemCols >= 4 ? 4 : 512 / kItemCols;
     static constexpr int kEpiGroups = kAcc >= 4 ? 3 : (kAcc >= 3 ? 2 : 1);
@@ -103,8 +111,8 @@ struct CfgP {
     static constexpr int kGroups = BN / 16;
 };
 
-template <int BN, int CHUNK>
-constexpr int threads_for() { return CfgP<BN, CHUNK>::kThreads; }
+template <int BN, int CHUNK, int MT>
+constexpr int threads_for() { return CfgP<BN, CHUNK, MT>::kThreads; }
 
 // Branch-free activation: max(v, slope * v) with slope 0 (ReLU), alpha (leaky,
 // 0 <= alpha <= 1) or 1 (none) -- the layer's slope is resolved once.
@@ -218,11 +226,11 @@ __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, floa
     return ip;
 }
 
-template <int BN, int CHUNK, int MODE>
-__global__ void __launch_bounds__(threads_for<BN, CHUNK>()) k_conv_p(
+template <int BN, int CHUNK, int MODE, int MT_ = default_mt(BN)>
+__global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
-    using C = CfgP<BN, CHUNK>;
+    using C = CfgP<BN, CHUNK, MT_>;
     constexpr int KYS = MODE == kTransposed ? 1 : 3;
     constexpr int MT = C::kMT;
     constexpr int kTileH = kTH * MT;
@@ -1227,6 +1235,7 @@ struct ls_conv_plan {
     CUtensorMap a0, a1, b;
     ConvParamsP p;
     int bn, chunk, grid, mode;
+    int mt;    // k_conv_p: 128-pixel sub-tiles per work item
     int kind;  // 0: k_conv_p, 1: k_conv_kx (kx taps stacked along N), 2: k_conv_px2 (pixel pairs)
     size_t smem;
 };
@@ -1244,11 +1253,11 @@ static bool pdl_enabled() {
     return v == 1;
 }
 
-template <int BN, int CHUNK, int MODE>
+template <int BN, int CHUNK, int MODE, int MT>
 static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;  // idempotent: racing threads set the same value
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK, MODE>,
+        cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK, MODE, MT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
@@ -1256,7 +1265,7 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)CfgP<BN, CHUNK>::kThreads);
+    cfg.blockDim = dim3((unsigned)CfgP<BN, CHUNK, MT>::kThreads);
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1264,7 +1273,8 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE>, pl->a0, pl->a1, pl->b, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE, MT>, pl->a0, pl->a1, pl->b,
+                                   pl->p);
 }
 
 template <int CHUNK, int COUT, int MODE>
@@ -1358,17 +1368,36 @@ static bool kx_enabled() {
     return v == 1;
 }
 
-template <int BN, int CHUNK>
+template <int BN, int CHUNK, int MT = default_mt(BN)>
 static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
     switch (pl->mode) {
-        case kPlain: return launch_m<BN, CHUNK, kPlain>(pl, st);
-        case kPool: return launch_m<BN, CHUNK, kPool>(pl, st);
-        case kHead: return launch_m<BN, CHUNK, kHead>(pl, st);
-        default: return launch_m<BN, CHUNK, kTransposed>(pl, st);
+        case kPlain: return launch_m<BN, CHUNK, kPlain, MT>(pl, st);
+        case kPool: return launch_m<BN, CHUNK, kPool, MT>(pl, st);
+        case kHead: return launch_m<BN, CHUNK, kHead, MT>(pl, st);
+        default: return launch_m<BN, CHUNK, kTransposed, MT>(pl, st);
     }
 }
 
-static int mt_for(int bn) { return bn <= 32 ? 4 : (bn <= 64 ? 2 : (bn <= 128 ? LS_MT128 : LS_MT256)); }
+// LS_CONV_MT2=0 keeps 256-column tiles at one sub-tile per item (A/B).
+static bool mt2_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_CONV_MT2");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transposed) {
+    const int mt = default_mt(bn);
+    if (bn == 256 && mt == 1 && !transposed && mt2_enabled()) {
+        const int items2 = ((w + kTW - 1) / kTW) * ((h + 2 * kTH - 1) / (2 * kTH)) * batch * n_tiles_n;
+        int n_sm = 148;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        if (items2 * 5 >= n_sm * 4) return 2;
+    }
+    return mt;
+}
 
 }  // namespace unet
 }  // namespace ls
@@ -1649,8 +1678,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     // Fit >= 3 pipeline stages: first try whole-chunk stages (all kx boxes in
     // one stage), then one kx per stage, then a narrower K chunk, then a
     // narrower column tile.
+    int mt = 1;
     for (;;) {
-        const int mt = mt_for(bn);
+        mt = mt_for(bn, h, w, batch, (n_total + bn - 1) / bn, transposed != 0);
         const int box_h = kTH * mt + 2 * p.pad;
         const uint32_t row = (uint32_t)chunk * 2;
         p.tiles_x = (w + kTW - 1) / kTW;
@@ -1700,7 +1730,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
-    const int box_h = kTH * mt_for(bn) + 2 * p.pad;
+    const int box_h = kTH * mt + 2 * p.pad;
+    pl->mt = mt;
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, box_h);
     ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
                           chunk, box_h);
@@ -1723,12 +1754,14 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
         return launch_kx<64>(pl, st);
     }
 #define LS_CASE(B, K) \
-    if (pl->bn == B && pl->chunk == K) return launch_p<B, K>(pl, st);
+    if (pl->bn == B && pl->chunk == K && pl->mt == default_mt(B)) return launch_p<B, K>(pl, st);
     LS_CASE(32, 16) LS_CASE(32, 32) LS_CASE(32, 64)
     LS_CASE(64, 16) LS_CASE(64, 32) LS_CASE(64, 64)
     LS_CASE(128, 16) LS_CASE(128, 32) LS_CASE(128, 64)
     LS_CASE(256, 16) LS_CASE(256, 32)
 #undef LS_CASE
+    if (pl->bn == 256 && pl->chunk == 32 && pl->mt == 2) return launch_p<256, 32, 2>(pl, st);
+    if (pl->bn == 256 && pl->chunk == 16 && pl->mt == 2) return launch_p<256, 16, 2>(pl, st);
     return LS_EINVAL;
 }
 
