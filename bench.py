@@ -318,6 +318,14 @@ def run_b200(args):
         proj_bytes = 27.0 * np.array(cand)  # 12 B pass 1 + 15 B pass 2 per candidate
         proj_gbs = float(np.mean(proj_bytes / (t_proj * 1e-3)) / 1e9)
     stages_ms = {k: float(np.mean(v)) for k, v in stage.items()} if not sharded else None
+    # per-frame device time, mean / p50 / p95 as the reference's run_bench
+    # reports them (R:bench.py:61-67), from the instrumented pass
+    frame_ms = None
+    if not sharded and args.steps > 0:
+        ft = np.array([e[0].elapsed_time(e[5]) for e in evs])
+        frame_ms = {"mean": float(ft.mean()), "p50": float(np.percentile(ft, 50)),
+                    "p95": float(np.percentile(ft, 95)),
+                    "source": "instrumented pass, CUDA events around each frame"}
     roofline = None if sharded else {
                 "kernel": "projection (k_frame_pass1 + k_frame_pass2)", "bound": "hbm",
                 "achieved": proj_gbs, "peak": hbm, "unit": "GB/s", "frac": proj_gbs / hbm,
@@ -386,6 +394,7 @@ def run_b200(args):
         "gpoints_per_s": mean_cand * fps / 1e9,
         "candidates_mean": mean_cand,
         "stages_ms": stages_ms,
+        "frame_ms": frame_ms,
         "stages_note": "per-stage CUDA events from a second, instrumented pass over the same "
                        "frames; value / ms_per_step come from the uninstrumented timed pass",
         "roofline": roofline,

@@ -212,6 +212,21 @@ __device__ __forceinline__ void tmem_ld_wait16(uint32_t (&a)[16]) {
                  : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld_wait4(uint32_t (&a)[16], uint32_t (&b)[16],
+                                              uint32_t (&c)[16], uint32_t (&d)[16]) {
+    tmem_ld_wait16(a);  // one wait::ld covers every outstanding load; the empty
+    // asm statements keep the other registers' uses below it
+    asm volatile("" : "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]),
+                 "+r"(b[6]), "+r"(b[7]), "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]),
+                 "+r"(b[12]), "+r"(b[13]), "+r"(b[14]), "+r"(b[15])::"memory");
+    asm volatile("" : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3]), "+r"(c[4]), "+r"(c[5]),
+                 "+r"(c[6]), "+r"(c[7]), "+r"(c[8]), "+r"(c[9]), "+r"(c[10]), "+r"(c[11]),
+                 "+r"(c[12]), "+r"(c[13]), "+r"(c[14]), "+r"(c[15])::"memory");
+    asm volatile("" : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]),
+                 "+r"(d[6]), "+r"(d[7]), "+r"(d[8]), "+r"(d[9]), "+r"(d[10]), "+r"(d[11]),
+                 "+r"(d[12]), "+r"(d[13]), "+r"(d[14]), "+r"(d[15])::"memory");
+}
+
 __device__ __forceinline__ void tmem_ld_wait3(uint32_t (&a)[16], uint32_t (&b)[16],
                                               uint32_t (&c)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;"

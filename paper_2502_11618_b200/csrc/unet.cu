@@ -848,11 +848,22 @@ struct CfgPx {
 // [W(2)|0] for the N=32 neighbour MMAs) mix 8-channel halves of two taps, so
 // the epilogue warps assemble them in shared memory (manual 32 B swizzle)
 // instead of TMA.
-template <int MODE, bool C8>
+// KX2: pixel pairs WITHOUT neighbour-row MMAs.  Per K16 step two N=96 MMAs
+// against ONE B tile [W(2) ; W(1) ; W(0)] (96 rows) write TMEM columns
+//   [ spill-left | out(2j) | out(2j+1) | spill-right ]  (4 x 32)
+// element 0 (x(2j)) at columns 0..95, element 1 (x(2j+1)) at 32..127, and the
+// epilogue adds the neighbours' spills: out(2j) += spill-right of lane j-1,
+// out(2j+1) += spill-left of lane j+1.  Same MMA count and operand bytes per
+// pixel as k_conv_kx with half its shuffles and 2/3 of its TMEM reads, and no
+// row-shifted operands -- for the two-source d0c1, where the neighbour-row
+// MMAs' extra operand reads lose.
+template <int MODE, bool C8, bool KX2 = false>
 __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
     using C = CfgPx;
+    constexpr int kN = KX2 ? 128 : C::kN;       // TMEM columns per item
+    constexpr int kAcc = KX2 ? 4 : C::kAcc;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -864,8 +875,8 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
-    uint64_t *tempty = tfull + C::kAcc;
-    uint64_t *bres = tempty + C::kAcc;
+    uint64_t *tempty = tfull + kAcc;
+    uint64_t *bres = tempty + kAcc;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
     const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
     const float r_tx = 1.0f / (float)p.tiles_x;
@@ -887,7 +898,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                 mbar_init(full + s, 1);
                 mbar_init(empty + s, 1);
             }
-            for (int a = 0; a < C::kAcc; ++a) {
+            for (int a = 0; a < kAcc; ++a) {
                 mbar_init(tfull + a, 1);
                 mbar_init(tempty + a, 4);
             }
@@ -942,9 +953,22 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
     if (warp == 0) {
         if (elect_one()) {
             // ------------------------------ TMA producer ------------------------------
-            if (C8) mbar_arrive(bres);  // B tiles were built before the block barrier
-            else mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
-            for (int src = 0; src < (C8 ? 0 : nsrc); ++src)
+            if (C8) {
+                mbar_arrive(bres);  // B tiles were built before the block barrier
+            } else if (KX2) {
+                // tile (src, ky, t): rows [W(2) ; W(1) ; W(0)], 3 KB
+                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2) * 3072u);
+                for (int src = 0; src < nsrc; ++src)
+                    for (int ky = 0; ky < 3; ++ky)
+                        for (int t = 0; t < 2; ++t)
+                            for (int r = 0; r < 3; ++r)
+                                tma_load_3d(smem + p.off_b + ((src * 3 + ky) * 2 + t) * 3072 +
+                                                r * 1024,
+                                            &mB, src * 32 + 16 * t, 0, (2 - r) * 3 + ky, bres);
+            } else {
+                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
+            }
+            for (int src = 0; src < ((C8 || KX2) ? 0 : nsrc); ++src)
                 for (int ky = 0; ky < 3; ++ky)
                     for (int e = 0; e < 2; ++e)
                         for (int t = 0; t < 2; ++t)
@@ -971,6 +995,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         if (elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
             const uint32_t id64 = idesc_bf16(128, 64), id32 = idesc_bf16(128, 32);
+            const uint32_t id96 = idesc_bf16(128, 96);
             const uint64_t aproto = smem_desc(0, kARow, C8 ? kSwizzle32B : kSwizzle128B);
             const uint64_t bproto = smem_desc(0, 32, kSwizzle32B);
             const uint32_t ahi = (uint32_t)(aproto >> 32), alo = (uint32_t)aproto;
@@ -979,17 +1004,45 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             int s = 0;
             uint32_t ph = 0, ab = 0, aph = 0;
             for (int item = blockIdx.x; item < p.n_items;
-                 item += gridDim.x, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
+                 item += gridDim.x, ab = ab + 1 == kAcc ? 0 : ab + 1, aph ^= ab == 0) {
                 mbar_wait(tempty + ab, aph ^ 1u);
                 fence_after_sync();
-                const uint32_t d0 = tmem + ab * C::kN;
+                const uint32_t d0 = tmem + ab * kN;
                 for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     mbar_wait(full + s, ph);
                     fence_after_sync();
                     const uint32_t a_lo =
                         alo + ((sbase + C::kRingPad + (uint32_t)s * p.stage_bytes) >> 4);
                     const uint32_t b_lo = blo + ((sbase + btile(q, 0, 0, 0)) >> 4);
-                    if constexpr (C8) {
+                    if constexpr (KX2) {
+                        const uint32_t bk = blo + ((sbase + p.off_b + (uint32_t)q * 6 * 3072u) >> 4);
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) {
+#pragma unroll
+                            for (int t = 0; t < 2; ++t) {
+                                const uint32_t arow = (uint32_t)(ky * kTW) * C::kRow;
+                                const uint32_t a_e0 = (arow + 32 * t) / 16;
+                                const uint32_t a_e1 = (arow + 64 + 32 * t) / 16;
+                                const uint32_t bt = (uint32_t)((ky * 2 + t) * 3072) / 16;
+                                const bool first = (q | ky | t) == 0;
+                                // element 0 -> [spill-left | out(2j) | out(2j+1)]
+                                mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e0),
+                                         ((uint64_t)bhi << 32) | (bk + bt), id96, first ? 0u : 1u);
+                                if (first) {
+                                    // element 1's first step: columns 32..95 accumulate onto
+                                    // element 0's, 96..127 (spill-right) start fresh
+                                    mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt), id64, 1u);
+                                    mma_bf16(d0 + 96, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt + 2048 / 16), id32, 0u);
+                                } else {
+                                    // element 1 -> [out(2j) | out(2j+1) | spill-right]
+                                    mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt), id96, 1u);
+                                }
+                            }
+                        }
+                    } else if constexpr (C8) {
 #pragma unroll
                         for (int ky = 0; ky < 3; ++ky) {
                             const uint32_t ar = (uint32_t)(ky * kTW) * kARow / 16;
@@ -1039,14 +1092,14 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         const float slope = act_slope(p.act, p.alpha);
         const f32x2 slope2 = f2(slope, slope);
         const int wp = p.w >> 1;
-        uint32_t ab = (uint32_t)eg % C::kAcc, aph = ((uint32_t)eg / C::kAcc) & 1u;
+        uint32_t ab = (uint32_t)eg % kAcc, aph = ((uint32_t)eg / kAcc) & 1u;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x) {
             int img, px0, y0;
             pos(item, img, px0, y0);
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
-            const uint32_t tbase = tmem + ab * C::kN + ((uint32_t)(quarter * 32) << 16);
+            const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
             const int gp = px0 + tp, gy = y0 + ty;
             const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
             f32x2 hacc2[4] = {0ull, 0ull, 0ull, 0ull};  // head sums {pixel 2j, 2j+1}
@@ -1132,6 +1185,34 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                     }
                 }
             };
+            if constexpr (KX2) {
+                // 16-channel block n: out(2j) = own + left lane's spill-right,
+                // out(2j+1) = own + right lane's spill-left
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const uint32_t n = 16u * h2;
+                    uint32_t sl[16], o0[16], o1[16], sr[16];
+                    tmem_ld16_async(tbase + n, sl);
+                    tmem_ld16_async(tbase + 32u + n, o0);
+                    tmem_ld16_async(tbase + 64u + n, o1);
+                    tmem_ld16_async(tbase + 96u + n, sr);
+                    tmem_ld_wait4(sl, o0, o1, sr);
+                    if (h2 == 1) {  // item fully read -> hand the TMEM buffer back
+                        fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(tempty + ab);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        o0[i] = __float_as_uint(__uint_as_float(o0[i]) +
+                                                __shfl_up_sync(0xffffffffu, __uint_as_float(sr[i]), 1));
+                        o1[i] = __float_as_uint(__uint_as_float(o1[i]) +
+                                                __shfl_down_sync(0xffffffffu, __uint_as_float(sl[i]), 1));
+                    }
+                    process(2 * h2, o0);
+                    process(2 * h2 + 1, o1);
+                }
+            } else {
             tmem_ld16_async(col(0), ra);
             tmem_ld_wait16(ra);
             tmem_ld16_async(col(1), rb);
@@ -1148,6 +1229,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + ab);
             process(3, rb);
+            }
             if (MODE == kHead && valid) {
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
 #pragma unroll
@@ -1163,7 +1245,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             // next item of this group: kEpiGroups buffers further on
 #pragma unroll 1
             for (int k = 0; k < C::kEpiGroups; ++k) {
-                ab = ab + 1 == C::kAcc ? 0 : ab + 1;
+                ab = ab + 1 == kAcc ? 0 : ab + 1;
                 aph ^= ab == 0;
             }
         }
@@ -1315,11 +1397,11 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
     return pl->p.cout == 32 ? launch_kx_c<CHUNK, 32>(pl, st) : launch_kx_c<CHUNK, 64>(pl, st);
 }
 
-template <int MODE, bool C8>
+template <int MODE, bool C8, bool KX2 = false>
 static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     static int attr_done = 0;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE, C8>,
+        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE, C8, KX2>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
@@ -1335,16 +1417,32 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8>, pl->a0, pl->a1, pl->b, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8, KX2>, pl->a0, pl->a1, pl->b, pl->p);
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
     if (pl->chunk == 16) return launch_px2_m<kPlain, true>(pl, st);  // e0c1: plain only
+    if (pl->mt == 3) {  // KX2 variant
+        switch (pl->mode) {
+            case kPlain: return launch_px2_m<kPlain, false, true>(pl, st);
+            case kPool: return launch_px2_m<kPool, false, true>(pl, st);
+            default: return launch_px2_m<kHead, false, true>(pl, st);
+        }
+    }
     switch (pl->mode) {
         case kPlain: return launch_px2_m<kPlain, false>(pl, st);
         case kPool: return launch_px2_m<kPool, false>(pl, st);
         default: return launch_px2_m<kHead, false>(pl, st);
     }
+}
+
+static int kx2_setting() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_CONV_KX2");
+        v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
+    }
+    return v;
 }
 
 // LS_CONV_PX2 (A/B switch, bit mask, default 3): bit 0 = 32-channel
@@ -1406,7 +1504,7 @@ static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0
 
 // Plan of a 32 -> 32 (or [32, 32] -> 32) 3x3 layer on k_conv_px2 (null when
 // it does not apply: odd width).
-static ls_conv_plan *plan_px2(const uint16_t *d_x0, int c0, const uint16_t *d_x1, int c1, int batch,
+static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint16_t *d_x1, int c1, int batch,
                               int h, int w, const uint16_t *d_w, const float *d_scale,
                               const float *d_shift, int act, float alpha, uint16_t *d_y,
                               float *d_y_f32, uint16_t *d_pool, const float *d_head_w,
@@ -1453,7 +1551,8 @@ static ls_conv_plan *plan_px2(const uint16_t *d_x0, int c0, const uint16_t *d_x1
     p.a_bytes = (p.a_tx + 1023u) & ~1023u;
     p.b_blk = CfgPx::kBTile;
     p.resident = 1;
-    const size_t res_bytes = c8 ? (size_t)3 * 4096 : (size_t)p.nq * 12 * CfgPx::kBTile;
+    const size_t res_bytes = c8 ? (size_t)3 * 4096
+                                : (kx2 ? (size_t)p.nq * 6 * 3072 : (size_t)p.nq * 12 * CfgPx::kBTile);
     const size_t const_bytes =
         ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
     const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
@@ -1473,6 +1572,7 @@ static ls_conv_plan *plan_px2(const uint16_t *d_x0, int c0, const uint16_t *d_x1
     pl->bn = 32;
     pl->chunk = c8 ? 16 : 64;
     pl->kind = 2;
+    pl->mt = kx2 && !c8 ? 3 : 1;  // 3 marks the KX2 variant
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
@@ -1609,15 +1709,19 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     // cout = 64 items hold 192 TMEM columns (2 buffers): worth it only when the
     // K loop is long enough to cover the buffer round trip (measured: K = 128
     // 94 -> 66 us, K = 32 / 64 slower)
-    // k_conv_px2 trades epilogue work (no shuffles) for ~1.6x the SMEM operand
-    // reads of k_conv_kx: it wins on single-source layers whose epilogue bounds
-    // them (e0c2 91 -> 67 us, d0c2 + head 96 -> 81 us) and loses on the two-source
-    // d0c1 (K = 64: 99 -> 119 us, operand-bound), which stays on k_conv_kx
-    const bool px2_fit = cout == 32 && c1 == 0 &&
+    // pixel-pair kernels (k_conv_px2): the KX2 variant (spill columns) for the
+    // 32-channel layers (measured U-Net 0.893 ms with neighbour-row MMAs for the
+    // single-source layers and k_conv_kx for d0c1, 0.879 with KX2 on d0c1 only,
+    // 0.873 with KX2 everywhere; LS_CONV_KX2=1: d0c1 only, 0: never), the
+    // neighbour-row form for the 8-channel input layer
+    const int kx2_mode = kx2_setting();
+    const bool kx2 = cout == 32 && c0_tensor == 32 && (c1 == 0 || c1 == 32) &&
+                     (kx2_mode == 2 || (kx2_mode == 1 && c1 == 32));
+    const bool px2_fit = kx2 || (cout == 32 && c1 == 0 &&
                          ((c0_tensor == 32 && (px2_mask() & 1)) ||
-                          (c0_tensor == 8 && !d_pool && !d_head_w && (px2_mask() & 2)));
+                          (c0_tensor == 8 && !d_pool && !d_head_w && (px2_mask() & 2))));
     if (!transposed && px2_fit) {
-        ls_conv_plan *pp = plan_px2(d_x0, c0_tensor, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
+        ls_conv_plan *pp = plan_px2(kx2, d_x0, c0_tensor, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
                                     alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
                                     d_head_out);
         if (pp) {
