@@ -47,6 +47,10 @@ using namespace ls::umma;
 #ifndef LS_MT256
 #define LS_MT256 1
 #endif
+// k_conv_px2 KX2 epilogue warpgroups (A/B build switch)
+#ifndef LS_KX2_GROUPS
+#define LS_KX2_GROUPS 3
+#endif
 // k_conv_kx (cout = 32): issue the second 16-channel half's TMEM loads before
 // processing the first (A/B build switch)
 #ifndef LS_KX_PIPE
@@ -857,13 +861,19 @@ struct CfgPx {
 // pixel as k_conv_kx with half its shuffles and 2/3 of its TMEM reads, and no
 // row-shifted operands -- for the two-source d0c1, where the neighbour-row
 // MMAs' extra operand reads lose.
+// epilogue warpgroups: KX2 items hold 128 TMEM columns and their epilogue
+// more live registers (three groups: 448 threads, up to 144 registers)
+template <bool KX2>
+__host__ __device__ constexpr int px_groups() { return KX2 ? LS_KX2_GROUPS : CfgPx::kEpiGroups; }
+
 template <int MODE, bool C8, bool KX2 = false>
-__global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
+__global__ void __launch_bounds__(64 + 128 * px_groups<KX2>()) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
     using C = CfgPx;
     constexpr int kN = KX2 ? 128 : C::kN;       // TMEM columns per item
     constexpr int kAcc = KX2 ? 4 : C::kAcc;
+    constexpr int kGroups = px_groups<KX2>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -912,7 +922,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         tmem_alloc(tslot, C::kTmemCols);
     } else if (warp >= 2) {
         const int t = threadIdx.x - 64;
-        constexpr int kEpiThreads = 128 * C::kEpiGroups;
+        constexpr int kEpiThreads = 128 * kGroups;
         for (int i = t; i < p.n_total; i += kEpiThreads) {
             sconst[i] = p.scale[i];
             sconst[p.n_total + i] = p.shift[i];
@@ -1094,7 +1104,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
         const int wp = p.w >> 1;
         uint32_t ab = (uint32_t)eg % kAcc, aph = ((uint32_t)eg / kAcc) & 1u;
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
-             item += C::kEpiGroups * gridDim.x) {
+             item += kGroups * gridDim.x) {
             int img, px0, y0;
             pos(item, img, px0, y0);
             mbar_wait(tfull + ab, aph);
@@ -1109,11 +1119,11 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             // (px1, 16-31); group g+1's tcgen05.ld is in flight while g is processed
             uint32_t ra[16], rb[16];
             auto col = [&](int g) -> uint32_t { return tbase + (uint32_t)((g & 1) * 32 + (g >> 1) * 16); };
-            auto process = [&](int g, const uint32_t(&rr)[16]) {
-                const int px = g & 1, n = (g >> 1) * 16;
+            // BN fold + activation of 16 channels of NP pixels (constants read once)
+            auto bnact = [&](int n, const uint32_t(&r0)[16], const uint32_t(&r1)[16],
+                             float(&v0)[16], float(&v1)[16], int np) {
                 const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
                 const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
-                float v[16];
 #pragma unroll
                 for (int i4 = 0; i4 < 4; ++i4) {
                     const float4 sc = sc4[i4], sh = sh4[i4];
@@ -1122,11 +1132,19 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
 #pragma unroll
                     for (int jp = 0; jp < 2; ++jp) {
                         const int i = 4 * i4 + 2 * jp;
-                        act2(fma2(f2(__uint_as_float(rr[i]), __uint_as_float(rr[i + 1])), sc2[jp],
+                        act2(fma2(f2(__uint_as_float(r0[i]), __uint_as_float(r0[i + 1])), sc2[jp],
                                   sh2[jp]),
-                             slope2, v[i], v[i + 1]);
+                             slope2, v0[i], v0[i + 1]);
+                        if (np > 1)
+                            act2(fma2(f2(__uint_as_float(r1[i]), __uint_as_float(r1[i + 1])),
+                                      sc2[jp], sh2[jp]),
+                                 slope2, v1[i], v1[i + 1]);
                     }
                 }
+            };
+            // head / bf16 stores / pool of one pixel's 16 channels
+            auto emit = [&](int g, const float(&v)[16]) {
+                const int px = g & 1, n = (g >> 1) * 16;
                 if (MODE == kHead) {
                     // both pixels of the pair at once: one FFMA2 per channel and
                     // head output, weights read once (each pixel's sum keeps the
@@ -1185,6 +1203,11 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                     }
                 }
             };
+            auto process = [&](int g, const uint32_t(&rr)[16]) {
+                float v[16];
+                bnact((g >> 1) * 16, rr, rr, v, v, 1);
+                emit(g, v);
+            };
             if constexpr (KX2) {
                 // 16-channel block n: out(2j) = own + left lane's spill-right,
                 // out(2j+1) = own + right lane's spill-left
@@ -1209,8 +1232,10 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
                         o1[i] = __float_as_uint(__uint_as_float(o1[i]) +
                                                 __shfl_down_sync(0xffffffffu, __uint_as_float(sl[i]), 1));
                     }
-                    process(2 * h2, o0);
-                    process(2 * h2 + 1, o1);
+                    float v0[16], v1[16];
+                    bnact((int)n, o0, o1, v0, v1, 2);
+                    emit(2 * h2, v0);
+                    emit(2 * h2 + 1, v1);
                 }
             } else {
             tmem_ld16_async(col(0), ra);
@@ -1244,7 +1269,7 @@ __global__ void __launch_bounds__(CfgPx::kThreads) k_conv_px2(
             }
             // next item of this group: kEpiGroups buffers further on
 #pragma unroll 1
-            for (int k = 0; k < C::kEpiGroups; ++k) {
+            for (int k = 0; k < kGroups; ++k) {
                 ab = ab + 1 == kAcc ? 0 : ab + 1;
                 aph ^= ab == 0;
             }
@@ -1409,7 +1434,7 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)CfgPx::kThreads);
+    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2>()));
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
