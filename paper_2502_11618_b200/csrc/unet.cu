@@ -863,17 +863,17 @@ struct CfgPx {
 // MMAs' extra operand reads lose.
 // epilogue warpgroups: KX2 items hold 128 TMEM columns and their epilogue
 // more live registers (three groups: 448 threads, up to 144 registers)
-template <bool KX2>
-__host__ __device__ constexpr int px_groups() { return KX2 ? LS_KX2_GROUPS : CfgPx::kEpiGroups; }
+template <bool G3>
+__host__ __device__ constexpr int px_groups() { return G3 ? LS_KX2_GROUPS : CfgPx::kEpiGroups; }
 
 template <int MODE, bool C8, bool KX2 = false>
-__global__ void __launch_bounds__(64 + 128 * px_groups<KX2>()) k_conv_px2(
+__global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
     using C = CfgPx;
     constexpr int kN = KX2 ? 128 : C::kN;       // TMEM columns per item
     constexpr int kAcc = KX2 ? 4 : C::kAcc;
-    constexpr int kGroups = px_groups<KX2>();
+    constexpr int kGroups = px_groups<KX2 || C8>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -1238,22 +1238,33 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2>()) k_conv_px2(
                     emit(2 * h2 + 1, v1);
                 }
             } else {
+            // both pixels of a 16-channel block per step (BN constants read once);
+            // the next block's loads are in flight while one is processed
+            uint32_t rc[16], rd[16];
             tmem_ld16_async(col(0), ra);
-            tmem_ld_wait16(ra);
             tmem_ld16_async(col(1), rb);
-            process(0, ra);
-            tmem_ld_wait16(rb);
-            tmem_ld16_async(col(2), ra);
-            process(1, rb);
             tmem_ld_wait16(ra);
-            tmem_ld16_async(col(3), rb);
-            process(2, ra);
             tmem_ld_wait16(rb);
+            tmem_ld16_async(col(2), rc);
+            tmem_ld16_async(col(3), rd);
+            {
+                float v0[16], v1[16];
+                bnact(0, ra, rb, v0, v1, 2);
+                emit(0, v0);
+                emit(1, v1);
+            }
+            tmem_ld_wait16(rc);
+            tmem_ld_wait16(rd);
             // item fully read -> hand the TMEM buffer back
             fence_before_sync();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty + ab);
-            process(3, rb);
+            {
+                float v0[16], v1[16];
+                bnact(16, rc, rd, v0, v1, 2);
+                emit(2, v0);
+                emit(3, v1);
+            }
             }
             if (MODE == kHead && valid) {
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
@@ -1434,7 +1445,7 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2>()));
+    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8>()));
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
