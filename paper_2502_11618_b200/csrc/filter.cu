@@ -14,6 +14,7 @@
 // Each output pixel depends only on a 3x3 coarse window, so every step is a
 // pure stencil; the working set (<= 8 MB at 1080p) stays in L2.
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "ls_common.cuh"
 
@@ -21,15 +22,20 @@ namespace ls {
 
 __device__ __forceinline__ float sentinel(float d) { return d <= 0.0f ? INFINITY : d; }
 
+// The stencil helpers read the image through an accessor get(y, x) (only ever
+// called for in-image coordinates), so the global-memory kernels and the
+// fused shared-memory steps run the same arithmetic.
+
 // _native.pyx:173-196 at one pixel
-__device__ __forceinline__ bool lap_edge(const float *__restrict__ img, int64_t h, int64_t w,
-                                         int64_t y, int64_t x, double thr) {
-    const double c = (double)img[y * w + x];
+template <typename Get>
+__device__ __forceinline__ bool lap_edge_t(Get get, int64_t h, int64_t w, int64_t y, int64_t x,
+                                           double thr) {
+    const double c = (double)get(y, x);
     if (!finite_d(c)) return false;
-    double up = y > 0 ? (double)img[(y - 1) * w + x] : c;
-    double dn = y + 1 < h ? (double)img[(y + 1) * w + x] : c;
-    double lf = x > 0 ? (double)img[y * w + x - 1] : c;
-    double rt = x + 1 < w ? (double)img[y * w + x + 1] : c;
+    double up = y > 0 ? (double)get(y - 1, x) : c;
+    double dn = y + 1 < h ? (double)get(y + 1, x) : c;
+    double lf = x > 0 ? (double)get(y, x - 1) : c;
+    double rt = x + 1 < w ? (double)get(y, x + 1) : c;
     if (!finite_d(up)) up = c;
     if (!finite_d(dn)) dn = c;
     if (!finite_d(lf)) lf = c;
@@ -39,16 +45,17 @@ __device__ __forceinline__ bool lap_edge(const float *__restrict__ img, int64_t 
 }
 
 // _native.pyx:205-220: reference depth of coarse pixel (cy,cx)
-__device__ __forceinline__ double parent_ref(const float *__restrict__ coarse, int64_t ch,
-                                             int64_t cw, int64_t cy, int64_t cx, bool edge) {
-    const double c = (double)coarse[cy * cw + cx];
+template <typename Get>
+__device__ __forceinline__ double parent_ref_t(Get get, int64_t ch, int64_t cw, int64_t cy,
+                                               int64_t cx, bool edge) {
+    const double c = (double)get(cy, cx);
     double ref = finite_d(c) ? c : -INFINITY;
     if (edge) {
         for (int64_t ny = cy - 1; ny <= cy + 1; ++ny) {
             if (ny < 0 || ny >= ch) continue;
             for (int64_t nx = cx - 1; nx <= cx + 1; ++nx) {
                 if (nx < 0 || nx >= cw || (ny == cy && nx == cx)) continue;
-                const double v = (double)coarse[ny * cw + nx];
+                const double v = (double)get(ny, nx);
                 if (finite_d(v) && v > ref) ref = v;
             }
         }
@@ -62,8 +69,9 @@ __device__ __forceinline__ bool keep_test(float f, double ref, double fs) {
 }
 
 // _native.pyx:240-297 at one fine pixel (called only for holes)
-__device__ __forceinline__ float bilinear_at(const float *__restrict__ coarse, int64_t ch,
-                                             int64_t cw, int64_t y, int64_t x) {
+template <typename Get>
+__device__ __forceinline__ float bilinear_at_t(Get get, int64_t ch, int64_t cw, int64_t y,
+                                               int64_t x) {
     const double gy = dsub(dmul(0.5, (double)y), 0.25);
     const int64_t y0r = (int64_t)floor(gy);
     const double wy1 = dsub(gy, (double)y0r), wy0 = dsub(1.0, wy1);
@@ -81,7 +89,7 @@ __device__ __forceinline__ float bilinear_at(const float *__restrict__ coarse, i
     for (int a = 0; a < 2; ++a) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-            const double v = (double)coarse[yy[a] * cw + xx[b]];
+            const double v = (double)get(yy[a], xx[b]);
             if (finite_d(v)) {
                 const double wgt = dmul(wy[a], wx[b]);
                 num = dadd(num, dmul(wgt, v));
@@ -90,6 +98,27 @@ __device__ __forceinline__ float bilinear_at(const float *__restrict__ coarse, i
         }
     }
     return den > 0.0 ? __double2float_rn(ddiv(num, den)) : INFINITY;
+}
+
+struct GlobalImg {
+    const float *img;
+    int64_t w;
+    __device__ float operator()(int64_t y, int64_t x) const { return img[y * w + x]; }
+};
+
+__device__ __forceinline__ bool lap_edge(const float *__restrict__ img, int64_t h, int64_t w,
+                                         int64_t y, int64_t x, double thr) {
+    return lap_edge_t(GlobalImg{img, w}, h, w, y, x, thr);
+}
+
+__device__ __forceinline__ double parent_ref(const float *__restrict__ coarse, int64_t ch,
+                                             int64_t cw, int64_t cy, int64_t cx, bool edge) {
+    return parent_ref_t(GlobalImg{coarse, cw}, ch, cw, cy, cx, edge);
+}
+
+__device__ __forceinline__ float bilinear_at(const float *__restrict__ coarse, int64_t ch,
+                                             int64_t cw, int64_t y, int64_t x) {
+    return bilinear_at_t(GlobalImg{coarse, cw}, ch, cw, y, x);
 }
 
 // ----------------------------------------------------------------- twins ---
@@ -476,6 +505,118 @@ inline void level_sizes(int64_t H, int64_t W, int L, int64_t *h, int64_t *w) {
     }
 }
 
+// ---- fused non-final steps ------------------------------------------------
+// All L-1 non-final steps of the filter in ONE launch (filtering.py:124-131):
+// each CTA produces a 64x32 tile of the last non-final step's output and
+// recomputes, in shared memory, exactly the parts of the coarser steps' outputs
+// its stencils read (every output pixel depends on a 3x3 coarse window, so a
+// level-k region needs its parents +-1 at level k+1).  Neighbouring CTAs
+// recompute overlapping halos with the same arithmetic, so the result is the
+// per-step kernels' bit for bit; the L-1 launches (each latency-bound on a
+// small image) become one.
+constexpr int kFuseTX = 64, kFuseTY = 32, kFuseMaxSteps = 4, kFuseBuf = 1024;
+
+struct Rect {
+    int y0, y1, x0, x1;  // [y0, y1) x [x0, x1)
+    __device__ int h() const { return y1 - y0; }
+    __device__ int w() const { return x1 - x0; }
+};
+
+// the coarse pixels a fine region's stencils read: parents +-1, clipped
+__device__ __forceinline__ Rect coarse_of(const Rect &f, int ch, int cw) {
+    Rect c;
+    c.y0 = max((f.y0 >> 1) - 1, 0);
+    c.y1 = min(((f.y1 - 1) >> 1) + 2, ch);
+    c.x0 = max((f.x0 >> 1) - 1, 0);
+    c.x1 = min(((f.x1 - 1) >> 1) + 2, cw);
+    return c;
+}
+
+struct SmemImg {
+    const float *buf;
+    Rect r;
+    __device__ float operator()(int64_t y, int64_t x) const {
+        return buf[((int)y - r.y0) * r.w() + ((int)x - r.x0)];
+    }
+};
+
+__global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *__restrict__ out,
+                                                             double fs, double et) {
+    pdl_wait();
+    __shared__ float ubuf[2][kFuseBuf];     // coarse input of the current step / its output
+    __shared__ double refbuf[kFuseBuf];     // reference depth per parent pixel
+    const int L = lv.L, nsteps = L - 1;
+    // regions: R[i] = output region of step i+1 (level L-1-i), R[nsteps-1] = this tile
+    Rect R[kFuseMaxSteps];
+    {
+        Rect t;
+        t.y0 = blockIdx.y * kFuseTY;
+        t.y1 = min(t.y0 + kFuseTY, (int)lv.h[1]);
+        t.x0 = blockIdx.x * kFuseTX;
+        t.x1 = min(t.x0 + kFuseTX, (int)lv.w[1]);
+        R[nsteps - 1] = t;
+        for (int i = nsteps - 2; i >= 0; --i) {
+            const int lev = L - 1 - i;  // level of R[i]
+            (void)lev;
+            R[i] = coarse_of(R[i + 1], (int)lv.h[L - 1 - i], (int)lv.w[L - 1 - i]);
+        }
+    }
+    // coarse input of step 1: pooled^L on coarse_of(R[0])
+    Rect C = coarse_of(R[0], (int)lv.h[L], (int)lv.w[L]);
+    int cur = 0;
+    for (int i = threadIdx.x; i < C.h() * C.w(); i += blockDim.x) {
+        const int y = C.y0 + i / C.w(), x = C.x0 + i % C.w();
+        ubuf[cur][i] = lv.img[L - 1][(int64_t)y * lv.w[L] + x];
+    }
+    __syncthreads();
+    for (int st = 0; st < nsteps; ++st) {
+        const int clev = L - st, flev = L - st - 1;  // coarse / fine levels of this step
+        const int64_t ch = lv.h[clev], cw = lv.w[clev], fw = lv.w[flev];
+        const float *fine = lv.img[flev - 1];        // pooled^flev
+        const Rect F = R[st];
+        const SmemImg getC{ubuf[cur], C};
+        // parents of F (inside C by construction)
+        Rect P;
+        P.y0 = F.y0 >> 1;
+        P.y1 = ((F.y1 - 1) >> 1) + 1;
+        P.x0 = F.x0 >> 1;
+        P.x1 = ((F.x1 - 1) >> 1) + 1;
+        for (int i = threadIdx.x; i < P.h() * P.w(); i += blockDim.x) {
+            const int cy = P.y0 + i / P.w(), cx = P.x0 + i % P.w();
+            const bool edge = lap_edge_t(getC, ch, cw, cy, cx, et);
+            refbuf[i] = parent_ref_t(getC, ch, cw, cy, cx, edge);
+        }
+        __syncthreads();
+        const bool last = st == nsteps - 1;
+        for (int i = threadIdx.x; i < F.h() * F.w(); i += blockDim.x) {
+            const int y = F.y0 + i / F.w(), x = F.x0 + i % F.w();
+            const double ref = refbuf[((y >> 1) - P.y0) * P.w() + ((x >> 1) - P.x0)];
+            const float f = fine[(int64_t)y * fw + x];
+            const float o = keep_test(f, ref, fs) ? f : bilinear_at_t(getC, ch, cw, y, x);
+            if (last) out[(int64_t)y * fw + x] = o;
+            else ubuf[cur ^ 1][i] = o;
+        }
+        __syncthreads();
+        cur ^= 1;
+        C = F;
+    }
+    pdl_trigger();
+}
+
+// Does a fused coarse launch cover this pyramid?  (every intermediate region
+// must fit the shared buffers: true for kFuseTY x kFuseTX tiles and L <= 5)
+inline bool fused_ok(const Levels &lv) { return lv.L >= 2 && lv.L - 1 <= kFuseMaxSteps; }
+
+// LS_FILTER_FUSED=0 runs one launch per non-final step (A/B measurements).
+inline bool fused_steps_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_FILTER_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 // Pyramid + steps over an existing sentinel-able depth image.  `lvl` holds
 // pooled^1..pooled^L, `up` the filled images of steps 1..L-1.
 int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, int64_t H,
@@ -486,7 +627,19 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
     const int L = lv.L;
     const float *coarse = lv.img[L - 1];  // pyr.levels[0]
     float *up = up_base;
-    for (int i = 1; i <= L; ++i) {
+    int first = 1;
+    if (fused_ok(lv) && fused_steps_enabled()) {
+        // steps 1..L-1 in one launch; its output sits where step L-1 would write
+        for (int i = 1; i < L - 1; ++i) up += lv.h[L - i] * lv.w[L - i];
+        const dim3 g((unsigned)((lv.w[1] + kFuseTX - 1) / kFuseTX),
+                     (unsigned)((lv.h[1] + kFuseTY - 1) / kFuseTY));
+        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up, fs, et);
+        if (e != cudaSuccess) return (int)e;
+        coarse = up;
+        up += lv.h[1] * lv.w[1];
+        first = L;
+    }
+    for (int i = first; i <= L; ++i) {
         const int64_t ch = lv.h[L - i + 1], cw = lv.w[L - i + 1];
         const int64_t fh = lv.h[L - i], fw = lv.w[L - i];
         if (i < L) {

@@ -19,9 +19,20 @@ from .frame import FrameRGBDA, RenderParams
 from .render import FrameBuffers, ViewBuffers, project_scene, project_scene_views
 
 # kernel launches per frame of the fused path: cull, work-list counter reset,
-# tile work list, pass 1, pass 2, assemble+pyramid, L filter steps (+ U-Net
+# tile work list, pass 1, pass 2, assemble+pyramid, the filter steps (+ U-Net
 # layers when attached)
 BASE_LAUNCHES = 6
+
+
+def filter_launches(levels_n: int) -> int:
+    """Launches of the filter steps: the L-1 non-final steps run as one fused
+    launch when 2 <= L <= 5 (csrc/filter.cu k_filter_coarse_fused), then the
+    final step; LS_FILTER_FUSED=0 restores one launch per step."""
+    import os
+
+    if 2 <= levels_n <= 5 and os.environ.get("LS_FILTER_FUSED", "1") != "0":
+        return 2
+    return levels_n
 
 
 class FrameRenderer:
@@ -68,7 +79,7 @@ class FrameRenderer:
 
     @property
     def launches_per_frame(self) -> int:
-        n = BASE_LAUNCHES + self.fp.levels_n
+        n = BASE_LAUNCHES + filter_launches(self.fp.levels_n)
         if self.unet is not None:
             n += self.unet.launches
         return n
@@ -246,7 +257,7 @@ class ViewBatchRenderer:
     def launches_per_batch(self) -> int:
         # per view: cull, assemble+pyramid, L filter steps; per batch: count
         # reset, work list, 2 passes (+ U-Net layers)
-        n = self.n_views * (2 + self.fp.levels_n) + 4
+        n = self.n_views * (2 + filter_launches(self.fp.levels_n)) + 4
         if self.unet is not None:
             n += self.unet.launches
         return n
