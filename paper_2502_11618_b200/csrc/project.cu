@@ -16,6 +16,8 @@
 #include "ls_common.cuh"
 #include "umma.cuh"
 
+#include <stdlib.h>
+
 #include <type_traits>
 
 namespace ls {
@@ -497,6 +499,53 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
+    });
+    pdl_trigger();
+}
+
+// Pass 1 with 32-bit pixel indices (frames with W*H < 2^32 - 1).
+__device__ __forceinline__ void drop_culled_u32(const SceneArgs &s,
+                                                const uint32_t *__restrict__ bits,
+                                                const Item &it, uint32_t (&pix)[4]) {
+    if (!(it.e & kMixed)) return;
+    const int64_t tile = it.e & ~kMixed;
+    const int c0 = __ldg(s.tile_c0 + tile), c1 = __ldg(s.tile_c1 + tile);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (pix[k] != kNoPixel && !point_kept(s, bits, c0, c1, it.base + k)) pix[k] = kNoPixel;
+}
+
+__global__ void __launch_bounds__(256) k_frame_pass1_u32(SceneArgs s, ProjCam c,
+                                                         const uint32_t *__restrict__ bits,
+                                                         const uint32_t *__restrict__ list,
+                                                         const uint32_t *__restrict__ count,
+                                                         unsigned long long *__restrict__ minz,
+                                                         uint32_t *__restrict__ cache) {
+    pdl_wait();
+    for_each_item<kPass1Stages, kXyz>(s, list, count, nullptr, [&](const Item &it, uint3) {
+        float P[12];
+        const int cnt = item_points(s, it, P);
+        uint32_t pix[4];
+        double zc[4];
+        project4_u32(P, cnt, c, pix, zc);
+        drop_culled_u32(s, bits, it, pix);
+        if (cache) {
+            const int lane = threadIdx.x & 31;
+            uint32_t *blk = cache + it.index * (kCacheBytes / 4);
+            reinterpret_cast<uint4 *>(blk)[lane] = make_uint4(pix[0], pix[1], pix[2], pix[3]);
+            reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
+                make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
+                            __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+        }
+        unsigned long long cur[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            cur[k] = pix[k] != kNoPixel ? __ldca(minz + pix[k]) : 0ull;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long key = (unsigned long long)__double_as_longlong(zc[k]);
+            if (pix[k] != kNoPixel && key < cur[k]) red_min_u64(minz + pix[k], key);
+        }
     });
     pdl_trigger();
 }
@@ -1003,6 +1052,16 @@ static bool cache_ok(const ls_camera *cam, const void *d_cache) {
                         (reinterpret_cast<uintptr_t>(d_cache) & 15) == 0);
 }
 
+// LS_PASS1_U32=0 keeps 64-bit pixel indices in pass 1 (A/B measurements).
+static bool pass1_u32() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("LS_PASS1_U32");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,
                    const uint32_t *d_count, const ls_camera *cam, uint64_t *d_minz_bits,
                    uint32_t *d_cache, void *stream) {
@@ -1012,6 +1071,11 @@ int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
     if (scene->n_points == 0) return 0;
     SceneArgs a = scene_args(*scene);
     a.n_tiles = (a.n + LS_TILE_POINTS - 1) / LS_TILE_POINTS;
+    if (cam->width * cam->height < (int64_t)kNoPixel && pass1_u32())
+        return (int)launch_pdl(k_frame_pass1_u32,
+                               dim3(frame_grid(k_frame_pass1_u32, kSmem1, a.n_tiles)), dim3(256),
+                               kSmem1, (cudaStream_t)stream, a, make_cam(*cam), d_keep_bits,
+                               d_list, d_count, (unsigned long long *)d_minz_bits, d_cache);
     return (int)launch_pdl(k_frame_pass1, dim3(frame_grid(k_frame_pass1, kSmem1, a.n_tiles)),
                            dim3(256), kSmem1, (cudaStream_t)stream, a, make_cam(*cam), d_keep_bits,
                            d_list, d_count, (unsigned long long *)d_minz_bits, d_cache);
