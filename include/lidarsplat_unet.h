@@ -60,6 +60,14 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
                                   uint16_t *d_pool, const float *d_head_w, const float *d_head_b,
                                   int32_t head_c, float *d_head_out, int32_t *status);
 int ls_conv_plan_launch(const ls_conv_plan *plan, void *stream);
+
+/* Row bands: restrict a plan to the output rows [row_begin, row_end) of its
+ * grid (input rows for transposed convs), row_begin a multiple of
+ * ls_conv_plan_tile_rows(plan); the inputs are still read from the whole
+ * tensors (halo rows included).  Running a producer layer and its consumer
+ * band by band keeps the intermediate band in L2. */
+int ls_conv_plan_set_rows(ls_conv_plan *plan, int32_t row_begin, int32_t row_end);
+int32_t ls_conv_plan_tile_rows(const ls_conv_plan *plan);
 void ls_conv_plan_destroy(ls_conv_plan *plan);
 
 /* One-shot convenience: plan, launch, destroy. */

@@ -66,6 +66,7 @@ enum EpiMode { kPlain = 0, kPool = 1, kHead = 2, kTransposed = 3 };
 struct ConvParamsP {
     int batch, h, w;
     int tiles_x, tiles_y, n_tiles_m, n_tiles_n, n_items;
+    int ty0;                // first tile row of a row band (ls_conv_plan_set_rows)
     int c0, c1, ctot, nq0, nq;
     int kxs, kxps, pad;     // kx taps, kx taps per pipeline stage (1 or kxs)
     int n_total, cout, act;
@@ -225,7 +226,7 @@ __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, floa
     ip.img = fdiv(mt, tpi, r_tpi);
     const int r = mt - ip.img * tpi;
     const int ty = fdiv(r, p.tiles_x, r_tx);
-    ip.y0 = ty * tile_h;
+    ip.y0 = (p.ty0 + ty) * tile_h;
     ip.x0 = (r - ty * p.tiles_x) * kTW;
     return ip;
 }
@@ -585,7 +586,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
         img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
         const int r = item - img * p.tiles_x * p.tiles_y;
         const int ty = fdiv(r, p.tiles_x, r_tx);
-        y0 = ty * kTH;
+        y0 = (p.ty0 + ty) * kTH;
         x0 = (r - ty * p.tiles_x) * kKxCols;
     };
 
@@ -895,7 +896,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
         img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
         const int r = item - img * p.tiles_x * p.tiles_y;
         const int ty = fdiv(r, p.tiles_x, r_tx);
-        y0 = ty * kTH;
+        y0 = (p.ty0 + ty) * kTH;
         px0 = (r - ty * p.tiles_x) * kPxCols - 1;
     };
     const int nsrc = p.nq;  // 1 or 2 sources of 32 channels, one 64-channel pair chunk each
@@ -1354,6 +1355,7 @@ struct ls_conv_plan {
     ConvParamsP p;
     int bn, chunk, grid, mode;
     int mt;    // k_conv_p: 128-pixel sub-tiles per work item
+    int full_tiles_y;  // tile rows of the whole layer (row bands restrict p.ty0 / p.tiles_y)
     int kind;  // 0: k_conv_p, 1: k_conv_kx (kx taps stacked along N), 2: k_conv_px2 (pixel pairs)
     size_t smem;
 };
@@ -1547,7 +1549,7 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
                               const float *d_head_b, int head_c, float *d_head_out) {
     using namespace ls::unet;
     if (w % 2) return nullptr;
-    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan();
     if (!pl) return nullptr;
     ConvParamsP &p = pl->p;
     p = ConvParamsP{};
@@ -1613,6 +1615,7 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    pl->full_tiles_y = p.tiles_y;
     // the NHWC tensors read as (W/2) pair pixels of 2*c channels
     const int pc = c8 ? 16 : 64;
     bool ok = encode_act(&pl->a0, d_x0, pc, w / 2, h, batch, pc, kTH + 2);
@@ -1638,7 +1641,7 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     int chunk = 64;
     while (chunk > 16 && ((c0 % chunk) || (c1 % chunk))) chunk >>= 1;
     if ((c0 % chunk) || (c1 % chunk)) return nullptr;
-    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan();
     if (!pl) return nullptr;
     ConvParamsP &p = pl->p;
     p = ConvParamsP{};
@@ -1700,6 +1703,7 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    pl->full_tiles_y = p.tiles_y;
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, kTH + 2);
     ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
                           chunk, kTH + 2);
@@ -1785,7 +1789,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     int chunk = bn >= 256 ? 32 : 64;
     while (chunk > 16 && ((c0 % chunk) || (c1 % chunk))) chunk >>= 1;
 
-    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan;
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan();
     if (!pl) return fail(LS_EINVAL);
     pl->kind = 0;
     ConvParamsP &p = pl->p;
@@ -1870,6 +1874,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    pl->full_tiles_y = p.tiles_y;
     const int box_h = kTH * mt + 2 * p.pad;
     pl->mt = mt;
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, box_h);
@@ -1906,6 +1911,29 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
 }
 
 void ls_conv_plan_destroy(ls_conv_plan *pl) { delete pl; }
+
+int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) {
+    if (!pl) return LS_EINVAL;
+    const int th = pl->kind == 0 ? kTH * pl->mt : kTH;  // rows per tile
+    const int h = pl->p.h;
+    if (row_begin < 0 || row_end > h || row_begin >= row_end || row_begin % th) return LS_EINVAL;
+    const int t0 = row_begin / th, t1 = (row_end + th - 1) / th;
+    if (t1 > pl->full_tiles_y) return LS_EINVAL;
+    ConvParamsP &p = pl->p;
+    p.ty0 = t0;
+    p.tiles_y = t1 - t0;
+    p.n_tiles_m = p.tiles_x * p.tiles_y * p.batch;
+    p.n_items = p.n_tiles_m * p.n_tiles_n;
+    int n_sm = 148;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    return 0;
+}
+
+int32_t ls_conv_plan_tile_rows(const ls_conv_plan *pl) {
+    if (!pl) return LS_EINVAL;
+    return pl->kind == 0 ? kTH * pl->mt : kTH;
+}
 
 int ls_conv2d(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1, int32_t c1, int32_t batch,
               int32_t h, int32_t w, const uint16_t *d_w, int32_t ksize, int32_t cout,

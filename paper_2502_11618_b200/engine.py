@@ -81,7 +81,7 @@ class FrameRenderer:
     def launches_per_frame(self) -> int:
         n = BASE_LAUNCHES + filter_launches(self.fp.levels_n)
         if self.unet is not None:
-            n += self.unet.launches
+            n += self.unet.launches_for(self.unet_in.shape[1], self.width)
         return n
 
     def _outputs(self, slot: int):
@@ -259,7 +259,7 @@ class ViewBatchRenderer:
         # reset, work list, 2 passes (+ U-Net layers)
         n = self.n_views * (2 + filter_launches(self.fp.levels_n)) + 4
         if self.unet is not None:
-            n += self.unet.launches
+            n += self.unet.launches_for(self.unet_in.shape[1], self.width, self.n_views)
         return n
 
     def enqueue(self, cameras) -> None:

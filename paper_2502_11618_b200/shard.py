@@ -122,7 +122,11 @@ class ShardedRenderer:
     def launches_per_frame(self) -> int:
         # cull, counter reset, work list, pass 1, pass 2 on every rank; finish +
         # filter + U-Net on the root (1/world of the frames)
-        n = 5 + (1 + self.fp.levels_n + (self.unet.launches if self.unet else 0)) / self.world
+        from .engine import filter_launches
+
+        unet_n = (self.unet.launches_for(self.unet_in.shape[1], self.unet_in.shape[2])
+                  if self.unet else 0)
+        n = 5 + (1 + filter_launches(self.fp.levels_n) + unet_n) / self.world
         return int(round(n))
 
     def enqueue(self, camera) -> None:

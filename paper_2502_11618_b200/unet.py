@@ -279,7 +279,13 @@ class UNet:
 
     @property
     def launches(self) -> int:
-        return 5 * self.cfg.depth + 2
+        return 5 * self.cfg.depth + 2  # unbanded; see launches_for(h, w, batch)
+
+    def launches_for(self, h: int, w: int, batch: int = 1) -> int:
+        """Conv launches of one forward at this size (full-resolution row bands
+        multiply the 5 full-resolution layers' launches)."""
+        nb = _full_res_bands(batch, h, w)
+        return 5 * self.cfg.depth + 2 + (5 * (nb - 1) if nb > 1 else 0)
 
     def flops(self, width: int, height: int) -> float:
         return unet_flops(self.cfg, width, height)
@@ -386,7 +392,7 @@ class UNet:
         keep = []
 
         def mk(src0, c0, src1, c1, hs, ws, layer, act, y=None, pool=None, transposed=False,
-               head=None):
+               head=None, rows=None):
             st = ctypes.c_int32(0)
             hw, hb, hc, ho = (None, None, 0, None) if head is None else head
             pl = lib.ls_conv_plan_create(
@@ -398,14 +404,36 @@ class UNet:
             if not pl:
                 raise RuntimeError(f"conv plan failed ({st.value})")
             plans.append(pl)
+            if rows is not None:
+                t = lib.ls_conv_plan_tile_rows(pl)
+                hh = hs  # the plan's row grid (input rows for transposed convs)
+                lo = max(rows[0] // t * t, 0)
+                hi = min(-(-rows[1] // t) * t, hh)
+                _lib.check(lib.ls_conv_plan_set_rows(pl, lo, hi), "conv_plan_set_rows")
+            return pl
+
+        # Optional full-resolution row bands (LS_UNET_BANDS): a producer layer
+        # and its consumer run band by band so the producer's band is still in
+        # L2 when the consumer reads it; halo rows are recomputed per band.
+        # Off by default (measured slower, see _full_res_bands).
+        nb = _full_res_bands(batch, h, w)
+        edges = [min(h, (k * h // nb + 15) // 16 * 16) for k in range(nb + 1)]
+        edges[-1] = h
 
         cur, ccur = x, cin
         for s in range(cfg.depth):
             hs, ws = h >> s, w >> s
             c = _pad16(stage_width(cfg, s))
-            mk(cur, ccur, None, 0, hs, ws, L[f"enc{s}_conv1"], 1, y=B[("t1", s)])
-            mk(B[("t1", s)], c, None, 0, hs, ws, L[f"enc{s}_conv2"], 1, y=B[("skip", s)],
-               pool=B[("pooled", s + 1)])
+            if s == 0 and nb > 1:
+                for b0, b1 in zip(edges[:-1], edges[1:]):
+                    mk(cur, ccur, None, 0, hs, ws, L["enc0_conv1"], 1, y=B[("t1", 0)],
+                       rows=(b0 - 1, b1 + 1))
+                    mk(B[("t1", 0)], c, None, 0, hs, ws, L["enc0_conv2"], 1, y=B[("skip", 0)],
+                       pool=B[("pooled", 1)], rows=(b0, b1))
+            else:
+                mk(cur, ccur, None, 0, hs, ws, L[f"enc{s}_conv1"], 1, y=B[("t1", s)])
+                mk(B[("t1", s)], c, None, 0, hs, ws, L[f"enc{s}_conv2"], 1, y=B[("skip", s)],
+                   pool=B[("pooled", s + 1)])
             cur, ccur = B[("pooled", s + 1)], c
         d = cfg.depth
         hs, ws, cb = h >> d, w >> d, _pad16(stage_width(cfg, d))
@@ -416,6 +444,19 @@ class UNet:
         for s in range(cfg.depth - 1, -1, -1):
             hs, ws = h >> s, w >> s
             c = _pad16(stage_width(cfg, s))
+            if s == 0 and nb > 1:
+                for b0, b1 in zip(edges[:-1], edges[1:]):
+                    # conv2 rows [b0, b1) read conv1 rows b0-1 .. b1 (tile-aligned by
+                    # mk), conv1 rows read up rows one further, up rows 2i, 2i+1 come
+                    # from input row i of the transposed conv
+                    c1r = (max(b0 - 8, 0), min(b1 + 8, h))
+                    mk(cur, ccur, None, 0, hs // 2, ws // 2, L["dec0_up"], 0, y=B[("up", 0)],
+                       transposed=True, rows=((c1r[0] - 1) // 2, (c1r[1] + 2) // 2))
+                    mk(B[("up", 0)], c, B[("skip", 0)], c, hs, ws, L["dec0_conv1"], 2,
+                       y=B[("d1", 0)], rows=c1r)
+                    mk(B[("d1", 0)], c, None, 0, hs, ws, L["dec0_conv2"], 2,
+                       head=(fc["w"], fc["b"], cfg.outChannels, out), rows=(b0, b1))
+                continue
             mk(cur, ccur, None, 0, hs // 2, ws // 2, L[f"dec{s}_up"], 0, y=B[("up", s)],
                transposed=True)
             mk(B[("up", s)], c, B[("skip", s)], c, hs, ws, L[f"dec{s}_conv1"], 2, y=B[("d1", s)])
@@ -436,6 +477,19 @@ class UNet:
 
 
 import ctypes  # noqa: E402  (used by the plan helpers above)
+
+
+def _full_res_bands(batch: int, h: int, w: int) -> int:
+    """Row bands of the full-resolution layers (LS_UNET_BANDS, default 1 = off).
+    Measured at 1920x1088 (profiles/README.md): 1 band 0.881 ms, 2 bands 0.897,
+    4 bands 0.936, 8 bands 1.027 -- the per-band launch tails and halo
+    recompute cost more than the L2 residency of the band saves."""
+    import os
+
+    nb = max(1, int(os.environ.get("LS_UNET_BANDS", "1")))
+    while nb > 1 and h // nb < 64:  # bands of at least 64 rows
+        nb //= 2
+    return nb
 
 
 class _Plans:

@@ -213,3 +213,19 @@ def test_full_frame_with_unet_vs_oracle(port):
     err = float(np.abs(got - ref).max())
     print(f"frame+unet max-abs {err:.3e} PSNR {_psnr(got, ref):.1f} dB")
     assert err <= 1.5e-2 and _psnr(got, ref) >= 40.0
+
+
+def test_full_res_row_bands_identical(monkeypatch):
+    """LS_UNET_BANDS: the full-resolution layers run band by band
+    (ls_conv_plan_set_rows, halo rows recomputed per band) -- the same kernels
+    on the same pixels, so the output is bit-identical to the unbanded run."""
+    from paper_2502_11618_b200.unet import UNet
+
+    x = _input(np.random.default_rng(8), 256, 160)
+    monkeypatch.setenv("LS_UNET_BANDS", "1")
+    a = _run_device(UNet.from_config("default", seed=6), x, 8)
+    monkeypatch.setenv("LS_UNET_BANDS", "4")
+    net = UNet.from_config("default", seed=6)
+    b = _run_device(net, x, 8)
+    assert net.launches_for(256, 160) == net.launches + 15
+    assert np.array_equal(a, b)
