@@ -514,7 +514,7 @@ inline void level_sizes(int64_t H, int64_t W, int L, int64_t *h, int64_t *w) {
 // recompute overlapping halos with the same arithmetic, so the result is the
 // per-step kernels' bit for bit; the L-1 launches (each latency-bound on a
 // small image) become one.
-constexpr int kFuseTX = 64, kFuseTY = 32, kFuseMaxSteps = 4, kFuseBuf = 1024;
+constexpr int kFuseTX = 32, kFuseTY = 16, kFuseMaxSteps = 4, kFuseBuf = 512;
 
 struct Rect {
     int y0, y1, x0, x1;  // [y0, y1) x [x0, x1)
