@@ -51,6 +51,9 @@ typedef struct ls_conv_plan ls_conv_plan;
  * (read as 16 channels whose upper 8 are zero -- TMA out-of-bounds fill --
  * so W rows then hold 16 channels); cout multiple of 16;
  * columns (cout or 4*cout) <= 4096; h, w even when pooling.
+ * scale / shift may be captured by value when the plan is created (the
+ * 32-channel full-resolution kernels keep them as kernel parameters): create
+ * the plan after they hold their final values.
  * *status receives 0 or LS_EINVAL / a CUDA error; returns NULL on failure. */
 ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1,
                                   int32_t c1, int32_t batch, int32_t h, int32_t w,

@@ -79,6 +79,10 @@ struct ConvParamsP {
     int head_c;
     float *head_out;
     const void *wts;        // weights [tap][n][c] (k_conv_px2 C8 builds its B tiles from it)
+    // k_conv_px2: the 32 columns' BN scale / shift as kernel parameters (copied at
+    // plan creation) -- the epilogue reads them as constant-bank operands instead
+    // of shared-memory loads, which competed with the MMA operand reads in L1
+    float pc_scale[32], pc_shift[32];
     int resident;           // weights resident in smem
     int stages;
     uint32_t a_bytes;       // one A box footprint (1024-aligned)
@@ -1123,13 +1127,12 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             // BN fold + activation of 16 channels of NP pixels (constants read once)
             auto bnact = [&](int n, const uint32_t(&r0)[16], const uint32_t(&r1)[16],
                              float(&v0)[16], float(&v1)[16], int np) {
-                const float4 *sc4 = reinterpret_cast<const float4 *>(s_scale + n);
-                const float4 *sh4 = reinterpret_cast<const float4 *>(s_shift + n);
 #pragma unroll
                 for (int i4 = 0; i4 < 4; ++i4) {
-                    const float4 sc = sc4[i4], sh = sh4[i4];
-                    const f32x2 sc2[2] = {f2(sc.x, sc.y), f2(sc.z, sc.w)};
-                    const f32x2 sh2[2] = {f2(sh.x, sh.y), f2(sh.z, sh.w)};
+                    const float *sc = p.pc_scale + n + 4 * i4;
+                    const float *sh = p.pc_shift + n + 4 * i4;
+                    const f32x2 sc2[2] = {f2(sc[0], sc[1]), f2(sc[2], sc[3])};
+                    const f32x2 sh2[2] = {f2(sh[0], sh[1]), f2(sh[2], sh[3])};
 #pragma unroll
                     for (int jp = 0; jp < 2; ++jp) {
                         const int i = 4 * i4 + 2 * jp;
@@ -1561,6 +1564,11 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.c1 = c1;
     p.ctot = p.c0 + c1;
     p.wts = d_w;
+    if (cudaMemcpy(p.pc_scale, d_scale, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(p.pc_shift, d_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        delete pl;
+        return nullptr;
+    }
     p.kxs = 3;
     p.kxps = 1;
     p.pad = 1;
