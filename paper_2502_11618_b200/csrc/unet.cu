@@ -884,8 +884,6 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
     const uint32_t sbase = smem_u32(smem);
     const int S = p.stages;
     float *sconst = reinterpret_cast<float *>(smem + p.off_const);
-    const float *s_scale = sconst;
-    const float *s_shift = sconst + p.n_total;
     const float *s_hw = sconst + 2 * p.n_total;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
     uint64_t *empty = full + S;
