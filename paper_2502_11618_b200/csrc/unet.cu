@@ -1788,6 +1788,17 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     int bn = n_total >= 256 ? 256 : (n_total >= 128 ? 128 : (n_total >= 64 ? 64 : 32));
     if (n_total % bn) bn = 32;
+    {
+        // small grids (the 1/16-resolution bottleneck): 128-column tiles when
+        // 256-column ones leave SMs idle (LS_CONV_SMALLN=0 keeps 256)
+        int n_sm = 148;
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        const long long m_tiles = (long long)((w + kTW - 1) / kTW) * ((h + kTH - 1) / kTH) * batch;
+        const char *e = getenv("LS_CONV_SMALLN");
+        if (bn == 256 && !transposed && !d_head_w && !(e && e[0] == '0') &&
+            m_tiles * (n_total / 256) < n_sm)
+            bn = 128;
+    }
     // transposed convs are epilogue-bound (K is small, 4x cout outputs per
     // input pixel): 128-column tiles leave room for 3 epilogue warpgroups
     if (transposed && bn > 128) bn = 128;
