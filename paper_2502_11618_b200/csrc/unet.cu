@@ -83,6 +83,7 @@ struct ConvParamsP {
     // plan creation) -- the epilogue reads them as constant-bank operands instead
     // of shared-memory loads, which competed with the MMA operand reads in L1
     float pc_scale[32], pc_shift[32];
+    float pc_head[4 * 32];  // k_conv_px2 head: the final 1x1 conv's weights [head_c][32]
     int resident;           // weights resident in smem
     int stages;
     uint32_t a_bytes;       // one A box footprint (1024-aligned)
@@ -1158,11 +1159,11 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
 #pragma unroll
                         for (int j2 = 0; j2 < 4; ++j2) {
                             if (j2 >= p.head_c) break;
-                            const float4 *w4 = reinterpret_cast<const float4 *>(s_hw + j2 * p.cout + n);
+                            const float *wp = p.pc_head + j2 * 32 + n;  // constant bank
 #pragma unroll
                             for (int q4 = 0; q4 < 4; ++q4) {
-                                const float4 w = w4[q4];
-                                const float wv[4] = {w.x, w.y, w.z, w.w};
+                                const float wv[4] = {wp[4 * q4], wp[4 * q4 + 1], wp[4 * q4 + 2],
+                                                     wp[4 * q4 + 3]};
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
                                     hacc2[j2] = fma2(f2(wv[k], wv[k]),
@@ -1563,7 +1564,9 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.ctot = p.c0 + c1;
     p.wts = d_w;
     if (cudaMemcpy(p.pc_scale, d_scale, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(p.pc_shift, d_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaMemcpy(p.pc_shift, d_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        (d_head_w && cudaMemcpy(p.pc_head, d_head_w, (size_t)head_c * 32 * sizeof(float),
+                                cudaMemcpyDeviceToHost) != cudaSuccess)) {
         delete pl;
         return nullptr;
     }
