@@ -1116,6 +1116,13 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
             const int gp = px0 + tp, gy = y0 + ty;
             const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
+            // this lane's first output pixel and the item's store bases (one 64-bit
+            // address computation per item instead of one per 16-channel store)
+            const int64_t pix0 = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
+            __nv_bfloat16 *const ybase = p.y ? p.y + pix0 * 32 : nullptr;
+            __nv_bfloat16 *const pbase =
+                MODE == kPool ? p.pool + (((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp) * 32
+                              : nullptr;
             f32x2 hacc2[4] = {0ull, 0ull, 0ull, 0ull};  // head sums {pixel 2j, 2j+1}
             float vkeep[16];   // pixel 2j's activations for the pair-wise head
             uint32_t keep[8];  // pixel 2j's packed half for the horizontal pool
@@ -1176,10 +1183,11 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                 uint32_t pk[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-                const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp + px;
                 if (valid) {
-                    if (p.y) st_global_v8(p.y + pix * p.cout + n, pk);
+                    // element offsets from the item's per-lane base (cout = 32)
+                    if (p.y) st_global_v8(ybase + px * 32 + n, pk);
                     if (p.y_f32) {
+                        const int64_t pix = pix0 + px;
                         float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + n);
                         dst[0] = make_float4(v[0], v[1], v[2], v[3]);
                         dst[1] = make_float4(v[4], v[5], v[6], v[7]);
@@ -1198,11 +1206,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                             const uint32_t a = hmax2u(keep[i], pk[i]);
                             pk[i] = hmax2u(a, __shfl_xor_sync(0xffffffffu, a, 16));
                         }
-                        if (valid && !(ty & 1)) {
-                            const int64_t pp =
-                                ((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp;
-                            st_global_v8(p.pool + pp * p.cout + n, pk);
-                        }
+                        if (valid && !(ty & 1)) st_global_v8(pbase + n, pk);
                     }
                 }
             };
@@ -1229,11 +1233,21 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                         if (lane == 0) mbar_arrive(tempty + ab);
                     }
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        o0[i] = __float_as_uint(__uint_as_float(o0[i]) +
-                                                __shfl_up_sync(0xffffffffu, __uint_as_float(sr[i]), 1));
-                        o1[i] = __float_as_uint(__uint_as_float(o1[i]) +
-                                                __shfl_down_sync(0xffffffffu, __uint_as_float(sl[i]), 1));
+                    for (int i = 0; i < 16; i += 2) {
+                        // two channels per FADD2 (same IEEE adds as the scalar form)
+                        float a0, a1, b0, b1;
+                        unf2(add2(f2(__uint_as_float(o0[i]), __uint_as_float(o0[i + 1])),
+                                  f2(__shfl_up_sync(0xffffffffu, __uint_as_float(sr[i]), 1),
+                                     __shfl_up_sync(0xffffffffu, __uint_as_float(sr[i + 1]), 1))),
+                             a0, a1);
+                        unf2(add2(f2(__uint_as_float(o1[i]), __uint_as_float(o1[i + 1])),
+                                  f2(__shfl_down_sync(0xffffffffu, __uint_as_float(sl[i]), 1),
+                                     __shfl_down_sync(0xffffffffu, __uint_as_float(sl[i + 1]), 1))),
+                             b0, b1);
+                        o0[i] = __float_as_uint(a0);
+                        o0[i + 1] = __float_as_uint(a1);
+                        o1[i] = __float_as_uint(b0);
+                        o1[i + 1] = __float_as_uint(b1);
                     }
                     float v0[16], v1[16];
                     bnact((int)n, o0, o1, v0, v1, 2);
