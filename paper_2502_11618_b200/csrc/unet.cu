@@ -94,6 +94,12 @@ struct ConvParamsP {
     uint32_t off_const;     // scale[n_total], shift[n_total], head_w (f32)
     uint32_t off_pool;      // (unused: pooling is done with warp shuffles)
     uint32_t off_bar;       // barriers
+    // transposed convs with 32 output channels: each epilogue group stages its
+    // item's 16x32-pixel output tile (32 KB, 128 B swizzle) at off_stage + 32 KB*eg
+    // and writes it with one TMA store (pixel-shuffle lanes otherwise store 32 B
+    // chunks 128 B apart, ~32 L1 wavefronts per store instruction)
+    int stage_store;
+    uint32_t off_stage;
 };
 
 // 128-pixel sub-tiles per work item: more sub-tiles share each streamed
@@ -239,7 +245,8 @@ __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, floa
 template <int BN, int CHUNK, int MODE, int MT_ = default_mt(BN)>
 __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
-    const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
+    const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mY,
+    const ConvParamsP p) {
     using C = CfgP<BN, CHUNK, MT_>;
     constexpr int KYS = MODE == kTransposed ? 1 : 3;
     constexpr int MT = C::kMT;
@@ -457,6 +464,19 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     uint32_t pk[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                    if (MODE == kTransposed && p.stage_store) {
+                        // staging tile row (2*ty + dy)*16 + tx, 128 B per row holding
+                        // [dx][32 channels]; 16 B chunks XOR-swizzled by row (TMA 128 B)
+                        const int dd = n >> 5, dy = dd >> 1, dx = dd & 1;
+                        const int r = (2 * ty + dy) * kTW + tx;
+                        const int c = dx * 4 + ((n & 31) >> 3);
+                        uint8_t *row = smem + p.off_stage + (uint32_t)eg * 32768u + r * 128;
+                        *reinterpret_cast<uint4 *>(row + ((c ^ (r & 7)) << 4)) =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4 *>(row + (((c + 1) ^ (r & 7)) << 4)) =
+                            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        continue;
+                    }
                     if (valid) {
                         int64_t pix;
                         int o = n;
@@ -533,8 +553,22 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     process((s + 1) / ng, (s + 1) % ng, rb);
                 }
             }
+            if (MODE == kTransposed && p.stage_store) {
+                // the group's tile is complete: one TMA store, then the staging
+                // buffer is reusable once the store has read it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                named_bar_sync(1 + eg, 128);
+                if (quarter == 0 && lane == 0) {
+                    tma_store_5d(&mY, smem + p.off_stage + (uint32_t)eg * 32768u, 0, ip.x0, 0,
+                                 ip.y0, ip.img);
+                    tma_store_wait_read();
+                }
+                named_bar_sync(1 + eg, 128);
+            }
         }
     }
+    if (MODE == kTransposed && p.stage_store && warp >= 2 && (warp & 3) == 0 && lane == 0)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     fence_before_sync();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
@@ -1364,13 +1398,29 @@ static bool encode_wts(CUtensorMap *map, const void *base, int ctot, int n_total
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output of a transposed conv with 32 channels viewed as [n][i][dy][j][dx*32+c]
+// (i, j = input pixel; the output pixel is (2i+dy, 2j+dx)), box {64, 16, 2, 8, 1}
+// = one 8x16-input-pixel item's 16x32-pixel output tile, 128 B swizzle.
+static bool encode_up_store(CUtensorMap *map, void *base, int w_in, int h_in, int batch) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t row = (cuuint64_t)2 * w_in * 64;  // one output row, bytes
+    cuuint64_t dims[5] = {64, (cuuint64_t)w_in, 2, (cuuint64_t)h_in, (cuuint64_t)batch};
+    cuuint64_t strides[4] = {128, row, 2 * row, (cuuint64_t)2 * h_in * row};
+    cuuint32_t box[5] = {64, (cuuint32_t)kTW, 2, (cuuint32_t)kTH, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace unet
 }  // namespace ls
 
 using namespace ls::unet;
 
 struct ls_conv_plan {
-    CUtensorMap a0, a1, b;
+    CUtensorMap a0, a1, b, y;
     ConvParamsP p;
     int bn, chunk, grid, mode;
     int mt;    // k_conv_p: 128-pixel sub-tiles per work item
@@ -1413,7 +1463,7 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE, MT>, pl->a0, pl->a1, pl->b,
-                                   pl->p);
+                                   pl->y, pl->p);
 }
 
 template <int CHUNK, int COUT, int MODE>
@@ -1856,6 +1906,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
                                ~size_t(1023);
     size_t res_bytes = 0;
     int stages = 0;
+    // staged TMA stores for 32-channel transposed convs (LS_CONV_UPSTORE=0: off)
+    const char *ue = getenv("LS_CONV_UPSTORE");
+    const bool want_stage = transposed && cout == 32 && d_y && !d_y_f32 && !(ue && ue[0] == '0');
     // Fit >= 3 pipeline stages: first try whole-chunk stages (all kx boxes in
     // one stage), then one kx per stage, then a narrower K chunk, then a
     // narrower column tile.
@@ -1877,7 +1930,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         const size_t nk = (size_t)p.kxs * p.nq;
         p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
         res_bytes = p.resident ? nk * p.b_blk : 0;
-        const size_t fixed = res_bytes + const_bytes + 512;
+        const bool stage_now = want_stage && bn == 128 && mt == 1;
+        const size_t fixed = res_bytes + const_bytes + 512 + (stage_now ? 3 * 32768 + 1024 : 0);
         bool fit = false;
         for (int kxps = p.kxs; kxps >= 1 && !fit; kxps = kxps == 1 ? 0 : 1) {
             const size_t stage_bytes = (size_t)kxps * (p.a_bytes + (p.resident ? 0 : p.b_blk));
@@ -1903,11 +1957,20 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     p.off_b = (uint32_t)(stages * p.stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
+    p.stage_store = want_stage && bn == 128 && mt == 1 ? 1 : 0;
+    if (p.stage_store) {
+        p.off_stage = (p.off_pool + 1023u) & ~1023u;
+        p.off_pool = p.off_stage + 3 * 32768;
+    }
     p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = bn;
     pl->chunk = chunk;
     pl->mode = transposed ? kTransposed : (d_head_w ? kHead : (d_pool ? kPool : kPlain));
+    if (p.stage_store && !encode_up_store(&pl->y, d_y, w, h, batch)) {
+        delete pl;
+        return fail(LS_EINVAL);
+    }
     int n_sm = 148;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
