@@ -229,3 +229,39 @@ def test_full_res_row_bands_identical(monkeypatch):
     b = _run_device(net, x, 8)
     assert net.launches_for(256, 160) == net.launches + 15
     assert np.array_equal(a, b)
+
+
+def test_conv_plan_set_rows_validation():
+    """ls_conv_plan_set_rows rejects bands that do not start on a tile row or
+    leave the layer; a valid band restricts the launch to its rows."""
+    import ctypes
+
+    import torch
+
+    from paper_2502_11618_b200 import _lib
+
+    lib = _lib.load()
+    dev = torch.device("cuda")
+    h, w, c = 64, 64, 32
+    x = torch.randn(1, h, w, c, device=dev).to(torch.bfloat16)
+    wt = (torch.randn(9, c, c, device=dev) * 0.05).to(torch.bfloat16)
+    sc, sh = torch.ones(c, device=dev), torch.zeros(c, device=dev)
+    y = torch.zeros(1, h, w, c, dtype=torch.bfloat16, device=dev)
+    st = ctypes.c_int32(0)
+    pl = lib.ls_conv_plan_create(x.data_ptr(), c, None, 0, 1, h, w, wt.data_ptr(), 3, c, 0,
+                                 sc.data_ptr(), sh.data_ptr(), 1, 0.1, y.data_ptr(), None, None,
+                                 None, None, 0, None, ctypes.byref(st))
+    assert pl, st.value
+    try:
+        t = lib.ls_conv_plan_tile_rows(pl)
+        assert t > 0 and h % t == 0
+        assert lib.ls_conv_plan_set_rows(pl, 1, h) == _lib.LS_EINVAL      # not on a tile row
+        assert lib.ls_conv_plan_set_rows(pl, 0, h + 1) == _lib.LS_EINVAL  # past the layer
+        assert lib.ls_conv_plan_set_rows(pl, t, t) == _lib.LS_EINVAL      # empty band
+        assert lib.ls_conv_plan_set_rows(pl, t, 2 * t) == 0
+        assert lib.ls_conv_plan_launch(pl, _lib.stream_ptr()) == 0
+        torch.cuda.synchronize()
+        nz = (y.float().abs().sum(dim=(0, 2, 3)) > 0).cpu().numpy()
+        assert nz[t:2 * t].all() and not nz[:t].any() and not nz[2 * t:].any()
+    finally:
+        lib.ls_conv_plan_destroy(pl)
