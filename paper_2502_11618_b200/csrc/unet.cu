@@ -186,15 +186,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&h);
 }
 
-__device__ __forceinline__ uint32_t hmax4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162 *>(&a);
-    __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162 *>(&b);
-    __nv_bfloat162 z = *reinterpret_cast<__nv_bfloat162 *>(&c);
-    __nv_bfloat162 w = *reinterpret_cast<__nv_bfloat162 *>(&d);
-    __nv_bfloat162 m = __hmax2(__hmax2(x, y), __hmax2(z, w));
-    return *reinterpret_cast<uint32_t *>(&m);
-}
-
 // Final 1x1 conv partial sums over 16 channels (same sequential FMA order
 // per output as a scalar loop; weights read as float4 broadcasts).
 __device__ __forceinline__ void head_accumulate(const float *s_hw, int cout, int head_c, int n,
@@ -502,10 +493,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     if (MODE == kPool) {
 #pragma unroll
                         for (int i = 0; i < 8; ++i) {
-                            const uint32_t a1 = __shfl_xor_sync(0xffffffffu, pk[i], 1);
-                            const uint32_t a2 = __shfl_xor_sync(0xffffffffu, pk[i], 16);
-                            const uint32_t a3 = __shfl_xor_sync(0xffffffffu, pk[i], 17);
-                            pk[i] = hmax4(pk[i], a1, a2, a3);
+                            // horizontal pair (lane ^ 1), then vertical (lane ^ 16): two
+                            // shuffles per word (max is exact and order-free)
+                            const uint32_t a = hmax2u(pk[i], __shfl_xor_sync(0xffffffffu, pk[i], 1));
+                            pk[i] = hmax2u(a, __shfl_xor_sync(0xffffffffu, a, 16));
                         }
                         if (valid && (lane & 17) == 0) {
                             const int64_t pp =
