@@ -912,8 +912,6 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
     const int S = p.stages;
-    float *sconst = reinterpret_cast<float *>(smem + p.off_const);
-    const float *s_hw = sconst + 2 * p.n_total;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
     uint64_t *empty = full + S;
     uint64_t *tfull = empty + S;
@@ -953,15 +951,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
         __syncwarp();
         tmem_alloc(tslot, C::kTmemCols);
     } else if (warp >= 2) {
+        // (BN constants and head weights are kernel parameters: p.pc_*)
         const int t = threadIdx.x - 64;
         constexpr int kEpiThreads = 128 * kGroups;
-        for (int i = t; i < p.n_total; i += kEpiThreads) {
-            sconst[i] = p.scale[i];
-            sconst[p.n_total + i] = p.shift[i];
-        }
-        if (MODE == kHead)
-            for (int i = t; i < p.head_c * p.cout; i += kEpiThreads)
-                sconst[2 * p.n_total + i] = p.head_w[i];
         if (C8) {
             // per ky 4 KB: [0, 2 KB) the N=64 tile, [2, 3) [0|W0], [3, 4) [W2|0];
             // one thread per (ky, row, 16 B half); W is [tap][32][16] bf16
