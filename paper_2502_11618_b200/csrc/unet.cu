@@ -516,10 +516,6 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     hacc[0] = hacc[1] = hacc[2] = hacc[3] = 0.0f;
                 }
             };
-            auto col = [&](int s) -> uint32_t {
-                const int u = s / ng;
-                return tbase + (uint32_t)(u * BN + (s - u * ng) * 32);
-            };
             // the TMEM buffer goes back to the MMA warp as soon as its last
             // group is in registers
             auto release = [&]() {
@@ -530,19 +526,39 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             // two register buffers: group s+1's tcgen05.ld is in flight while
             // group s is processed
             uint32_t ra[32], rb[32];
-            tmem_ld32_async(col(0), ra);
+            // (sub-tile, column group) of steps s and s+1, advanced without
+            // integer division (ng is a runtime value)
+            auto adv = [&](int &u, int &g) {
+                if (++g == ng) {
+                    g = 0;
+                    ++u;
+                }
+            };
+            int u0 = 0, g0 = 0, u1 = 0, g1 = 0;
+            adv(u1, g1);
+            auto colug = [&](int u, int g) -> uint32_t {
+                return tbase + (uint32_t)(u * BN + g * 32);
+            };
+            tmem_ld32_async(colug(0, 0), ra);
 #pragma unroll 1
             for (int s = 0; s < steps; s += 2) {
+                int u2 = u1, g2 = g1;
+                adv(u2, g2);  // step s + 2
                 tmem_ld_wait(ra);
-                if (s + 1 < steps) tmem_ld32_async(col(s + 1), rb);
+                if (s + 1 < steps) tmem_ld32_async(colug(u1, g1), rb);
                 else release();
-                process(s / ng, s % ng, ra);
+                process(u0, g0, ra);
                 if (s + 1 < steps) {
                     tmem_ld_wait(rb);
-                    if (s + 2 < steps) tmem_ld32_async(col(s + 2), ra);
+                    if (s + 2 < steps) tmem_ld32_async(colug(u2, g2), ra);
                     else release();
-                    process((s + 1) / ng, (s + 1) % ng, rb);
+                    process(u1, g1, rb);
                 }
+                u0 = u2;
+                g0 = g2;
+                u1 = u2;
+                g1 = g2;
+                adv(u1, g1);  // step s + 3
             }
             if (MODE == kTransposed && p.stage_store) {
                 // the group's tile is complete: one TMA store, then the staging
