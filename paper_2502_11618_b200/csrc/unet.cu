@@ -233,6 +233,47 @@ __device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, floa
     return ip;
 }
 
+// Work-item position as a mixed-radix counter (n-tile, tile x, tile y,
+// image), advanced by a fixed stride without divisions: a persistent CTA walks
+// items blockIdx.x, +gridDim.x, ... and each step's position came from three
+// f32-reciprocal divisions (conversion latency on every item).
+struct ItemWalk {
+    int nt, tx, ty, img;
+    int s_nt, s_tx, s_ty, s_img;
+    __device__ static void digits(const ConvParamsP &p, int v, int &a, int &b, int &c, int &d) {
+        a = v % p.n_tiles_n;
+        v /= p.n_tiles_n;
+        b = v % p.tiles_x;
+        v /= p.tiles_x;
+        c = v % p.tiles_y;
+        d = v / p.tiles_y;
+    }
+    __device__ void init(const ConvParamsP &p, int item, int stride) {
+        digits(p, item, nt, tx, ty, img);
+        digits(p, stride, s_nt, s_tx, s_ty, s_img);
+    }
+    __device__ void next(const ConvParamsP &p) {
+        nt += s_nt;
+        int c = nt >= p.n_tiles_n;
+        nt -= c * p.n_tiles_n;
+        tx += s_tx + c;
+        c = tx >= p.tiles_x;
+        tx -= c * p.tiles_x;
+        ty += s_ty + c;
+        c = ty >= p.tiles_y;
+        ty -= c * p.tiles_y;
+        img += s_img + c;
+    }
+    __device__ ItemPos pos(const ConvParamsP &p, int tile_h) const {
+        ItemPos ip;
+        ip.nt = nt;
+        ip.img = img;
+        ip.y0 = (p.ty0 + ty) * tile_h;
+        ip.x0 = tx * kTW;
+        return ip;
+    }
+};
+
 template <int BN, int CHUNK, int MODE, int MT_ = default_mt(BN)>
 __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
@@ -257,9 +298,6 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     uint64_t *tempty = tfull + C::kAcc;
     uint64_t *bres = tempty + C::kAcc;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
-    const float r_nt = 1.0f / (float)p.n_tiles_n;
-    const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
-    const float r_tx = 1.0f / (float)p.tiles_x;
     const int n_kg = p.kxs / p.kxps;  // stages per channel chunk
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -321,8 +359,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int s = 0;
             uint32_t ph = 0;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-                const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
+            ItemWalk walk;
+            walk.init(p, blockIdx.x, gridDim.x);
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
+                const ItemPos ip = walk.pos(p, kTileH);
                 for (int q = 0; q < p.nq; ++q) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
@@ -408,9 +448,11 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
         const f32x2 slope2 = f2(slope, slope);
         const float r_cout = 1.0f / (float)p.cout;
         uint32_t acc = (uint32_t)eg;
+        ItemWalk walk;
+        walk.init(p, blockIdx.x + eg * gridDim.x, C::kEpiGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
-             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
-            const ItemPos ip = item_pos(p, item, r_nt, r_tpi, r_tx, kTileH);
+             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups, walk.next(p)) {
+            const ItemPos ip = walk.pos(p, kTileH);
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
