@@ -671,15 +671,6 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
     uint64_t *tempty = tfull + C::kAcc;
     uint64_t *bres = tempty + C::kAcc;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
-    const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
-    const float r_tx = 1.0f / (float)p.tiles_x;
-    auto pos = [&](int item, int &img, int &x0, int &y0) {
-        img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
-        const int r = item - img * p.tiles_x * p.tiles_y;
-        const int ty = fdiv(r, p.tiles_x, r_tx);
-        y0 = (p.ty0 + ty) * kTH;
-        x0 = (r - ty * p.tiles_x) * kKxCols;
-    };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -733,9 +724,10 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int s = 0;
             uint32_t ph = 0;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-                int img, x0, y0;
-                pos(item, img, x0, y0);
+            ItemWalk walk;
+            walk.init(p, blockIdx.x, gridDim.x);
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
+                const int img = walk.img, x0 = walk.tx * kKxCols, y0 = (p.ty0 + walk.ty) * kTH;
                 for (int q = 0; q < p.nq; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
@@ -790,10 +782,11 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
         const float slope = act_slope(p.act, p.alpha);
         const f32x2 slope2 = f2(slope, slope);
         uint32_t acc = (uint32_t)eg;
+        ItemWalk walk;
+        walk.init(p, blockIdx.x + eg * gridDim.x, C::kEpiGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
-             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups) {
-            int img, x0, y0;
-            pos(item, img, x0, y0);
+             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups, walk.next(p)) {
+            const int img = walk.img, x0 = walk.tx * kKxCols, y0 = (p.ty0 + walk.ty) * kTH;
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
@@ -976,16 +969,6 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
     uint64_t *tempty = tfull + kAcc;
     uint64_t *bres = tempty + kAcc;
     uint32_t *tslot = reinterpret_cast<uint32_t *>(bres + 1);
-    const float r_tpi = 1.0f / (float)(p.tiles_x * p.tiles_y);
-    const float r_tx = 1.0f / (float)p.tiles_x;
-    // item -> (image, first loaded pair column, first row)
-    auto pos = [&](int item, int &img, int &px0, int &y0) {
-        img = fdiv(item, p.tiles_x * p.tiles_y, r_tpi);
-        const int r = item - img * p.tiles_x * p.tiles_y;
-        const int ty = fdiv(r, p.tiles_x, r_tx);
-        y0 = (p.ty0 + ty) * kTH;
-        px0 = (r - ty * p.tiles_x) * kPxCols - 1;
-    };
     const int nsrc = p.nq;  // 1 or 2 sources of 32 channels, one 64-channel pair chunk each
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1072,9 +1055,11 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int s = 0;
             uint32_t ph = 0;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-                int img, px0, y0;
-                pos(item, img, px0, y0);
+            ItemWalk walk;
+            walk.init(p, blockIdx.x, gridDim.x);
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
+                const int img = walk.img, px0 = walk.tx * kPxCols - 1,
+                          y0 = (p.ty0 + walk.ty) * kTH;
                 for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     mbar_wait(empty + s, ph ^ 1u);
                     mbar_expect_tx(full + s, p.a_tx);
@@ -1185,10 +1170,11 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
         const f32x2 slope2 = f2(slope, slope);
         const int wp = p.w >> 1;
         uint32_t ab = (uint32_t)eg % kAcc, aph = ((uint32_t)eg / kAcc) & 1u;
+        ItemWalk walk;
+        walk.init(p, blockIdx.x + eg * gridDim.x, kGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
-             item += kGroups * gridDim.x) {
-            int img, px0, y0;
-            pos(item, img, px0, y0);
+             item += kGroups * gridDim.x, walk.next(p)) {
+            const int img = walk.img, px0 = walk.tx * kPxCols - 1, y0 = (p.ty0 + walk.ty) * kTH;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
