@@ -219,20 +219,6 @@ struct ItemPos {
     int img, y0, x0, nt;
 };
 
-__device__ __forceinline__ ItemPos item_pos(const ConvParamsP &p, int item, float r_nt, float r_tpi,
-                                            float r_tx, int tile_h) {
-    ItemPos ip;
-    const int mt = fdiv(item, p.n_tiles_n, r_nt);
-    ip.nt = item - mt * p.n_tiles_n;
-    const int tpi = p.tiles_x * p.tiles_y;
-    ip.img = fdiv(mt, tpi, r_tpi);
-    const int r = mt - ip.img * tpi;
-    const int ty = fdiv(r, p.tiles_x, r_tx);
-    ip.y0 = (p.ty0 + ty) * tile_h;
-    ip.x0 = (r - ty * p.tiles_x) * kTW;
-    return ip;
-}
-
 // Work-item position as a mixed-radix counter (n-tile, tile x, tile y,
 // image), advanced by a fixed stride without divisions: a persistent CTA walks
 // items blockIdx.x, +gridDim.x, ... and each step's position came from three
