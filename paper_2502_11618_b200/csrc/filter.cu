@@ -13,6 +13,7 @@
 //                       the U-Net input.
 // Each output pixel depends only on a 3x3 coarse window, so every step is a
 // pure stencil; the working set (<= 8 MB at 1080p) stays in L2.
+#include <atomic>
 #include <cuda_bf16.h>
 #include <stdlib.h>
 
@@ -609,12 +610,14 @@ inline bool fused_ok(const Levels &lv) { return lv.L >= 2 && lv.L - 1 <= kFuseMa
 
 // LS_FILTER_FUSED=0 runs one launch per non-final step (A/B measurements).
 inline bool fused_steps_enabled() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_FILTER_FUSED");
-        v = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] == '0') ? 0 : 1;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v == 1;
+    return r == 1;
 }
 
 // Pyramid + steps over an existing sentinel-able depth image.  `lvl` holds

@@ -13,6 +13,8 @@
 // lane owns 4 consecutive points = 48 contiguous bytes (3 x LDG.128) of xyz and
 // 12 bytes (3 x LDG.32) of rgb.  Per-tile occupied-cell spans (built once per
 // scan) let a warp skip a fully culled tile without touching its points.
+#include <atomic>
+#include <mutex>
 #include "ls_common.cuh"
 #include "umma.cuh"
 
@@ -934,6 +936,8 @@ static int ring_blocks_per_sm(const void *fn, size_t smem) {
     };
     static Entry cache[32];
     static int n = 0;
+    static std::mutex mu;  // ABI calls may come from several host threads
+    std::lock_guard<std::mutex> lock(mu);
     for (int i = 0; i < n; ++i)
         if (cache[i].fn == fn) return cache[i].blocks;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1054,12 +1058,14 @@ static bool cache_ok(const ls_camera *cam, const void *d_cache) {
 
 // LS_PASS1_U32=0 keeps 64-bit pixel indices in pass 1 (A/B measurements).
 static bool pass1_u32() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_PASS1_U32");
-        v = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] == '0') ? 0 : 1;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v == 1;
+    return r == 1;
 }
 
 int ls_frame_pass1(const ls_scene *scene, const uint32_t *d_keep_bits, const uint32_t *d_list,

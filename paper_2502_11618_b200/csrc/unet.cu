@@ -25,6 +25,7 @@
 // 8-row swizzle atoms, so only the descriptor start moves.
 // Small weight tensors (<= kResidentMax, one column tile) stay resident in
 // shared memory for the whole CTA; otherwise weight boxes stream with A.
+#include <atomic>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <stdlib.h>
@@ -1366,15 +1367,16 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 static EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
+    // function-local static: initialised once, thread-safe (C++11 magic statics)
+    static const EncodeTiledFn fn = [] {
         void *ptr = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
                 cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(ptr);
-    }
+            return reinterpret_cast<EncodeTiledFn>(ptr);
+        return EncodeTiledFn(nullptr);
+    }();
     return fn;
 }
 
@@ -1447,23 +1449,25 @@ namespace unet {
 
 // LS_UNET_PDL=0 launches the layers fully serialised (A/B measurements).
 static bool pdl_enabled() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_UNET_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] == '0') ? 0 : 1;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v == 1;
+    return r == 1;
 }
 
 template <int BN, int CHUNK, int MODE, int MT>
 static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static int attr_done = 0;  // idempotent: racing threads set the same value
-    if (!attr_done) {
+    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
+    if (!attr_done.load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK, MODE, MT>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
-        attr_done = 1;
+        attr_done.store(1, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
@@ -1481,13 +1485,13 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
 
 template <int CHUNK, int COUT, int MODE>
 static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static int attr_done = 0;
-    if (!attr_done) {
+    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
+    if (!attr_done.load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(k_conv_kx<CHUNK, COUT, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
-        attr_done = 1;
+        attr_done.store(1, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
@@ -1519,13 +1523,13 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
 
 template <int MODE, bool C8, bool KX2 = false>
 static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static int attr_done = 0;
-    if (!attr_done) {
+    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
+    if (!attr_done.load(std::memory_order_acquire)) {
         cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE, C8, KX2>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)(kSmemBudget + 2048));
         if (e != cudaSuccess) return (int)e;
-        attr_done = 1;
+        attr_done.store(1, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
@@ -1557,33 +1561,39 @@ static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
 }
 
 static int kx2_setting() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_CONV_KX2");
-        v = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
+        r = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 2;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v;
+    return r;
 }
 
 // LS_CONV_PX2 (A/B switch, bit mask, default 3): bit 0 = 32-channel
 // single-source layers on k_conv_px2, bit 1 = the 8-channel input layer.
 static int px2_mask() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_CONV_PX2");
-        v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+        r = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v;
+    return r;
 }
 
 // LS_CONV_KX=0 keeps cout = 32 layers on the generic kernel (A/B measurements).
 static bool kx_enabled() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_CONV_KX");
-        v = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] == '0') ? 0 : 1;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v == 1;
+    return r == 1;
 }
 
 template <int BN, int CHUNK, int MT = default_mt(BN)>
@@ -1598,12 +1608,14 @@ static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
 
 // LS_CONV_MT2=0 keeps 256-column tiles at one sub-tile per item (A/B).
 static bool mt2_enabled() {
-    static int v = -1;
-    if (v < 0) {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
         const char *e = getenv("LS_CONV_MT2");
-        v = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] == '0') ? 0 : 1;
+        v.store(r, std::memory_order_relaxed);
     }
-    return v == 1;
+    return r == 1;
 }
 
 static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transposed) {

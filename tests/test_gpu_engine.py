@@ -85,3 +85,49 @@ def test_unfiltered_outputs_same_reconstruction():
         # b's assembly writes the U-Net input directly (no raw f32 rgb) and its
         # final filter step clears the rejected pixels: the same input tensor
         assert bool((a.unet_in == b.unet_in).all())
+
+
+def test_concurrent_host_threads_separate_streams():
+    """The ABI keeps no per-call global state (include/lidarsplat_cuda.h):
+    two host threads, each with its own renderer on its own stream, issue
+    frames concurrently (first-use attribute/occupancy caches raced) and get
+    exactly the frames a single thread renders."""
+    import threading
+
+    import torch
+
+    from paper_2502_11618_b200 import build_grid
+    from paper_2502_11618_b200.engine import FrameRenderer
+    from paper_2502_11618_b200.unet import UNet
+
+    rng = np.random.default_rng(21)
+    cloud = random_cloud(rng, 150_000, extent=10.0, offset=-5.0)
+    views = [random_view(rng, cloud, width=256, height=192) for _ in range(6)]
+    grid = build_grid(cloud, 1.0)
+    # activation buffers belong to a UNet instance: one instance per thread
+    unets = [UNet.from_config("reduced", seed=4) for _ in range(3)]
+    results = {}
+    errors = []
+    start = threading.Barrier(2)
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                r = FrameRenderer(grid, 256, 192, unet=unets[k])
+                start.wait()
+                results[k] = [r.render(v).copy() for v in views[k::2]]
+                r.check_flags()
+        except Exception as e:  # surfaced in the main thread
+            errors.append(e)
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    ref = FrameRenderer(grid, 256, 192, unet=unets[2])
+    for k in range(2):
+        for v, got in zip(views[k::2], results[k]):
+            assert np.array_equal(ref.render(v), got)
