@@ -190,16 +190,17 @@ def run_reference(args):
         return 0
     pos, col, cams = make_scene(args)
     with_unet = args.unet != "none"
-    n = max(1, args.warmup) + max(1, args.steps)
     # bounded sample: the CPU path costs ~seconds per frame; time `steps`
-    # frames after one warm-up frame (capped so the run stays within minutes)
-    n_time = min(args.steps, 6)
-    times, kind, cores = cpu_frames(pos, col, cams, args, 1 + n_time, with_unet)
-    times = times[1:]
+    # frames after `warmup` warm-up frames (both capped so the run stays
+    # within minutes)
+    n_warm = min(max(1, args.warmup), 10)
+    n_time = min(max(1, args.steps), 6)
+    times, kind, cores = cpu_frames(pos, col, cams, args, n_warm + n_time, with_unet)
+    times = times[n_warm:]
     fps = len(times) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": len(times), "warmup": 1,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": n_warm,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded multi-station hall scan)",
