@@ -16,7 +16,10 @@ import numpy as np
 from .errors import LidarSplatError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblidarsplat_cuda.so")
+# LS_DEBUG_BOUNDS=1 selects the checked build (build.py --debug): same kernels
+# with their bounds asserts compiled in.
+LIB_PATH = os.path.join(_HERE, "liblidarsplat_cuda_debug.so"
+                        if os.environ.get("LS_DEBUG_BOUNDS") == "1" else "liblidarsplat_cuda.so")
 
 LS_EINVAL = -22
 LS_TILE_POINTS = 128

@@ -50,30 +50,47 @@ def _deps_mtime() -> float:
     return max(_mtime(p) for p in paths)
 
 
-def build(force: bool = False, verbose: bool = True) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+# Checked build (LS_DEBUG_BOUNDS=1): the index-arithmetic kernels with their
+# LS_ASSERT bounds checks compiled in, linked with the product U-Net object
+# (whose global traffic goes through bounds-checked TMA), into a separate
+# library that `_lib` loads when LS_DEBUG_BOUNDS=1 is set at run time.
+BUILD_DEBUG = os.path.join(PKG, "_build_debug")
+LIB_DEBUG = os.path.join(PKG, "liblidarsplat_cuda_debug.so")
+CHECKED = {"project.cu", "filter.cu", "cull.cu", "grid.cu"}
+
+
+def build(force: bool = False, verbose: bool = True, debug: bool = False) -> str:
+    if debug:
+        build(force, verbose)  # the product objects (unet.o is shared)
+    bdir, lib = (BUILD_DEBUG, LIB_DEBUG) if debug else (BUILD, LIB)
+    os.makedirs(bdir, exist_ok=True)
     objs = []
     dep_t = _deps_mtime()
     procs = []
     for src, flags in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(BUILD, src.replace(".cu", ".o"))
+        if debug and src not in CHECKED:
+            objs.append(os.path.join(BUILD, src.replace(".cu", ".o")))
+            continue
+        o = os.path.join(bdir, src.replace(".cu", ".o"))
         objs.append(o)
         if force or _mtime(o) < max(_mtime(s), dep_t, _mtime(__file__)):
-            cmd = [NVCC, *ARCH, *COMMON, *flags, "-c", s, "-o", o]
+            extra = ["-DLS_DEBUG_BOUNDS"] if debug else []
+            cmd = [NVCC, *ARCH, *COMMON, *flags, *extra, "-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd), flush=True)
             procs.append((src, subprocess.Popen(cmd)))
     for src, p in procs:
         if p.wait() != 0:
             raise RuntimeError(f"nvcc failed on {src}")
-    if procs or not os.path.exists(LIB) or _mtime(LIB) < max(_mtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+    if procs or not os.path.exists(lib) or _mtime(lib) < max(_mtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", lib, *objs]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv)
+    build(force="--force" in sys.argv,
+          debug="--debug" in sys.argv or os.environ.get("LS_DEBUG_BOUNDS") == "1")

@@ -556,11 +556,8 @@ __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *_
         t.x0 = blockIdx.x * kFuseTX;
         t.x1 = min(t.x0 + kFuseTX, (int)lv.w[1]);
         R[nsteps - 1] = t;
-        for (int i = nsteps - 2; i >= 0; --i) {
-            const int lev = L - 1 - i;  // level of R[i]
-            (void)lev;
+        for (int i = nsteps - 2; i >= 0; --i)  // R[i] lies on level L-1-i
             R[i] = coarse_of(R[i + 1], (int)lv.h[L - 1 - i], (int)lv.w[L - 1 - i]);
-        }
     }
     // coarse input of step 1: pooled^L on coarse_of(R[0])
     Rect C = coarse_of(R[0], (int)lv.h[L], (int)lv.w[L]);

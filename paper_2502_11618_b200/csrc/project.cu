@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *
         uint32_t off = 0;
         if (lane == 0) off = atomicAdd(count, (uint32_t)__popc(vote));
         off = __shfl_sync(0xffffffffu, off, 0);
+        LS_ASSERT(off + (uint32_t)__popc(vote) <= (uint32_t)s.n_tiles);
         if (keep_any)
             list[off + __popc(vote & ((1u << lane) - 1u))] = (uint32_t)t | (cull_any ? kMixed : 0u);
     }
@@ -499,8 +500,10 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
         for (int k = 0; k < 4; ++k)
             cur[k] = pix[k] >= 0 ? __ldca(minz + pix[k]) : 0ull;  // stale L1 is safe: min only decreases
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 4; ++k) {
+            LS_ASSERT(pix[k] < c.w * c.h);
             if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(minz + pix[k], key[k]);
+        }
     });
     pdl_trigger();
 }
@@ -546,7 +549,10 @@ __global__ void __launch_bounds__(256) k_frame_pass1_u32(SceneArgs s, ProjCam c,
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const unsigned long long key = (unsigned long long)__double_as_longlong(zc[k]);
-            if (pix[k] != kNoPixel && key < cur[k]) red_min_u64(minz + pix[k], key);
+            if (pix[k] != kNoPixel && key < cur[k]) {
+                LS_ASSERT((int64_t)pix[k] < c.w * c.h);
+                red_min_u64(minz + pix[k], key);
+            }
         }
     });
     pdl_trigger();
@@ -584,9 +590,11 @@ __global__ void __launch_bounds__(256) k_frame_pass2(SceneArgs s, ProjCam c,
         merge_lane_sum(pix, sum);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (pix[k] >= 0)
+            if (pix[k] >= 0) {
+                LS_ASSERT(pix[k] < c.w * c.h);
                 red_add_v4c(acc + 4 * pix[k], (float)sum[k][0], (float)sum[k][1], (float)sum[k][2],
                             (float)sum[k][3]);
+            }
     });
     pdl_trigger();
 }
@@ -650,9 +658,11 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
                 }
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (pix[k] != kNoPixel)
+            if (pix[k] != kNoPixel) {
+                LS_ASSERT((int64_t)pix[k] < c.w * c.h);
                 red_add_v4c(acc + 4 * (size_t)pix[k], (float)sum[k][0], (float)sum[k][1],
                             (float)sum[k][2], (float)sum[k][3]);
+            }
     });
     pdl_trigger();
 }
@@ -773,8 +783,10 @@ __global__ void __launch_bounds__(256, 3) k_frame_pass1_views(
 #pragma unroll
             for (int k = 0; k < 4; ++k) cur[k] = pix[k] >= 0 ? __ldca(mz + pix[k]) : 0ull;
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k) {
+                LS_ASSERT(pix[k] < npix);
                 if (pix[k] >= 0 && key[k] < cur[k]) red_min_u64(mz + pix[k], key[k]);
+            }
         }
     });
     pdl_trigger();
