@@ -32,6 +32,17 @@ def test_checked_library_has_asserts_product_has_none():
     assert _assert_refs(PRODUCT) == 0
 
 
+def _exports(lib):
+    out = subprocess.run(["nm", "-D", "--defined-only", lib], capture_output=True, text=True,
+                         check=True).stdout
+    return {l.split()[-1] for l in out.splitlines() if l.split()[-1].startswith("ls_")}
+
+
+def test_checked_library_exports_the_same_abi():
+    exp = _exports(PRODUCT)
+    assert len(exp) > 20 and _exports(CHECKED) == exp
+
+
 @pytest.mark.gpu
 def test_parity_suites_on_checked_library():
     env = dict(os.environ, LS_DEBUG_BOUNDS="1")
