@@ -1459,16 +1459,36 @@ static bool pdl_enabled() {
     return r == 1;
 }
 
+// The dynamic shared-memory opt-in of a kernel, once per device: function
+// attributes live in each device's context, so a process-wide flag would skip
+// the opt-in for the second GPU a plan runs on.
+template <typename F>
+static int smem_optin(F *fn, std::atomic<uint64_t> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return (int)e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return 0;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kSmemBudget + 2048));
+    if (e != cudaSuccess) return (int)e;
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return 0;
+}
+
+// SM count of the current device (plans are sized for the GPU they run on).
+static int current_sm_count() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+        return 148;
+    return n;
+}
+
 template <int BN, int CHUNK, int MODE, int MT>
 static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
-    if (!attr_done.load(std::memory_order_acquire)) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_p<BN, CHUNK, MODE, MT>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(kSmemBudget + 2048));
-        if (e != cudaSuccess) return (int)e;
-        attr_done.store(1, std::memory_order_release);
-    }
+    static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
+    if (int e = smem_optin(k_conv_p<BN, CHUNK, MODE, MT>, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
     cfg.blockDim = dim3((unsigned)CfgP<BN, CHUNK, MT>::kThreads);
@@ -1485,14 +1505,8 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
 
 template <int CHUNK, int COUT, int MODE>
 static int launch_kx_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
-    if (!attr_done.load(std::memory_order_acquire)) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_kx<CHUNK, COUT, MODE>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(kSmemBudget + 2048));
-        if (e != cudaSuccess) return (int)e;
-        attr_done.store(1, std::memory_order_release);
-    }
+    static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
+    if (int e = smem_optin(k_conv_kx<CHUNK, COUT, MODE>, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
     cfg.blockDim = dim3((unsigned)CfgKx<CHUNK, COUT>::kThreads);
@@ -1523,14 +1537,8 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
 
 template <int MODE, bool C8, bool KX2 = false>
 static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
-    static std::atomic<int> attr_done{0};  // idempotent: racing threads set the same value
-    if (!attr_done.load(std::memory_order_acquire)) {
-        cudaError_t e = cudaFuncSetAttribute(k_conv_px2<MODE, C8, KX2>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)(kSmemBudget + 2048));
-        if (e != cudaSuccess) return (int)e;
-        attr_done.store(1, std::memory_order_release);
-    }
+    static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
+    if (int e = smem_optin(k_conv_px2<MODE, C8, KX2>, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
     cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8>()));
@@ -1622,8 +1630,7 @@ static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transpose
     const int mt = default_mt(bn);
     if (bn == 256 && mt == 1 && !transposed && mt2_enabled()) {
         const int items2 = ((w + kTW - 1) / kTW) * ((h + 2 * kTH - 1) / (2 * kTH)) * batch * n_tiles_n;
-        int n_sm = 148;
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        const int n_sm = current_sm_count();
         if (items2 * 5 >= n_sm * 4) return 2;
     }
     return mt;
@@ -1713,8 +1720,7 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     pl->kind = 2;
     pl->mt = kx2 && !c8 ? 3 : 1;  // 3 marks the KX2 variant
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     pl->full_tiles_y = p.tiles_y;
     // the NHWC tensors read as (W/2) pair pixels of 2*c channels
@@ -1801,8 +1807,7 @@ static ls_conv_plan *plan_kx(const uint16_t *d_x0, int c0_tensor, int c0, const 
     pl->chunk = chunk;
     pl->kind = 1;
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     pl->full_tiles_y = p.tiles_y;
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, kTH + 2);
@@ -1886,8 +1891,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     {
         // small grids (the 1/16-resolution bottleneck): 128-column tiles when
         // 256-column ones leave SMs idle (LS_CONV_SMALLN=0 keeps 256)
-        int n_sm = 148;
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+        const int n_sm = current_sm_count();
         const long long m_tiles = (long long)((w + kTW - 1) / kTW) * ((h + kTH - 1) / kTH) * batch;
         const char *e = getenv("LS_CONV_SMALLN");
         if (bn == 256 && !transposed && !d_head_w && !(e && e[0] == '0') &&
@@ -1996,8 +2000,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         delete pl;
         return fail(LS_EINVAL);
     }
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     pl->full_tiles_y = p.tiles_y;
     const int box_h = kTH * mt + 2 * p.pad;
@@ -2049,8 +2052,7 @@ int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) 
     p.tiles_y = t1 - t0;
     p.n_tiles_m = p.tiles_x * p.tiles_y * p.batch;
     p.n_items = p.n_tiles_m * p.n_tiles_n;
-    int n_sm = 148;
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     return 0;
 }

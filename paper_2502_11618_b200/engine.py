@@ -16,7 +16,8 @@ import numpy as np
 from . import _lib
 from .filtering import FilterParams
 from .frame import FrameRGBDA, RenderParams
-from .render import FrameBuffers, ViewBuffers, project_scene, project_scene_views
+from .render import (FrameBuffers, ViewBuffers, _exact_frame, project_scene,
+                     project_scene_views)
 
 # kernel launches per frame of the fused path: cull, work-list counter reset,
 # tile work list, pass 1, pass 2, assemble+pyramid, the filter steps (+ U-Net
@@ -45,11 +46,18 @@ class FrameRenderer:
         import torch
 
         self.device = _lib.device()
+        self.grid = grid
         self.scene = grid.scene()
+        # this renderer's own cull bits / work list / pass-1 cache: renderers
+        # sharing a grid (one per host thread / stream) never share scratch
+        self.scratch = self.scene.new_scratch()
         self.width, self.height = int(width), int(height)
         self.rp = render_params or RenderParams()
         self.fp = filter_params or FilterParams()
         self.bufs = FrameBuffers(width, height, self.device)
+        # accumulator-bound flag of each output slot (render / render_stream
+        # read it back with the slot's result and reset it)
+        self.slot_flags = torch.zeros(2, dtype=torch.int32, device=self.device)
         h, w, dev = self.height, self.width, self.device
         self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.fdepth = torch.empty((h, w), dtype=torch.float32, device=dev)
@@ -76,6 +84,7 @@ class FrameRenderer:
         self._copy_stream = None
         self._copy_done = [None, None]
         self._ring = None
+        self._exact_bufs = None
 
     @property
     def launches_per_frame(self) -> int:
@@ -113,41 +122,82 @@ class FrameRenderer:
                       filter_params=self.fp, filtered=filtered,
                       unet_in=None if self.unet is None else self.unet_in[0],
                       pyramid=self.pyramid, stage_events=events,
-                      raw=self.unet is None or self.filtered_outputs)
+                      raw=self.unet is None or self.filtered_outputs, scratch=self.scratch,
+                      flags=self.slot_flags[slot:slot + 1])
         if self.unet is not None:
             self.unet.forward(self.unet_in, outs[0])
         if events is not None:
             events[-1].record()
 
     def check_flags(self) -> None:
-        if int(self.bufs.flags.item()):
-            raise RuntimeError("f32 accumulator bound exceeded; use project_points() for "
-                               "the exact path")
+        """Raise if a frame ``enqueue``d since the last check kept more points
+        in one pixel than the f32 accumulators hold exactly (> 65,793); its
+        device result is then not exact.  ``render`` / ``render_stream``
+        check every frame themselves and recompute such frames exactly."""
+        bad = int(self.slot_flags.max().item())
+        self.slot_flags.zero_()
+        if bad:
+            raise RuntimeError("f32 accumulator bound exceeded; use render() / "
+                               "project_points() for the exact path")
 
-    def render(self, camera):
-        """Public end-to-end call: one frame, result copied to pinned host
-        memory.  Returns the reconstructed RGB (H,W,3) f32 when a U-Net is
-        attached, else the filtered FrameRGBDA."""
+    def _exact_outputs(self, camera):
+        """Recompute ``camera``'s frame on the exact u64 x 4 accumulator path
+        (the reference-interface twins) and return device result tensors shaped
+        like ``_outputs`` (U-Net rgb, or the filtered frame).  Stream-ordered on
+        the current stream after every frame enqueued before it."""
         import torch
 
-        self.enqueue(camera)
+        from .filtering import depth_filter
+
+        raw = _exact_frame(None, self.grid, camera, self.rp)
+        filt = depth_filter(raw, self.fp)
+        dev = self.device
+        if self.unet is None:
+            return tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                         for a in (filt.rgb, filt.depth, filt.alpha))
+        if self.filtered_outputs:
+            for dst, a in zip((self.frgb, self.fdepth, self.falpha),
+                              (filt.rgb, filt.depth, filt.alpha)):
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        if self._exact_bufs is None:
+            self._exact_bufs = (torch.zeros_like(self.unet_in), torch.empty_like(self.rgb_out))
+        x, out = self._exact_bufs
+        planes = torch.from_numpy(np.ascontiguousarray(np.concatenate(
+            [filt.rgb.transpose(2, 0, 1), filt.depth[None],
+             filt.alpha[None].astype(np.float32)]), dtype=np.float32)).to(dev)
+        _lib.check(_lib.load().ls_unet_pack_rgbda(
+            planes.data_ptr(), self.height, self.width, self.unet.in_pad,
+            float(self.unet.cfg.depthZNear), x.data_ptr(), _lib.stream_ptr()),
+            "unet_pack_rgbda")
+        self.unet.forward(x, out)
+        return (out,)
+
+    def render(self, camera):
+        """Public end-to-end call: one frame, result copied to host memory.
+        Returns the reconstructed RGB (H,W,3) f32 when a U-Net is attached,
+        else the filtered FrameRGBDA.  The arrays are fresh copies (the
+        reference returns new arrays too).  A frame in which one pixel kept
+        more than 65,793 points is recomputed on the exact u64 path, so the
+        result is always the reference's."""
+        import torch
+
         if self._pinned is None:
-            if self.unet is not None:
-                self._pinned = (torch.empty((self.height, self.width, 3), dtype=torch.float32,
-                                            pin_memory=True),)
-            else:
-                self._pinned = (torch.empty_like(self.frgb, device="cpu", pin_memory=True),
-                                torch.empty_like(self.fdepth, device="cpu", pin_memory=True),
-                                torch.empty_like(self.falpha, device="cpu", pin_memory=True))
-        if self.unet is not None:
-            self._pinned[0].copy_(self.rgb_out[0, : self.height], non_blocking=True)
-        else:
-            for dst, src in zip(self._pinned, (self.frgb, self.fdepth, self.falpha)):
-                dst.copy_(src, non_blocking=True)
+            self._pinned = self._host_set() + (torch.zeros(1, dtype=torch.int32,
+                                                           pin_memory=True),)
+        *host, hflag = self._pinned
+        self.slot_flags[0:1].zero_()
+        self.enqueue(camera, slot=0)
+        hflag.copy_(self.slot_flags[0:1], non_blocking=True)
+        for dst, src in zip(host, self._outputs(0)):
+            dst.copy_(src[0, : self.height] if src.dim() == 4 else src, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if int(hflag[0]):
+            self.slot_flags[0:1].zero_()
+            for dst, src in zip(host, self._exact_outputs(camera)):
+                dst.copy_(src[0, : self.height] if src.dim() == 4 else src)
         if self.unet is not None:
-            return self._pinned[0].numpy()
-        return FrameRGBDA(*(t.numpy() for t in self._pinned))
+            return host[0].numpy().copy()
+        return FrameRGBDA(*(t.numpy().copy() for t in host))
 
     def _host_set(self):
         """One set of pinned host buffers matching the device results."""
@@ -178,12 +228,16 @@ class FrameRenderer:
         copy = self._copy_stream
         if self._ring is None or len(self._ring) != depth + 2:  # pinned once, reused
             self._ring = [self._host_set() for _ in range(depth + 2)]
-        ring = self._ring
+            self._ring_flags = torch.zeros(depth + 2, dtype=torch.int32, pin_memory=True)
+        ring, rflags = self._ring, self._ring_flags
         pending = collections.deque()
 
         def result(item):
-            done, hs = item
+            done, hs, cam = item
             done.synchronize()
+            if int(rflags[hs]):  # accumulator bound hit: recompute exactly
+                for dst, src in zip(ring[hs], self._exact_outputs(cam)):
+                    dst.copy_(src[0, : self.height] if src.dim() == 4 else src)
             if self.unet is not None:
                 return ring[hs][0].numpy()
             return FrameRGBDA(*(t.numpy() for t in ring[hs]))
@@ -199,10 +253,14 @@ class FrameRenderer:
             with torch.cuda.stream(copy):
                 for dst, src in zip(ring[hs], self._outputs(slot)):
                     dst.copy_(src[0, : self.height] if src.dim() == 4 else src, non_blocking=True)
+                # the slot's flag goes out with its result and is reset before
+                # the slot is reused (comp waits for this copy-out)
+                rflags[hs:hs + 1].copy_(self.slot_flags[slot:slot + 1], non_blocking=True)
+                self.slot_flags[slot:slot + 1].zero_()
                 done = torch.cuda.Event()
                 done.record(copy)
             self._copy_done[slot] = done
-            pending.append((done, hs))
+            pending.append((done, hs, cam))
             if len(pending) > depth:
                 yield result(pending.popleft())
         while pending:
@@ -229,7 +287,9 @@ class ViewBatchRenderer:
         import torch
 
         self.device = _lib.device()
+        self.grid = grid
         self.scene = grid.scene()
+        self.scratch = self.scene.new_scratch()
         self.width, self.height, self.n_views = int(width), int(height), int(n_views)
         self.rp = render_params or RenderParams()
         self.fp = filter_params or FilterParams()
@@ -268,24 +328,42 @@ class ViewBatchRenderer:
         project_scene_views(self.scene, cameras, self.rp.zbuffer_epsilon_rel, self.vbufs,
                             cull=True, filter_params=self.fp, filtered=filtered,
                             unet_in=self.unet_in, pyramid=self.pyramid,
-                            raw=self.unet is None)
+                            raw=self.unet is None, scratch=self.scratch)
         if self.unet is not None:
             self.unet.forward(self.unet_in, self.rgb_out)
 
     def check_flags(self) -> None:
-        if int(self.vbufs.flags.max().item()):
-            raise RuntimeError("f32 accumulator bound exceeded; use project_points() for "
-                               "the exact path")
+        """Raise if a batch ``enqueue``d since the last check had a view whose
+        pixel kept more points than the f32 accumulators hold exactly."""
+        bad = int(self.vbufs.flags.max().item())
+        self.vbufs.flags.zero_()
+        if bad:
+            raise RuntimeError("f32 accumulator bound exceeded; use render() / "
+                               "project_points() for the exact path")
 
     def render(self, cameras):
         """Public call: one batch, results on the host.  Returns a list of
-        (H,W,3) f32 U-Net outputs, or of filtered FrameRGBDA frames."""
-        import torch
-
+        (H,W,3) f32 U-Net outputs, or of filtered FrameRGBDA frames.  A view
+        in which one pixel kept more than 65,793 points is recomputed on the
+        exact u64 path (same result as rendering it with FrameRenderer)."""
+        cameras = list(cameras)
+        self.vbufs.flags.zero_()
         self.enqueue(cameras)
+        flags = self.vbufs.flags.cpu().numpy()
         if self.unet is not None:
             out = self.rgb_out[:, : self.height].cpu().numpy()
-            return [out[v] for v in range(self.n_views)]
-        rgb, depth, alpha = (t.cpu().numpy() for t in (self.frgb, self.fdepth, self.falpha))
-        torch.cuda.current_stream().synchronize()
-        return [FrameRGBDA(rgb[v], depth[v], alpha[v]) for v in range(self.n_views)]
+            res = [out[v] for v in range(self.n_views)]
+        else:
+            rgb, depth, alpha = (t.cpu().numpy() for t in (self.frgb, self.fdepth, self.falpha))
+            res = [FrameRGBDA(rgb[v], depth[v], alpha[v]) for v in range(self.n_views)]
+        if flags.any():
+            self.vbufs.flags.zero_()
+            exact = FrameRenderer(self.grid, self.width, self.height, self.rp, self.fp,
+                                  unet=self.unet, filtered_outputs=self.unet is None)
+            for v in np.flatnonzero(flags):
+                outs = exact._exact_outputs(cameras[v])
+                if self.unet is not None:
+                    res[v] = outs[0][0, : self.height].cpu().numpy()
+                else:
+                    res[v] = FrameRGBDA(*(t.cpu().numpy() for t in outs))
+        return res

@@ -13,6 +13,7 @@ ascending cell ids as the reference.
 from __future__ import annotations
 
 import os
+import threading
 
 import numpy as np
 
@@ -57,9 +58,13 @@ class DeviceScene:
             _lib.check(lib.ls_scene_tile_index(self.occ_offsets.data_ptr(), n_occ,
                                                self.n_points, self.tile_c0.data_ptr(),
                                                self.tile_c1.data_ptr(), st), "scene_tile_index")
-        self.keep_bits = torch.empty(max((n_occ + 31) // 32, 1), dtype=torch.int32, device=dev)
-        self.tile_list = torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev)
-        self.tile_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.words = max((n_occ + 31) // 32, 1)
+        # per-frame scratch of one-shot synchronous calls (project_points,
+        # cull_cells ...), serialised by ``lock``; renderers own their own
+        # FrameScratch so concurrent frames never share cull bits, work
+        # lists or pass-1 caches
+        self.lock = threading.RLock()
+        self.scratch = FrameScratch(self)
         s = _lib.LsScene()
         s.d_positions, s.d_colors, s.n_points = (positions.data_ptr(), colors.data_ptr(),
                                                  self.n_points)
@@ -72,37 +77,69 @@ class DeviceScene:
         s.dims[:] = [int(v) for v in dims]
         self.struct = s
 
-    def cull_bits(self, planes: np.ndarray, out=None):
-        """Warp-ballot cull of every occupied cell; returns the u32 keep bits."""
-        bits = self.keep_bits if out is None else out
+    # the default scratch's buffers (tests and one-shot calls)
+    keep_bits = property(lambda self: self.scratch.keep_bits)
+    tile_list = property(lambda self: self.scratch.tile_list)
+    tile_count = property(lambda self: self.scratch.tile_count)
+
+    def new_scratch(self) -> "FrameScratch":
+        return FrameScratch(self)
+
+    def cull_bits(self, planes: np.ndarray, out=None, scratch=None):
+        """Warp-ballot cull of every occupied cell; returns the u32 keep bits
+        (written to ``out``, else to the scratch's keep bits)."""
+        bits = (scratch or self.scratch).keep_bits if out is None else out
         pl = np.ascontiguousarray(planes, np.float64)
         _lib.check(_lib.load().ls_cull(self.struct, pl.ctypes.data, CULL_SLACK, bits.data_ptr(),
                                        _lib.stream_ptr()), "cull")
         return bits
 
+    def view_buffers(self, scratch=None):
+        return (scratch or self.scratch).view_buffers()
+
+    def worklist(self, scratch=None):
+        """Frame work list of non-culled tiles from the scratch's keep bits."""
+        sc = scratch or self.scratch
+        _lib.check(_lib.load().ls_tile_worklist(self.struct, sc.keep_bits.data_ptr(),
+                                                sc.tile_list.data_ptr(),
+                                                sc.tile_count.data_ptr(), _lib.stream_ptr()),
+                   "tile_worklist")
+        return sc.tile_list, sc.tile_count
+
+
+class FrameScratch:
+    """Per-frame device scratch of one frame stream over a DeviceScene: keep
+    bits, tile work list + counter, the pass-1 -> pass-2 caches and the
+    multi-view cull buffers.  Frames enqueued on different streams must use
+    different scratch objects (each renderer owns one)."""
+
+    def __init__(self, scene: DeviceScene):
+        import torch
+
+        dev = scene.positions.device
+        self.scene_n_tiles = scene.n_tiles
+        self.words = scene.words
+        self.keep_bits = torch.empty(scene.words, dtype=torch.int32, device=dev)
+        self.tile_list = torch.empty(max(scene.n_tiles, 1), dtype=torch.int32, device=dev)
+        self.tile_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.frame_cache = None   # lazily sized by render.frame_cache
+        self.views_cache = None   # lazily sized by render.views_cache
+        self._view_bufs = None
+
     def view_buffers(self):
         """Multi-view cull/work-list buffers (allocated on first use):
         (LS_MAX_VIEWS, words) keep bits, work list, per-entry view status, count."""
-        vb = getattr(self, "_view_bufs", None)
-        if vb is None:
+        if self._view_bufs is None:
             import torch
 
             dev = self.keep_bits.device
-            words = int(self.keep_bits.shape[0])
-            vb = (torch.empty((_lib.LS_MAX_VIEWS, words), dtype=torch.int32, device=dev),
-                  torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev),
-                  torch.empty(max(self.n_tiles, 1), dtype=torch.int32, device=dev),
-                  torch.zeros(1, dtype=torch.int32, device=dev))
-            self._view_bufs = vb
-        return vb
-
-    def worklist(self):
-        """Frame work list of non-culled tiles from the current keep bits."""
-        _lib.check(_lib.load().ls_tile_worklist(self.struct, self.keep_bits.data_ptr(),
-                                                self.tile_list.data_ptr(),
-                                                self.tile_count.data_ptr(), _lib.stream_ptr()),
-                   "tile_worklist")
-        return self.tile_list, self.tile_count
+            n = max(self.scene_n_tiles, 1)
+            self._view_bufs = (
+                torch.empty((_lib.LS_MAX_VIEWS, self.words), dtype=torch.int32, device=dev),
+                torch.empty(n, dtype=torch.int32, device=dev),
+                torch.empty(n, dtype=torch.int32, device=dev),
+                torch.zeros(1, dtype=torch.int32, device=dev))
+        return self._view_bufs
 
 
 class UniformGrid:

@@ -15,6 +15,8 @@ backend-protocol twins).  Both return frames identical to the reference's.
 from __future__ import annotations
 
 import os
+import threading
+import types
 from dataclasses import dataclass
 
 import numpy as np
@@ -120,44 +122,48 @@ class FrameBuffers:
 USE_FRAME_CACHE = os.environ.get("LS_FRAME_CACHE", "1") != "0"
 
 
-def frame_cache(scene, camera: CameraModel):
-    """The scene's pass-1 -> pass-2 cache (allocated once per scene), or None
-    when disabled or the frame is too large for u32 pixel slots."""
+def frame_cache(scene, camera: CameraModel, scratch=None):
+    """The scratch's pass-1 -> pass-2 cache (allocated once per FrameScratch;
+    default: the scene's own), or None when disabled or the frame is too large
+    for u32 pixel slots."""
     if not USE_FRAME_CACHE or camera.width * camera.height >= 0xFFFFFFFF:
         return None
-    c = getattr(scene, "_frame_cache", None)
-    if c is None:
+    sc = scratch or scene.scratch
+    if sc.frame_cache is None:
         import torch
 
         nbytes = int(_lib.load().ls_frame_cache_bytes(scene.struct))
-        c = torch.empty(max(nbytes // 4, 4), dtype=torch.int32, device=_lib.device())
-        scene._frame_cache = c
-    return c
+        sc.frame_cache = torch.empty(max(nbytes // 4, 4), dtype=torch.int32,
+                                     device=_lib.device())
+    return sc.frame_cache
 
 
 def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs: FrameBuffers,
                   cull: bool = True, filter_params=None, filtered=None, keep=None,
                   unet_in=None, unet_znear: float = 0.1, pyramid=None,
-                  stage_events=None, raw: bool = True) -> None:
+                  stage_events=None, raw: bool = True, scratch=None, flags=None) -> None:
     """Enqueue one fused frame on the current stream (no host sync):
     cull -> pass 1 -> pass 2 -> assemble (+ filter / U-Net input).
     ``stage_events``: optional CUDA events recorded after cull, pass 1,
     pass 2 and assemble/filter.  ``raw=False`` (U-Net-only frames: a filter,
     ``unet_in`` and no filtered outputs) skips the raw f32 rgb / alpha frame:
     the assembly writes the U-Net input directly (bufs.rgb / bufs.alpha are
-    then not updated)."""
+    then not updated).  ``scratch``: the FrameScratch of this frame stream
+    (default: the scene's shared one -- hold ``scene.lock`` until the frame
+    has completed).  ``flags``: int32 word the assembly ORs 1 into when a
+    pixel's f32 accumulator reached 2^24 (default ``bufs.flags``)."""
     lib = _lib.load()
     st = _lib.stream_ptr()
     cam = _lib.make_camera(camera)
     ev = stage_events or [None] * 4
     bits = lst = cnt = None
     if cull:
-        bits = scene.cull_bits(extract_frustum(camera).planes).data_ptr()
-        tl, tc = scene.worklist()
+        bits = scene.cull_bits(extract_frustum(camera).planes, scratch=scratch).data_ptr()
+        tl, tc = scene.worklist(scratch)
         lst, cnt = tl.data_ptr(), tc.data_ptr()
     if ev[0] is not None:
         ev[0].record()
-    cache = _lib.ptr(frame_cache(scene, camera))
+    cache = _lib.ptr(frame_cache(scene, camera, scratch))
     _lib.check(lib.ls_frame_pass1(scene.struct, bits, lst, cnt, cam, bufs.minz.data_ptr(), cache,
                                   st), "frame_pass1")
     if ev[1] is not None:
@@ -179,7 +185,9 @@ def project_scene(scene: DeviceScene, camera: CameraModel, eps_rel: float, bufs:
                                    bufs.height, fp, raw_rgb, bufs.depth.data_ptr(),
                                    raw_alpha, frgb, fdepth, falpha, _lib.ptr(keep),
                                    _lib.ptr(unet_in), unet_h, unet_c, float(unet_znear),
-                                   _lib.ptr(pyramid), bufs.flags.data_ptr(), st), "frame_finish")
+                                   _lib.ptr(pyramid),
+                                   (bufs.flags if flags is None else flags).data_ptr(), st),
+               "frame_finish")
     if ev[3] is not None:
         ev[3].record()
 
@@ -205,25 +213,25 @@ class ViewBuffers:
         self.flags = torch.zeros(k, dtype=torch.int32, device=device)
 
 
-def views_cache(scene, camera: CameraModel, n_views: int):
-    """The scene's multi-view pass-1 -> pass-2 cache (n_views KB per warp tile,
-    grown on demand), or None when disabled / the frame is too large."""
+def views_cache(scene, camera: CameraModel, n_views: int, scratch=None):
+    """The scratch's multi-view pass-1 -> pass-2 cache (n_views KB per warp
+    tile, grown on demand), or None when disabled / the frame is too large."""
     if not USE_FRAME_CACHE or camera.width * camera.height >= 0xFFFFFFFF:
         return None
+    sc = scratch or scene.scratch
     nbytes = int(_lib.load().ls_frame_views_cache_bytes(scene.struct, n_views))
-    c = getattr(scene, "_views_cache", None)
-    if c is None or c.numel() * 4 < nbytes:
+    if sc.views_cache is None or sc.views_cache.numel() * 4 < nbytes:
         import torch
 
-        c = torch.empty(max(nbytes // 4, 4), dtype=torch.int32, device=_lib.device())
-        scene._views_cache = c
-    return c
+        sc.views_cache = torch.empty(max(nbytes // 4, 4), dtype=torch.int32,
+                                     device=_lib.device())
+    return sc.views_cache
 
 
 def project_scene_views(scene: DeviceScene, cameras, eps_rel: float, vb: ViewBuffers,
                         cull: bool = True, filter_params=None, filtered=None, keep=None,
                         unet_in=None, unet_znear: float = 0.1, pyramid=None,
-                        raw: bool = True) -> None:
+                        raw: bool = True, scratch=None) -> None:
     """Enqueue a batch of views on the current stream (no host sync): per-view
     culls, ONE multi-view pass pair over the scan (each tile read once for all
     views), then one assemble/filter per view.  ``filtered`` / ``keep`` /
@@ -241,12 +249,12 @@ def project_scene_views(scene: DeviceScene, cameras, eps_rel: float, vb: ViewBuf
     bits = lst = status = cnt = None
     stride = 0
     if cull:
-        vbits, lst_t, status_t, cnt_t = scene.view_buffers()
+        vbits, lst_t, status_t, cnt_t = scene.view_buffers(scratch)
         for v, cam in enumerate(cameras):
             scene.cull_bits(extract_frustum(cam).planes, out=vbits[v])
         bits, stride = vbits.data_ptr(), int(vbits.shape[1])
         lst, status, cnt = lst_t.data_ptr(), status_t.data_ptr(), cnt_t.data_ptr()
-    cache = _lib.ptr(views_cache(scene, cameras[0], k))
+    cache = _lib.ptr(views_cache(scene, cameras[0], k, scratch))
     _lib.check(lib.ls_frame_project_views(scene.struct, bits, stride, lst, status, cnt, cams, k,
                                           float(eps_rel), vb.minz.data_ptr(), cache,
                                           vb.accum.data_ptr(), st), "frame_project_views")
@@ -292,8 +300,9 @@ def project_points_views(cloud: PointCloud, grid: UniformGrid | None, cameras,
             out += [FrameRGBDA.empty(c.width, c.height) for c in batch]
             continue
         vb = ViewBuffers(batch[0].width, batch[0].height, len(batch), dev)
-        project_scene_views(scene, batch, params.zbuffer_epsilon_rel, vb, cull=cull)
-        flags = vb.flags.cpu().numpy()
+        with scene.lock:  # the scene's shared scratch, until the batch completed
+            project_scene_views(scene, batch, params.zbuffer_epsilon_rel, vb, cull=cull)
+            flags = vb.flags.cpu().numpy()
         rgb, depth, alpha = vb.rgb.cpu().numpy(), vb.depth.cpu().numpy(), vb.alpha.cpu().numpy()
         for v, cam in enumerate(batch):
             if flags[v] & 1:
@@ -327,11 +336,12 @@ def project_points(cloud: PointCloud, grid: UniformGrid | None, camera: CameraMo
         scene = grid.scene()
         cull = True
     bufs = FrameBuffers(camera.width, camera.height, dev)
-    if scene.n_points:
-        project_scene(scene, camera, params.zbuffer_epsilon_rel, bufs, cull=cull)
-    else:
+    if not scene.n_points:
         return FrameRGBDA.empty(camera.width, camera.height)
-    if int(bufs.flags.item()) & 1:
+    with scene.lock:  # the scene's shared scratch, until the frame completed
+        project_scene(scene, camera, params.zbuffer_epsilon_rel, bufs, cull=cull)
+        flagged = int(bufs.flags.item()) & 1
+    if flagged:
         return _exact_frame(cloud, grid, camera, params)
     return FrameRGBDA(bufs.rgb.cpu().numpy(), bufs.depth.cpu().numpy(),
                       bufs.alpha.cpu().numpy())
@@ -348,6 +358,9 @@ class _BruteScene:
         s.cell_size = 1.0
         self.struct = s
         self._keep = (pos, col)
+        self.lock = threading.RLock()
+        # no cull bits / work list: only the pass-1 -> pass-2 caches
+        self.scratch = types.SimpleNamespace(frame_cache=None, views_cache=None)
 
 
 def _brute_scene(cloud, pos, col):

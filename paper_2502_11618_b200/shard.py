@@ -100,6 +100,7 @@ class ShardedRenderer:
         offs = shard_cell_offsets(grid._device_field("cell_offsets", np.int64), start, end)
         self.scene = DeviceScene(full.positions[start:end], full.colors[start:end], offs,
                                  grid.origin, grid.cell_size, grid.dims)
+        self.scratch = self.scene.scratch  # the shard scene is this renderer's own
         self.sets = [FrameBuffers(width, height, self.device) for _ in range(2)]
         self.bufs = self.sets[0]
         h, w, dev = self.height, self.width, self.device

@@ -112,3 +112,116 @@ def make_leaky_pair(cloud: PointCloud, grid: UniformGrid, gt_image: np.ndarray,
                     pair_id: str = "", backend=None) -> TrainingPair:
     """Leaky recipe (R:synth.py:96-115)."""
     return _pair(grid, gt_image, gt_camera, fparams, rparams, pair_id, True, cloud)
+
+
+# ------------------------------------------------ augmentation + datasets ---
+# Host-side, seeded and pure (R:synth.py:37-58, 118-253): the per-group colour
+# jitter is a numpy Generator draw sequence, restated in the reference's order
+# so a seed gives the reference's bytes.
+
+_LATTICE_STEP = 32  # px between value-noise lattice nodes
+
+
+@dataclass(frozen=True)
+class AugmentParams:
+    """Grouped brightness/contrast jitter; identity when the ranges collapse."""
+
+    brightness_delta_range: tuple = (-0.15, 0.15)
+    contrast_scale_range: tuple = (0.8, 1.25)
+    group_count_range: tuple = (2, 4)
+    seed: int = 0
+
+    def __post_init__(self):
+        for name in ("brightness_delta_range", "contrast_scale_range", "group_count_range"):
+            lo, hi = getattr(self, name)
+            if lo > hi:
+                raise ValueError(f"{name} is not ordered: {(lo, hi)}")
+        if self.group_count_range[0] < 1:
+            raise ValueError("group count must be >= 1")
+        if not 0 <= self.seed < 2**64:
+            raise ValueError("seed must fit in 64 unsigned bits")
+
+
+def _group_field(height: int, width: int, k: int, rng) -> np.ndarray:
+    """Per-pixel group id in [0, k): a bilinear value-noise field quantised."""
+    lat = rng.random((height // _LATTICE_STEP + 2, width // _LATTICE_STEP + 2))
+    ys = np.arange(height) / _LATTICE_STEP
+    xs = np.arange(width) / _LATTICE_STEP
+    iy, ix = ys.astype(np.int64), xs.astype(np.int64)
+    fy, fx = (ys - iy)[:, None], (xs - ix)[None, :]
+    r0, r1 = iy[:, None], iy[:, None] + 1
+    c0, c1 = ix[None, :], ix[None, :] + 1
+    f = (lat[r0, c0] * (1 - fy) * (1 - fx) + lat[r0, c1] * (1 - fy) * fx
+         + lat[r1, c0] * fy * (1 - fx) + lat[r1, c1] * fy * fx)
+    lo, hi = f.min(), f.max()
+    f = (f - lo) / (hi - lo) if hi > lo else np.zeros_like(f)
+    return np.minimum((f * k).astype(np.int64), k - 1)
+
+
+def augment_brightness_contrast(image: np.ndarray, alpha: np.ndarray, params: AugmentParams,
+                                seed_sequence=None) -> np.ndarray:
+    """out = clamp(c * (in - 0.5) + 0.5 + b, 0, 1) on filled pixels, with (c, b)
+    drawn per spatial group; empty pixels are untouched.  Same seed, same bytes."""
+    rng = np.random.default_rng(np.random.SeedSequence(params.seed)
+                                if seed_sequence is None else seed_sequence)
+    h, w = image.shape[:2]
+    k = int(rng.integers(params.group_count_range[0], params.group_count_range[1] + 1))
+    groups = _group_field(h, w, k, rng)
+    contrast = rng.uniform(*params.contrast_scale_range, size=k)
+    brightness = rng.uniform(*params.brightness_delta_range, size=k)
+    shift = (0.5 - 0.5 * contrast) + brightness  # identity draw (1, 0) stays exact
+    c = contrast[groups][:, :, None].astype(np.float32)
+    s = shift[groups][:, :, None].astype(np.float32)
+    out = np.clip(c * image + s, 0.0, 1.0)
+    return np.where(alpha.astype(bool)[:, :, None], out, image).astype(np.float32)
+
+
+def generate_dataset(cloud: PointCloud, scene_frames, out_dir, mode: str,
+                     augment: AugmentParams, fparams: FilterParams, rparams: RenderParams,
+                     backend=None, grid: UniformGrid | None = None, progress=None):
+    """One training pair per (id, CameraModel, gt_image) plus a manifest
+    (R:synth.py:184-253).  Pairs come from the device recipes above; the
+    augmentation and file writing are host-side.  Deterministic."""
+    from pathlib import Path
+
+    from .grid import build_grid
+    from .io.dataset import DatasetManifest, pair_paths, save_manifest
+    from .io.frames import save_image_rgb, write_frame
+
+    if mode not in ("filtered", "leaky"):
+        raise DatasetError(f"unknown mode {mode!r}")
+    frames = list(scene_frames)
+    if not frames:
+        raise DatasetError("scene has no frames")
+    dims = {(cam.width, cam.height) for _, cam, _ in frames}
+    if len(dims) != 1:
+        raise DatasetError(f"frames disagree on dimensions: {sorted(dims)}")
+    out = Path(out_dir)
+    (out / "pairs").mkdir(parents=True, exist_ok=True)
+    if grid is None:
+        grid = build_grid(cloud, rparams.cell_size, backend)
+    make = make_filtered_pair if mode == "filtered" else make_leaky_pair
+    ids = []
+    for i, (pid, cam, gt) in enumerate(frames):
+        pair = make(cloud, grid, gt, cam, fparams, rparams, pair_id=str(pid), backend=backend)
+        child = np.random.SeedSequence(entropy=augment.seed, spawn_key=(i,))
+        rgb = augment_brightness_contrast(pair.input.rgb, pair.input.alpha, augment, child)
+        paths = pair_paths(out, pair.id)
+        write_frame(FrameRGBDA(rgb=rgb, depth=pair.input.depth, alpha=pair.input.alpha),
+                    paths["input"])
+        save_image_rgb(paths["target"], pair.target)
+        ids.append(pair.id)
+        if progress:
+            progress(i + 1, len(frames), pair.id)
+    manifest = DatasetManifest(
+        mode=mode, ids=tuple(ids), seed=augment.seed,
+        params={"filter": {"levels_n": fparams.levels_n,
+                           "filter_strength": fparams.filter_strength,
+                           "edge_threshold": fparams.edge_threshold},
+                "render": {"zbuffer_epsilon_rel": rparams.zbuffer_epsilon_rel,
+                           "cell_size": rparams.cell_size},
+                "augment": {"brightness_delta_range": list(augment.brightness_delta_range),
+                            "contrast_scale_range": list(augment.contrast_scale_range),
+                            "group_count_range": list(augment.group_count_range)}})
+    save_manifest(out, manifest)
+    return manifest

@@ -364,7 +364,9 @@ class UNet:
     def _buffers(self, batch, h, w):
         import torch
 
-        key = (batch, h, w)
+        # activations are per stream: forwards enqueued on different streams
+        # (one renderer per host thread) never share intermediate buffers
+        key = (_lib.stream_ptr(), batch, h, w)
         if key in self._bufs:
             return self._bufs[key]
         cfg, dev = self.cfg, self.device
@@ -383,7 +385,7 @@ class UNet:
         batch, h, w, cin = x.shape
         if h % self.divisor or w % self.divisor:
             raise ValueError(f"input {w}x{h} not divisible by 2^depth = {self.divisor}")
-        key = (x.data_ptr(), out.data_ptr(), batch, h, w)
+        key = (_lib.stream_ptr(), x.data_ptr(), out.data_ptr(), batch, h, w)
         if key in self._plans:
             return self._plans[key]
         cfg, L, lib = self.cfg, self.layers, _lib.load()
