@@ -2,18 +2,23 @@
 """Per-frame rendering pipeline throughput on B200 (BASELINE.json metric:
 "frames/sec at 1920x1080 for N-M-point scan (1/2/4/8 B200); Gpoints/s projected").
 
-Workload (default) = BASELINE configs[1]: synthetic 20M-point multi-station
-scan (paper_2502_11618_b200.scenes.multi_station_hall, seeded), 1920x1080,
-full pipeline per frame: grid-cell culling -> two-pass projection -> assemble
--> depth-filter pyramid (L=4) -> U-Net input -> U-Net (when --unet != none).
-A step = one frame of a seeded camera path inside the hall.  The scan
-(300 MB) is larger than L2, so no extra L2 flush is needed between frames.
+Workload (default) = the north-star target, BASELINE configs[2] at N=1..8:
+synthetic 100M-point multi-station scan (paper_2502_11618_b200.scenes.
+multi_station_hall, seeded), 1920x1080, full pipeline per frame: grid-cell
+culling -> two-pass projection -> assemble -> depth-filter pyramid (L=4) ->
+U-Net input -> U-Net (when --unet != none).  A step = one frame of a seeded
+camera path inside the hall.  The scan (1.5 GB) is larger than L2, so no
+extra L2 flush is needed between frames.  (--points 20000000 = configs[1].)
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
-N > 1 (torchrun): the scan is sharded by cell-major point ranges; per frame
-every rank projects its shard, minz is all-reduced (MIN), pass 2 accumulators
-are reduced (SUM) to the frame's root (round-robin), which finishes the frame.
+N > 1: without a torchrun environment the command re-executes itself as N
+ranks (torch.distributed.run, NCCL).  Default mode "sharded" (configs[2]):
+the scan is sharded by cell-major point ranges; per frame every rank
+projects its shard, minz is all-reduced (MIN), pass 2 accumulators are
+reduced (SUM) to the frame's root (round-robin), which filters and runs the
+U-Net on a side stream.  Frame-parallel replicas are measured too and
+reported under "replicas".
 
 --impl reference times the reference's own CPU kernels (oracle/_ref, compiled
 from /root/reference's _native.pyx; else the C port) driven by the oracle's
@@ -45,23 +50,59 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--points", type=int, default=20_000_000)
+    ap.add_argument("--points", type=int, default=100_000_000)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--unet", choices=["default", "reduced", "none"], default="default")
-    ap.add_argument("--cpu-frames", type=int, default=2, help="cpu_baseline sample frames")
+    ap.add_argument("--cpu-frames", type=int, default=2, help="cpu_baseline / parity frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--views", type=int, default=8, help="camera poses cycled")
-    ap.add_argument("--mode", choices=["replicas", "sharded"], default="replicas",
-                    help="N>1: frame-parallel replicas of the scan (default; each rank renders "
-                         "whole frames) or point-sharded frames (min/sum merges, root-side "
-                         "filter + U-Net)")
+    ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
+                    help="N>1: point-sharded frames (default; min/sum merges, root-side "
+                         "filter + U-Net, round-robin roots) or frame-parallel replicas; the "
+                         "other mode is measured too and reported as a sub-object")
     return ap.parse_args()
 
 
 def workload_name(args):
     return (f"multi-station hall scan {args.points / 1e6:g}M points, {args.width}x{args.height}, "
             "cull+project+filter" + ("" if args.unet == "none" else f"+unet({args.unet})"))
+
+
+def bench_config(args, world):
+    """The config dict both arms print (identical, so the driver can match them)."""
+    par = "single" if world == 1 else (f"point-shard{world}" if args.mode == "sharded"
+                                      else f"frame-replicas{world}")
+    return {"workload": workload_name(args), "points": args.points, "width": args.width,
+            "height": args.height, "views": args.views, "parallelism": par,
+            "l2": "inputs larger than L2 (scan 15 B/pt)"}
+
+
+def relaunch(args):
+    """--gpus N > 1 without a torchrun environment: re-exec this command as N
+    ranks (torch.distributed.run, one process per GPU, 127.0.0.1); with one,
+    WORLD_SIZE must equal --gpus.  Returns an exit code, or None to go on."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus <= 1:
+            return None
+        import socket
+        import subprocess
+
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd, env=env)
+    if int(ws) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    return None
 
 
 # ------------------------------------------------------------------ clocks ---
@@ -138,10 +179,12 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ scene ----
-def make_scene(args):
+def make_scene(args, device=None):
+    """Seeded scan + camera path.  The generator is host/device-independent
+    (scenes.py), so ``device="cuda"`` (fast) and the CPU give the same bytes."""
     from paper_2502_11618_b200.scenes import hall_cameras, multi_station_hall
 
-    pos, col, _ = multi_station_hall(args.points)
+    pos, col, _ = multi_station_hall(args.points, device=device)
     cams = hall_cameras(args.views, args.width, args.height)
     return pos, col, cams
 
@@ -156,10 +199,23 @@ def measured_peaks():
     return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def traffic_profile():
+    """DRAM bytes of the dominant kernels from the committed ncu capture of
+    this configuration (bench.py cannot profile itself)."""
+    for name in ("r02_traffic.json", "r01_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path):
+            with open(path) as fh:
+                return json.load(fh), f"profiles/{name}"
+    return {}, None
+
+
 # --------------------------------------------------------------- CPU legs ---
-def cpu_frames(pos, col, cams, args, n_frames, with_unet):
+def cpu_frames(pos, col, cams, args, n_frames, with_unet, keep_frames=False):
     """Reference CPU pipeline (oracle/_ref kernels, else the C port) on the
-    host cores; returns (seconds per frame list, kind, cores, note)."""
+    host cores.  Returns (seconds per frame, kind, cores, frames) where frames
+    holds (filtered rgb, depth, alpha, U-Net rgb) per frame when
+    ``keep_frames``."""
     from oracle import oracle as O
 
     kind = "reference" if O.reference_module_path() else "port"
@@ -172,20 +228,22 @@ def cpu_frames(pos, col, cams, args, n_frames, with_unet):
         from oracle.unet_ref import CpuUNet
 
         unet_ref = CpuUNet(args.unet, threads=workers)
-    times = []
+    times, frames = [], []
     for i in range(n_frames):
         cam = cams[i % len(cams)]
         t0 = time.perf_counter()
         rgb, depth, alpha, keep = O.render_frame(grid, cam, 0.01, 4, 0.1, 0.25, kern, port,
                                                  workers=workers)
-        if unet_ref is not None:
-            unet_ref.reconstruct(rgb, depth, alpha)
+        out = unet_ref.reconstruct(rgb, depth, alpha) if unet_ref is not None else None
         times.append(time.perf_counter() - t0)
-    return times, kind, workers
+        if keep_frames:
+            frames.append((rgb, depth, alpha, out))
+    return times, kind, workers, frames
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     pos, col, cams = make_scene(args)
@@ -193,19 +251,18 @@ def run_reference(args):
     # bounded sample: the CPU path costs ~seconds per frame; time `steps`
     # frames after `warmup` warm-up frames (both capped so the run stays
     # within minutes)
-    n_warm = min(max(1, args.warmup), 10)
-    n_time = min(max(1, args.steps), 6)
-    times, kind, cores = cpu_frames(pos, col, cams, args, n_warm + n_time, with_unet)
+    n_warm = min(max(1, args.warmup), 3)
+    n_time = min(max(1, args.steps), 4)
+    times, kind, cores, _ = cpu_frames(pos, col, cams, args, n_warm + n_time, with_unet)
     times = times[n_warm:]
     fps = len(times) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": fps, "unit": "frames/s",
-        "n_gpus": args.gpus, "steps": len(times), "warmup": n_warm,
+        "n_gpus": world, "steps": len(times), "warmup": n_warm,
         "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded multi-station hall scan)",
-        "config": {"workload": workload_name(args), "points": args.points,
-                   "width": args.width, "height": args.height},
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": cores, "kind": kind,
                          "sample": f"{len(times)} full frames (cull+project+filter"
                                    f"{'+unet f32 torch-cpu' if with_unet else ''})"},
@@ -217,6 +274,86 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU arm ---
+def _max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _timed(world, run, clocks=None):
+    """Barrier + sync, CUDA events around ``run()``, sync + barrier; returns
+    the max over ranks of the device time (ms)."""
+    import torch
+
+    if clocks is not None:
+        clocks.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    run()
+    t1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop() if clocks is not None else None
+    return _max_over_ranks(t0.elapsed_time(t1), world), clk
+
+
+def run_sharded(args, grid, unet, cams, rank, world):
+    """Point-sharded frames: every rank projects its shard of every frame, MIN
+    / SUM merges over NCCL, the frame's root (round-robin) filters and runs
+    the U-Net on its side stream.  Returns (ms total, clocks, e2e, renderer)."""
+    import torch
+
+    from paper_2502_11618_b200.shard import ShardedRenderer
+
+    r = ShardedRenderer(grid, args.width, args.height, rank, world, unet=unet)
+    main = torch.cuda.current_stream()
+
+    def frames(k0, n):
+        for i in range(n):
+            r.enqueue(cams[(k0 + i) % len(cams)])
+        main.wait_stream(r.side)
+
+    frames(0, args.warmup)
+    torch.cuda.synchronize()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    total_ms, clk = _timed(world, lambda: frames(args.warmup, args.steps), ClockSampler(local))
+    r.check_flags()
+    # e2e: each frame's root copies its result to pinned host memory
+    host = torch.empty((args.height, args.width, 3), dtype=torch.float32, pin_memory=True)
+    copies = []
+
+    def e2e_frames():
+        for i in range(args.steps):
+            root = r.frame_index % world
+            r.enqueue(cams[(args.warmup + i) % len(cams)])
+            if root == rank:
+                with torch.cuda.stream(r.side):
+                    src = r.rgb_out[0, : args.height] if unet is not None else r.frgb
+                    host.copy_(src, non_blocking=True)
+                    copies.append(1)
+        r.side.synchronize()
+        torch.cuda.synchronize()
+
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    e2e_frames()
+    e_s = _max_over_ranks(time.perf_counter() - t0, world)
+    e2e = {"value": args.steps / e_s, "unit": "frames/s",
+           "api": "ShardedRenderer.enqueue + root-side copy of each frame's result",
+           "h2d_bytes_per_step": 320, "d2h_bytes_per_step": args.height * args.width * 12}
+    return total_ms, clk, e2e, r
+
+
 def run_b200(args):
     import torch
 
@@ -230,8 +367,9 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # comm init lines (nranks) in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    pos, col, cams = make_scene(args)
+    pos, col, cams = make_scene(args, device="cuda")
     cloud = PointCloud(pos, col)
     grid = build_grid(cloud, 1.0)
     torch.cuda.synchronize()
@@ -240,176 +378,128 @@ def run_b200(args):
         from paper_2502_11618_b200.unet import UNet
 
         unet = UNet.from_config(args.unet, seed=7, device=torch.device("cuda", local))
-    sharded = world > 1 and args.mode == "sharded"
-    if sharded:
-        from paper_2502_11618_b200.shard import ShardedRenderer
-
-        renderer = ShardedRenderer(grid, args.width, args.height, rank, world, unet=unet)
-    else:
-        # with a U-Net the f32 filtered frame is an intermediate the U-Net does
-        # not read (it reads the packed bf16 input of the same filter kernel)
-        renderer = FrameRenderer(grid, args.width, args.height, unet=unet,
-                                 filtered_outputs=unet is None)
-    # replicas: rank r renders its own frames (views offset by rank)
-    view0 = 0 if sharded else rank * args.steps
-    # candidate counts per view (algorithmic bytes of the projection passes)
-    n_cand = []
+    n_cand = []  # candidate points per view (algorithmic bytes of the passes)
     for cam in cams:
-        cells = cull_cells(grid, extract_frustum(cam))
-        s, e = grid.cell_ranges(cells)
+        s, e = grid.cell_ranges(cull_cells(grid, extract_frustum(cam)))
         n_cand.append(int((e - s).sum()))
-
+    hbm, bf16, bf16s, peak_kind = measured_peaks()
+    traffic, traffic_src = traffic_profile()
+    sharded = world > 1 and args.mode == "sharded"
+    line = {"metric": METRIC, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+            "dtype": "f64" if unet is None else "f64+bf16",
+            "data": "synthetic (seeded multi-station hall scan, random-init U-Net weights)",
+            "config": bench_config(args, world)}
+    if sharded:
+        total_ms, clk, e2e, sr = run_sharded(args, grid, unet, cams, rank, world)
+        fps = args.steps * 1e3 / total_ms
+        cand = [n_cand[(args.warmup + i) % len(cams)] for i in range(args.steps)]
+        line.update({"value": fps, "ms_per_step": total_ms / args.steps,
+                     "gpoints_per_s": float(np.mean(cand)) * fps / 1e9,
+                     "candidates_mean": float(np.mean(cand)), "stages_ms": None,
+                     "roofline": None, "clocks": clk, "e2e": e2e,
+                     "gpu_launches": sr.launches_per_frame * args.steps,
+                     "merge_bytes_per_frame": {
+                         "all_reduce_min_minz": args.width * args.height * 8,
+                         "reduce_sum_accum": args.width * args.height * 16}})
+        del sr
+    # single-GPU frames, or frame-parallel replicas (every rank renders its
+    # own frames of the whole scan; no data-path collective)
+    renderer = FrameRenderer(grid, args.width, args.height, unet=unet,
+                             filtered_outputs=unet is None)
+    view0 = rank * args.steps
     for i in range(args.warmup):
         renderer.enqueue(cams[(view0 + i) % len(cams)])
     torch.cuda.synchronize()
-    # ---- device-timed region (inputs resident in HBM) ----
     # The K timed frames run uninstrumented: an event recorded between two
-    # kernels ends the programmatic-dependent-launch overlap at that boundary
-    # (~3% of a frame).  The per-stage breakdown used for the rooflines comes
-    # from a second, instrumented pass over the same frames afterwards.
-    clocks = ClockSampler(local)
-    clocks.start()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record()
-    for i in range(args.steps):
-        renderer.enqueue(cams[(view0 + args.warmup + i) % len(cams)])
-    if sharded:
-        torch.cuda.current_stream().wait_stream(renderer.side)
-    t_end.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    clk = clocks.stop()
-    total_ms = t_start.elapsed_time(t_end)
-    if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    # instrumented pass (stage events), not part of the timed value
+    # kernels ends the programmatic-dependent-launch overlap at that boundary.
+    # The per-stage breakdown used for the rooflines comes from a second,
+    # instrumented pass over the same frames afterwards.
+    seq = [cams[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
+
+    def frames():
+        for cam in seq:
+            renderer.enqueue(cam)
+
+    rep_ms, rep_clk = _timed(world, frames, None if sharded else ClockSampler(local))
     nst = 5
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)]
-           for _ in range(args.steps)]
-    if not sharded:  # root-side work is on a side stream: no per-stage events
-        for i in range(args.steps):
-            evs[i][0].record()
-            renderer.enqueue(cams[(view0 + args.warmup + i) % len(cams)], events=evs[i][1:])
-        torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in seq]
+    for cam, e in zip(seq, evs):
+        e[0].record()
+        renderer.enqueue(cam, events=e[1:])
+    torch.cuda.synchronize()
     renderer.check_flags()
     stage = {k: [] for k in ("cull", "pass1", "pass2", "filter", "unet")}
-    for e in ([] if sharded else evs):
-        stage["cull"].append(e[0].elapsed_time(e[1]))
-        stage["pass1"].append(e[1].elapsed_time(e[2]))
-        stage["pass2"].append(e[2].elapsed_time(e[3]))
-        stage["filter"].append(e[3].elapsed_time(e[4]))
-        stage["unet"].append(e[4].elapsed_time(e[5]))
-    # frames completed by the whole job in the timed region
-    frames = args.steps * (1 if sharded or world == 1 else world)
-    ms = total_ms / args.steps
-    fps = frames * 1e3 / total_ms
+    for e in evs:
+        for j, k in enumerate(stage):
+            stage[k].append(e[j].elapsed_time(e[j + 1]))
+    stages_ms = {k: float(np.mean(v)) for k, v in stage.items()}
+    ft = np.array([e[0].elapsed_time(e[nst]) for e in evs])
     cand = [n_cand[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
     mean_cand = float(np.mean(cand))
-    hbm, bf16, bf16s, peak_kind = measured_peaks()
-    proj_gbs = 0.0
-    if not sharded:
-        t_proj = np.array(stage["pass1"]) + np.array(stage["pass2"])
-        proj_bytes = 27.0 * np.array(cand)  # 12 B pass 1 + 15 B pass 2 per candidate
-        proj_gbs = float(np.mean(proj_bytes / (t_proj * 1e-3)) / 1e9)
-    stages_ms = {k: float(np.mean(v)) for k, v in stage.items()} if not sharded else None
-    # per-frame device time, mean / p50 / p95 as the reference's run_bench
-    # reports them (R:bench.py:61-67), from the instrumented pass
-    frame_ms = None
-    if not sharded and args.steps > 0:
-        ft = np.array([e[0].elapsed_time(e[5]) for e in evs])
-        frame_ms = {"mean": float(ft.mean()), "p50": float(np.percentile(ft, 50)),
-                    "p95": float(np.percentile(ft, 95)),
-                    "source": "instrumented pass, CUDA events around each frame"}
-    roofline = None if sharded else {
-                "kernel": "projection (k_frame_pass1 + k_frame_pass2)", "bound": "hbm",
-                "achieved": proj_gbs, "peak": hbm, "unit": "GB/s", "frac": proj_gbs / hbm,
-                "traffic": None, "peak_kind": peak_kind,
-                "algorithmic": "27 B per candidate point"}
-    # DRAM traffic of the same kernels from a committed ncu capture (bench.py
-    # cannot profile itself): profiles/r01_traffic.json
-    traffic = {}
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh)
-    if roofline is not None and "projection_dram_bytes_per_candidate" in traffic:
-        roofline["traffic"] = traffic["projection_dram_bytes_per_candidate"] * mean_cand
-        roofline["traffic_source"] = "profiles/r01_traffic.json (ncu dram bytes per candidate x candidates)"
-    if unet is not None and not sharded:
+    rep_fps = world * args.steps * 1e3 / rep_ms
+    # projection roofline: 27 B per candidate (pass 1 xyz, pass 2
+    # xyz + rgb) + 17 B per output pixel, over pass 1 + pass 2 time
+    npx = args.width * args.height
+    t_proj = np.array(stage["pass1"]) + np.array(stage["pass2"])
+    proj_bytes = 27.0 * np.array(cand) + 17.0 * npx
+    proj_gbs = float(np.mean(proj_bytes / (t_proj * 1e-3)) / 1e9)
+    roof_proj = {"kernel": "projection (k_frame_pass1 + k_frame_pass2)", "bound": "hbm",
+                 "achieved": proj_gbs, "peak": hbm, "unit": "GB/s", "frac": proj_gbs / hbm,
+                 "traffic": None, "peak_kind": peak_kind,
+                 "algorithmic": "27 B per candidate point + 17 B per output pixel"}
+    if "projection_dram_bytes_per_candidate" in traffic:
+        roof_proj["traffic"] = traffic["projection_dram_bytes_per_candidate"] * mean_cand
+        roof_proj["traffic_source"] = (f"{traffic_src} (ncu dram bytes of pass 1 + pass 2 per "
+                                       "candidate, same config, x this run's candidates)")
+    roofline = roof_proj
+    if unet is not None:
         flops = unet.flops(args.width, renderer.unet_in.shape[1])
         tflops = flops / (stages_ms["unet"] * 1e-3) / 1e12
-        roofline_unet = {"kernel": "U-Net (tcgen05 implicit-GEMM convs)", "bound": "tensor",
-                         "achieved": tflops, "peak": bf16, "unit": "TFLOP/s",
-                         "frac": tflops / bf16,
-                         "traffic": traffic.get("unet_dram_bytes_per_frame"),
-                         "traffic_source": "profiles/r01_traffic.json (ncu dram bytes, 22 launches)",
-                         "peak_kind": peak_kind,
-                         "algorithmic": f"{flops / 1e12:.4f} TFLOP per frame"}
+        roof_unet = {"kernel": "U-Net (tcgen05 implicit-GEMM convs)", "bound": "tensor",
+                     "achieved": tflops, "peak": bf16, "unit": "TFLOP/s", "frac": tflops / bf16,
+                     "traffic": traffic.get("unet_dram_bytes_per_frame"),
+                     "traffic_source": f"{traffic_src} (ncu dram bytes, all U-Net launches)",
+                     "peak_kind": peak_kind,
+                     "algorithmic": f"{flops / 1e12:.4f} TFLOP per frame"}
         if stages_ms["unet"] > stages_ms["pass1"] + stages_ms["pass2"]:
-            roofline, roofline_unet = roofline_unet, roofline
-        roofline["other"] = roofline_unet
+            roofline, roof_unet = roof_unet, roof_proj
+        roofline["other"] = roof_unet
     # ---- end to end through the public API (host result every frame) ----
-    # FrameRenderer.render_stream: every frame's camera goes in from the host
-    # and its full result comes back to pinned host memory; the copy-out of
-    # frame i overlaps the compute of frame i+1 (wall clock over K frames)
-    e2e = None
-    if not sharded:
-        for _ in renderer.render_stream([cams[(view0 + i) % len(cams)] for i in range(3)]):
-            pass
-        torch.cuda.synchronize()
-        seq = [cams[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
-        if world > 1:
-            torch.distributed.barrier()
-        e0 = time.perf_counter()
-        n_out = 0
-        for _ in renderer.render_stream(seq):
-            n_out += 1
-        e_s = time.perf_counter() - e0
-        if world > 1:  # slowest rank; every rank delivered n_out frames
-            t = torch.tensor([e_s], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_s = float(t.item())
-        e2e = {"value": n_out * world / e_s, "unit": "frames/s",
+    for _ in renderer.render_stream(seq[:3]):
+        pass
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    n_out = sum(1 for _ in renderer.render_stream(seq))
+    e_s = _max_over_ranks(time.perf_counter() - t0, world)
+    rep_e2e = {"value": n_out * world / e_s, "unit": "frames/s",
                "api": "FrameRenderer.render_stream",
                "h2d_bytes_per_step": 320,  # camera struct + 6 frustum planes (kernel params)
                "d2h_bytes_per_step": renderer.d2h_bytes}
-    line = {
-        "metric": METRIC, "value": fps, "unit": "frames/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "strong" if sharded else "weak",
-        "vs_baseline": None,
-        "dtype": "f64" if unet is None else "f64+bf16",
-        "data": "synthetic (seeded multi-station hall scan, random-init U-Net weights)",
-        "config": {"workload": workload_name(args), "points": args.points,
-                   "width": args.width, "height": args.height, "views": len(cams),
-                   "parallelism": (f"point-shard{world}" if sharded else
-                                   f"frame-replicas{world}" if world > 1 else "single"),
-                   "l2": "inputs larger than L2 (scan 15 B/pt)"},
-        "gpoints_per_s": mean_cand * fps / 1e9,
-        "candidates_mean": mean_cand,
-        "stages_ms": stages_ms,
-        "frame_ms": frame_ms,
-        "stages_note": "per-stage CUDA events from a second, instrumented pass over the same "
-                       "frames; value / ms_per_step come from the uninstrumented timed pass",
-        "roofline": roofline,
-        "clocks": clk,
-        "e2e": e2e,
-        "gpu_launches": renderer.launches_per_frame * args.steps,
-    }
+    rep = {"value": rep_fps, "ms_per_step": rep_ms / args.steps,
+           "gpoints_per_s": mean_cand * rep_fps / 1e9, "candidates_mean": mean_cand,
+           "stages_ms": stages_ms,
+           "frame_ms": {"mean": float(ft.mean()), "p50": float(np.percentile(ft, 50)),
+                        "p95": float(np.percentile(ft, 95)),
+                        "source": "instrumented pass, CUDA events around each frame"},
+           "stages_note": "per-stage CUDA events from a second, instrumented pass over the "
+                          "same frames; value / ms_per_step come from the uninstrumented "
+                          "timed pass",
+           "roofline": roofline, "e2e": rep_e2e,
+           "gpu_launches": renderer.launches_per_frame * args.steps}
+    if sharded:
+        rep.update({"scaling": "weak", "parallelism": f"frame-replicas{world}"})
+        line["replicas"] = rep
+        line["projection_roofline_single_rank"] = roofline
+    else:
+        line.update(rep)
+        line["clocks"] = rep_clk
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times, kind, cores = cpu_frames(pos, col, cams, args, 1 + args.cpu_frames,
-                                        args.unet != "none")
-        times = times[1:]
-        line["cpu_baseline"] = {"value": len(times) / sum(times), "unit": "frames/s",
-                                "cores": cores, "kind": kind,
-                                "sample": f"{len(times)} full frames of the same workload"}
+        line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(
+            args, pos, col, cams, grid, unet)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -417,9 +507,46 @@ def run_b200(args):
     return 0
 
 
+def cpu_baseline_and_parity(args, pos, col, cams, grid, unet):
+    """The reference CPU pipeline on this box's cores (cpu_baseline), and the
+    same frames compared with the device path: filtered RGBDA bit-exact, U-Net
+    output max-abs / PSNR against the CPU f32 U-Net of the reference frame."""
+    from paper_2502_11618_b200.engine import FrameRenderer
+    from paper_2502_11618_b200.metrics import psnr
+
+    n = 1 + args.cpu_frames
+    times, kind, cores, frames = cpu_frames(pos, col, cams, args, n, unet is not None,
+                                            keep_frames=True)
+    times = times[1:]
+    base = {"value": len(times) / sum(times), "unit": "frames/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} full frames of the same workload"}
+    chk = FrameRenderer(grid, args.width, args.height, unet=unet, filtered_outputs=True)
+    exact, errs, ps = True, [], []
+    for i, (rgb, depth, alpha, out) in enumerate(frames):
+        got = chk.render(cams[i % len(cams)])
+        exact &= (np.array_equal(chk.frgb.cpu().numpy(), rgb)
+                  and np.array_equal(chk.fdepth.cpu().numpy(), depth)
+                  and np.array_equal(chk.falpha.cpu().numpy(), alpha))
+        if out is not None:
+            errs.append(float(np.abs(got - out).max()))
+            ps.append(psnr(got, out))
+    par = {"frames": len(frames), "bit_exact": bool(exact),
+           "compared": "filtered RGBDA vs the reference kernels' frame (oracle/_ref)"}
+    if errs:
+        par.update({"unet_max_abs": max(errs), "unet_psnr_db": min(ps),
+                    "unet_tolerance": {"max_abs": 1.5e-2, "psnr_db": 40.0},
+                    "unet_within_tolerance": max(errs) <= 1.5e-2 and min(ps) >= 40.0,
+                    "unet_reference": "f32 torch-CPU restatement of FE:model/unet.ts "
+                                      "(unpinned: no node/tfjs here)"})
+    return base, par
+
+
 def main():
     faulthandler.enable()
     args = parse()
+    rc = relaunch(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

@@ -283,6 +283,24 @@ int ls_depth_filter_frame(const float *d_rgb, const float *d_depth, const uint8_
                           float *d_frgb, float *d_fdepth, uint8_t *d_falpha, uint8_t *d_keep,
                           float *d_pyramid, void *stream);
 
+/* A filter_strength sweep over one device frame (BASELINE configs[3]; the
+ * reference runs filtering.py:134-147 once per strength): the strength-
+ * independent min-pool pyramid is built once, then every strength's
+ * non-final steps run in one launch and every strength's final step in
+ * another.  Strength k's keep mask / filtered frame land at plane k of
+ * d_keep (K,H,W) / d_frgb (K,H,W,3) / d_fdepth (K,H,W) / d_falpha (K,H,W)
+ * (any may be NULL; rgb/alpha inputs are needed only for the filtered
+ * frame), each bit-identical to ls_depth_filter_frame at that strength.
+ * 1 <= n_strengths <= 16, 1 <= levels_n <= 5; d_work holds
+ * ls_filter_sweep_floats(height, width, levels_n, n_strengths) floats. */
+int64_t ls_filter_sweep_floats(int64_t height, int64_t width, int32_t levels_n,
+                               int32_t n_strengths);
+int ls_depth_filter_sweep(const float *d_rgb, const float *d_depth, const uint8_t *d_alpha,
+                          int64_t height, int64_t width, int32_t levels_n,
+                          double edge_threshold, const double *h_strengths, int32_t n_strengths,
+                          float *d_frgb, float *d_fdepth, uint8_t *d_falpha, uint8_t *d_keep,
+                          float *d_work, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

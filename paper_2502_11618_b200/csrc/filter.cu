@@ -541,9 +541,20 @@ struct SmemImg {
     }
 };
 
+// filter_strength per blockIdx.z: a sweep over strengths runs every strength's
+// steps in one launch (the pyramid they read is strength-independent); output
+// z lands at out + z * out_stride.
+constexpr int kMaxSweep = 16;
+struct FsSweep {
+    double fs[kMaxSweep];
+    int64_t out_stride;
+};
+
 __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *__restrict__ out,
-                                                             double fs, double et) {
+                                                             FsSweep sw, double et) {
     pdl_wait();
+    const double fs = sw.fs[blockIdx.z];
+    out += blockIdx.z * sw.out_stride;
     __shared__ float ubuf[2][kFuseBuf];     // coarse input of the current step / its output
     __shared__ double refbuf[kFuseBuf];     // reference depth per parent pixel
     const int L = lv.L, nsteps = L - 1;
@@ -633,7 +644,9 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
         for (int i = 1; i < L - 1; ++i) up += lv.h[L - i] * lv.w[L - i];
         const dim3 g((unsigned)((lv.w[1] + kFuseTX - 1) / kFuseTX),
                      (unsigned)((lv.h[1] + kFuseTY - 1) / kFuseTY));
-        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up, fs, et);
+        FsSweep sw{};
+        sw.fs[0] = fs;
+        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up, sw, et);
         if (e != cudaSuccess) return (int)e;
         coarse = up;
         up += lv.h[1] * lv.w[1];
@@ -677,6 +690,69 @@ __global__ void k_to_sentinel_pool(const float *__restrict__ depth, int64_t h, i
         }
         out[p] = m;
     }
+}
+
+// Final step of a filter_strength sweep (C4): one thread per
+// coarse pixel reads its <= 4 children's frame values ONCE and, for each of
+// the nk strengths, runs the edge / reference / keep test against that
+// strength's coarse image (coarse0 + k * cstride) and writes the k-th keep
+// mask and filtered frame (outputs at + k * fh * fw).  Same arithmetic as
+// k_filter_step<true>, so every strength's outputs equal a single-strength
+// depth filter bit for bit.
+__global__ void __launch_bounds__(256) k_filter_final_sweep(
+    const float *__restrict__ coarse0, int64_t cstride, int64_t ch, int64_t cw,
+    const float *__restrict__ depth, const float *__restrict__ rgb,
+    const uint8_t *__restrict__ alpha, int64_t fh, int64_t fw, FsSweep sw, int nk, double et,
+    float *__restrict__ frgb, float *__restrict__ fdepth, uint8_t *__restrict__ falpha,
+    uint8_t *__restrict__ keep_out) {
+    pdl_wait();
+    const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
+    if (cx >= cw || cy >= ch) return;
+    int64_t q[4];
+    float d[4], c[4][3];
+    uint8_t a[4];
+    int n = 0;
+    for (int dy = 0; dy < 2; ++dy) {
+        const int64_t y = 2 * cy + dy;
+        if (y >= fh) break;
+        for (int dx = 0; dx < 2; ++dx) {
+            const int64_t x = 2 * cx + dx;
+            if (x >= fw) break;
+            const int64_t p = y * fw + x;
+            q[n] = p;
+            d[n] = depth[p];
+            if (rgb) {
+                c[n][0] = rgb[3 * p];
+                c[n][1] = rgb[3 * p + 1];
+                c[n][2] = rgb[3 * p + 2];
+                a[n] = alpha[p];
+            }
+            ++n;
+        }
+    }
+    const int64_t hw = fh * fw;
+    for (int k = 0; k < nk; ++k) {
+        const float *coarse = coarse0 + k * cstride;
+        const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
+        const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+        const double fs = sw.fs[k];
+        for (int j = 0; j < n; ++j) {
+            const int64_t o = k * hw + q[j];
+            const bool kq = keep_test(sentinel(d[j]), ref, fs);
+            if (keep_out) keep_out[o] = (uint8_t)kq;
+            if (!rgb) continue;
+            const float m = kq ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
+            if (frgb) {
+                frgb[3 * o] = c[j][0] * m;
+                frgb[3 * o + 1] = c[j][1] * m;
+                frgb[3 * o + 2] = c[j][2] * m;
+            }
+            if (fdepth) fdepth[o] = d[j] * m;
+            if (falpha) falpha[o] = (uint8_t)(a[j] * (uint8_t)kq);
+        }
+    }
+    pdl_trigger();
 }
 
 bool setup_levels(int64_t H, int64_t W, int L, float *pyr, Levels &lv, float *&up_base) {
@@ -846,6 +922,66 @@ int ls_depth_filter_frame(const float *d_rgb, const float *d_depth, const uint8_
     return run_filter_steps(lv, up_base, d_depth, height, width, filter->filter_strength,
                             filter->edge_threshold, nullptr, d_rgb, d_alpha, d_frgb, d_fdepth,
                             d_falpha, d_keep, nullptr, 0, 0.0, st);
+}
+
+int64_t ls_filter_sweep_floats(int64_t height, int64_t width, int32_t levels_n,
+                               int32_t n_strengths) {
+    if (levels_n < 1 || levels_n > 5 || height <= 0 || width <= 0 || n_strengths < 1 ||
+        n_strengths > kMaxSweep)
+        return -1;
+    int64_t h[9], w[9];
+    level_sizes(height, width, levels_n, h, w);
+    int64_t total = 0;
+    for (int k = 1; k <= levels_n; ++k) total += h[k] * w[k];
+    return total + (levels_n >= 2 ? (int64_t)n_strengths * h[1] * w[1] : 0);
+}
+
+int ls_depth_filter_sweep(const float *d_rgb, const float *d_depth, const uint8_t *d_alpha,
+                          int64_t height, int64_t width, int32_t levels_n,
+                          double edge_threshold, const double *h_strengths, int32_t n_strengths,
+                          float *d_frgb, float *d_fdepth, uint8_t *d_falpha, uint8_t *d_keep,
+                          float *d_work, void *stream) {
+    if (!d_depth || !d_work || !h_strengths || height <= 0 || width <= 0 ||
+        !(edge_threshold > 0.0) || n_strengths < 1 || n_strengths > kMaxSweep ||
+        levels_n < 1 || levels_n > 5)
+        return LS_EINVAL;
+    if ((d_frgb || d_fdepth || d_falpha) && (!d_rgb || !d_alpha)) return LS_EINVAL;
+    FsSweep sw{};
+    for (int k = 0; k < n_strengths; ++k) {
+        if (!(h_strengths[k] >= 0.0)) return LS_EINVAL;
+        sw.fs[k] = h_strengths[k];
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Levels lv{};
+    float *up_base = nullptr;
+    if (!setup_levels(height, width, levels_n, d_work, lv, up_base)) return LS_EINVAL;
+    const int L = lv.L;
+    // strength-independent pyramid, once
+    k_to_sentinel_pool<<<grid_for(lv.h[1] * lv.w[1], 256), 256, 0, st>>>(d_depth, height, width,
+                                                                         lv.img[0]);
+    LS_LAUNCH_CHECK();
+    for (int k = 2; k <= L; ++k) {
+        k_min_pool<<<grid_for(lv.h[k] * lv.w[k], 256), 256, 0, st>>>(lv.img[k - 2], lv.h[k - 1],
+                                                                     lv.w[k - 1], lv.img[k - 1]);
+        LS_LAUNCH_CHECK();
+    }
+    const float *coarse = lv.img[L - 1];
+    int64_t cstride = 0;
+    if (L >= 2) {  // every strength's non-final steps: one launch, z = strength
+        sw.out_stride = lv.h[1] * lv.w[1];
+        const dim3 g((unsigned)((lv.w[1] + kFuseTX - 1) / kFuseTX),
+                     (unsigned)((lv.h[1] + kFuseTY - 1) / kFuseTY), (unsigned)n_strengths);
+        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up_base, sw,
+                                   edge_threshold);
+        if (e != cudaSuccess) return (int)e;
+        coarse = up_base;
+        cstride = sw.out_stride;
+    }
+    cudaError_t e = launch_pdl(k_filter_final_sweep, step_grid2(lv.h[1], lv.w[1]), dim3(32, 8),
+                               0, st, coarse, cstride, lv.h[1], lv.w[1], d_depth, d_rgb, d_alpha,
+                               height, width, sw, (int)n_strengths, edge_threshold, d_frgb,
+                               d_fdepth, d_falpha, d_keep);
+    return (int)e;
 }
 
 }  // extern "C"

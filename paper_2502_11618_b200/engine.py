@@ -39,10 +39,11 @@ def filter_launches(levels_n: int) -> int:
 class FrameRenderer:
     def __init__(self, grid, width: int, height: int, render_params: RenderParams | None = None,
                  filter_params: FilterParams | None = None, unet=None,
-                 filtered_outputs: bool = True):
+                 filtered_outputs: bool = True, keep_mask: bool = False):
         """``filtered_outputs=False`` (only with a U-Net): the f32 filtered frame
         (frgb/fdepth/falpha, 17 B/px) is not materialised -- the U-Net reads
-        the packed bf16 input the same filter kernel writes."""
+        the packed bf16 input the same filter kernel writes.  ``keep_mask``:
+        also write the filter's keep mask (u8, ``self.keep``) every frame."""
         import torch
 
         self.device = _lib.device()
@@ -62,6 +63,7 @@ class FrameRenderer:
         self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
         self.fdepth = torch.empty((h, w), dtype=torch.float32, device=dev)
         self.falpha = torch.empty((h, w), dtype=torch.uint8, device=dev)
+        self.keep = torch.empty((h, w), dtype=torch.uint8, device=dev) if keep_mask else None
         n = _lib.load().ls_pyramid_floats(h, w, self.fp.levels_n)
         if n < 0:
             raise ValueError(f"image {w}x{h} too small for {self.fp.levels_n} pyramid levels")
@@ -119,7 +121,7 @@ class FrameRenderer:
         else:
             filtered = (None, None, None)
         project_scene(self.scene, camera, self.rp.zbuffer_epsilon_rel, self.bufs, cull=True,
-                      filter_params=self.fp, filtered=filtered,
+                      filter_params=self.fp, filtered=filtered, keep=self.keep,
                       unet_in=None if self.unet is None else self.unet_in[0],
                       pyramid=self.pyramid, stage_events=events,
                       raw=self.unet is None or self.filtered_outputs, scratch=self.scratch,

@@ -73,6 +73,20 @@ def merge_accum(accum, root: int, group=None):
     return accum
 
 
+class DistComm:
+    """The collectives of a sharded frame over torch.distributed (NCCL on the
+    GPU box: NVLink/NVSwitch; gloo in the CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def all_min(self, minz_bits) -> None:
+        merge_minz(minz_bits, self.group)
+
+    def reduce_sum(self, accum, root: int) -> None:
+        merge_accum(accum, root, self.group)
+
+
 class ShardedRenderer:
     """FrameRenderer over one shard of the scan, merged across ranks.
 
@@ -81,22 +95,29 @@ class ShardedRenderer:
     projection (and its collectives, in which every rank takes part) never
     waits for a U-Net.  The per-frame pass buffers (minz, accum) alternate
     between two sets; set k is reused only after the side stream has consumed
-    (and reset) it."""
+    (and reset) it.
+
+    A frame is three phases around the two collectives -- ``_project_min``
+    (cull, work list, pass 1), ``_accumulate`` (pass 2 against the merged
+    minimum), ``_finish`` (root: assemble, filter, U-Net; others: reset) --
+    so ``VirtualShards`` can drive several ranks' renderers in one process."""
 
     def __init__(self, grid, width: int, height: int, rank: int, world: int,
                  render_params: RenderParams | None = None,
-                 filter_params: FilterParams | None = None, unet=None, group=None):
+                 filter_params: FilterParams | None = None, unet=None, group=None, comm=None):
         import torch
 
         from .render import FrameBuffers
 
         self.rank, self.world, self.group = rank, world, group
+        self.comm = comm or DistComm(group)
         self.device = _lib.device()
         self.rp = render_params or RenderParams()
         self.fp = filter_params or FilterParams()
         self.width, self.height = int(width), int(height)
         full = grid.scene()
         start, end = shard_bounds(full.n_points, rank, world)
+        self.shard = (start, end)
         offs = shard_cell_offsets(grid._device_field("cell_offsets", np.int64), start, end)
         self.scene = DeviceScene(full.positions[start:end], full.colors[start:end], offs,
                                  grid.origin, grid.cell_size, grid.dims)
@@ -118,6 +139,7 @@ class ShardedRenderer:
         self.side = torch.cuda.Stream()
         self._consumed = [None, None]  # side-stream event: set k finished + reset
         self.frame_index = 0
+        self.finished = None  # side-stream event of the last frame this rank finished
 
     @property
     def launches_per_frame(self) -> int:
@@ -130,41 +152,54 @@ class ShardedRenderer:
         n = 5 + (1 + filter_launches(self.fp.levels_n) + unet_n) / self.world
         return int(round(n))
 
-    def enqueue(self, camera) -> None:
-        """Enqueue one frame (this rank's share) on the current stream."""
+    def _next(self):
+        """(pass-buffer set, root) of the next frame; waits (on the current
+        stream) until the set's previous frame was consumed."""
         import torch
 
-        lib = _lib.load()
-        main = torch.cuda.current_stream()
         k = self.frame_index % 2
         root = self.frame_index % self.world
         self.frame_index += 1
-        b = self.sets[k]
         if self._consumed[k] is not None:
-            main.wait_event(self._consumed[k])
-        cam = _lib.make_camera(camera)
-        sc = self.scene
-        st = _lib.stream_ptr()
+            torch.cuda.current_stream().wait_event(self._consumed[k])
+        return k, root
+
+    def _project_min(self, camera, k) -> None:
+        """Cull this shard's cells, build its work list, pass 1 into set k."""
+        sc, b = self.scene, self.sets[k]
         bits = sc.cull_bits(extract_frustum(camera).planes).data_ptr()
         tl, tc = sc.worklist()
         cache = _lib.ptr(frame_cache(sc, camera))
-        _lib.check(lib.ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
-                                      b.minz.data_ptr(), cache, st), "frame_pass1")
-        merge_minz(b.minz, self.group)
-        _lib.check(lib.ls_frame_pass2(sc.struct, bits, tl.data_ptr(), tc.data_ptr(), cam,
-                                      float(self.rp.zbuffer_epsilon_rel), b.minz.data_ptr(),
-                                      cache, b.accum.data_ptr(), st), "frame_pass2")
-        merge_accum(b.accum, root, self.group)
+        _lib.check(_lib.load().ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(),
+                                              _lib.make_camera(camera), b.minz.data_ptr(), cache,
+                                              _lib.stream_ptr()), "frame_pass1")
+
+    def _accumulate(self, camera, k) -> None:
+        """Pass 2 of this shard against set k's (merged) minimum."""
+        sc, b = self.scene, self.sets[k]
+        _lib.check(_lib.load().ls_frame_pass2(
+            sc.struct, sc.keep_bits.data_ptr(), sc.tile_list.data_ptr(),
+            sc.tile_count.data_ptr(), _lib.make_camera(camera),
+            float(self.rp.zbuffer_epsilon_rel), b.minz.data_ptr(),
+            _lib.ptr(frame_cache(sc, camera)), b.accum.data_ptr(), _lib.stream_ptr()),
+            "frame_pass2")
+
+    def _finish(self, k, root) -> None:
+        """Root: assemble + filter (+ U-Net) from set k on the side stream.
+        Others: reset set k for the frame after next."""
+        import torch
+
+        b = self.sets[k]
         if self.rank != root:
             b.minz.fill_(_lib.INF_BITS)
             b.accum.zero_()
             self._consumed[k] = None
             return
         merged = torch.cuda.Event()
-        merged.record(main)
+        merged.record(torch.cuda.current_stream())
         self.side.wait_event(merged)
         with torch.cuda.stream(self.side):
-            _lib.check(lib.ls_frame_finish(
+            _lib.check(_lib.load().ls_frame_finish(
                 b.minz.data_ptr(), b.accum.data_ptr(), b.width, b.height,
                 _lib.make_filter(self.fp), b.rgb.data_ptr(), b.depth.data_ptr(),
                 b.alpha.data_ptr(), self.frgb.data_ptr(), self.fdepth.data_ptr(),
@@ -179,6 +214,18 @@ class ShardedRenderer:
             self._consumed[k] = done
             if self.unet is not None:
                 self.unet.forward(self.unet_in, self.rgb_out)
+            fin = torch.cuda.Event()
+            fin.record(self.side)
+            self.finished = fin
+
+    def enqueue(self, camera) -> None:
+        """Enqueue one frame (this rank's share) on the current stream."""
+        k, root = self._next()
+        self._project_min(camera, k)
+        self.comm.all_min(self.sets[k].minz)
+        self._accumulate(camera, k)
+        self.comm.reduce_sum(self.sets[k].accum, root)
+        self._finish(k, root)
 
     def synchronize(self) -> None:
         """Wait for this rank's side-stream work (the frames it is root of)."""
@@ -186,5 +233,51 @@ class ShardedRenderer:
 
     def check_flags(self) -> None:
         self.side.synchronize()
-        if any(int(b.flags.item()) for b in self.sets):
+        bad = any(int(b.flags.item()) for b in self.sets)
+        for b in self.sets:
+            b.flags.zero_()
+        if bad:
             raise RuntimeError("f32 accumulator bound exceeded")
+
+
+class VirtualShards:
+    """All ranks of a point-sharded frame in ONE process (tests, and a world
+    larger than the visible GPUs): each rank's ShardedRenderer runs its
+    phases on the current stream and the two collectives are done in memory
+    (MIN over the ranks' minima written back to every rank, SUM of the
+    accumulators into the root's set) -- the same data flow as ``enqueue``
+    over NCCL, with no rank ever waiting on another rank's kernel."""
+
+    def __init__(self, grid, width: int, height: int, world: int, **kw):
+        self.ranks = [ShardedRenderer(grid, width, height, r, world, comm=_NoComm(), **kw)
+                      for r in range(world)]
+        self.world = world
+
+    def enqueue(self, camera) -> int:
+        """One frame across every virtual rank; returns the root rank."""
+        import torch
+
+        ks = [r._next() for r in self.ranks]
+        k, root = ks[0]
+        for r in self.ranks:
+            r._project_min(camera, k)
+        gmin = torch.stack([r.sets[k].minz for r in self.ranks]).amin(0)
+        for r in self.ranks:
+            r.sets[k].minz.copy_(gmin)
+            r._accumulate(camera, k)
+        total = torch.stack([r.sets[k].accum for r in self.ranks]).sum(0)
+        self.ranks[root].sets[k].accum.copy_(total)
+        for r in self.ranks:
+            r._finish(k, root)
+        return root
+
+    def synchronize(self) -> None:
+        for r in self.ranks:
+            r.synchronize()
+
+
+class _NoComm:
+    def all_min(self, t):
+        raise RuntimeError("virtual ranks merge in VirtualShards.enqueue")
+
+    reduce_sum = all_min

@@ -15,11 +15,11 @@ from paper_2502_11618_b200.engine import FrameRenderer
 from paper_2502_11618_b200.scenes import hall_cameras, multi_station_hall
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--points", type=int, default=20_000_000)
+ap.add_argument("--points", type=int, default=100_000_000)
 ap.add_argument("--frames", type=int, default=3)
 ap.add_argument("--unet", default="none")
 a = ap.parse_args()
-pos, col, _ = multi_station_hall(a.points)
+pos, col, _ = multi_station_hall(a.points, device="cuda")
 grid = build_grid(PointCloud(pos, col), 1.0)
 unet = None
 if a.unet != "none":

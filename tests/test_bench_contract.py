@@ -19,12 +19,14 @@ BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_ste
              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
 
 
-def _run(args, env=None, timeout=300):
+def _run(args, env=None, timeout=300, rc=0):
     e = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        e.pop(k, None)
     e.update(env or {})
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT,
                        env=e, capture_output=True, text=True, timeout=timeout)
-    assert p.returncode == 0, p.stderr[-2000:]
+    assert p.returncode == rc, p.stderr[-2000:]
     lines = [l for l in p.stdout.splitlines() if l.strip().startswith("{")]
     return lines
 
@@ -45,8 +47,30 @@ def test_reference_arm_line():
 
 
 def test_reference_arm_other_ranks_silent():
-    assert _run(["--impl", "reference", "--steps", "1", "--warmup", "1"] + TINY,
+    assert _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"] + TINY,
                 env={"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_world_size_must_match_gpus():
+    assert _run(["--impl", "reference", "--gpus", "4", "--steps", "1"] + TINY,
+                env={"RANK": "0", "WORLD_SIZE": "2"}, rc=2) == []
+
+
+def test_gpus_flag_launches_ranks():
+    """--gpus 2 without torchrun re-executes bench.py as 2 ranks
+    (torch.distributed.run); the reference arm prints once, from rank 0, with
+    n_gpus 2 and the same config dict the b200 arm prints."""
+    lines = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1"] + TINY)
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "point-shard2"
+    sys.path.insert(0, ROOT)
+    import bench
+
+    class A:
+        points, width, height, views, unet, mode = 20000, 64, 64, 8, "reduced", "sharded"
+
+    assert d["config"] == bench.bench_config(A, 2)
 
 
 @pytest.mark.gpu
@@ -63,3 +87,8 @@ def test_b200_arm_line():
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["clocks"]["sm_max_mhz"] > 0
+    par = d["parity"]
+    assert par["bit_exact"] is True and par["frames"] >= 1
+    assert par["unet_within_tolerance"] is True
+    ref = json.loads(_run(["--impl", "reference", "--steps", "1", "--warmup", "1"] + TINY)[0])
+    assert ref["config"] == d["config"]

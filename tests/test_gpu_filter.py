@@ -189,3 +189,39 @@ def test_fused_frame_path_vs_oracle(port, size):
         exp = torch.from_numpy(ref).to(torch.bfloat16).float().numpy()
         assert np.array_equal(got, exp)
         assert (unet_in[:h, :, 5:].float() == 0).all() and (unet_in[h:].float() == 0).all()
+
+
+@pytest.mark.parametrize("levels,size,k", [(4, (333, 257), 7), (1, (40, 30), 3),
+                                           (2, (64, 48), 16), (5, (200, 150), 19),
+                                           (6, (130, 97), 2), (3, (3840, 2160), 7)])
+def test_depth_filter_sweep_vs_oracle(port, levels, size, k):
+    """filtering.depth_filter_sweep (pyramid once, all strengths batched, >16
+    strengths in chunks, L > 5 on the per-strength path): every strength's
+    filtered frame and keep mask equal the oracle's depth filter."""
+    import torch
+
+    from paper_2502_11618_b200 import FilterParams
+    from paper_2502_11618_b200.filtering import depth_filter_sweep
+
+    w, h = size
+    rng = np.random.default_rng(levels * 100 + k)
+    depth = sparse_depth(rng, h, w, fill=0.55)
+    alpha = (depth > 0).astype(np.uint8)
+    rgb = (rng.random((h, w, 3)) * alpha[..., None]).astype(np.float32)
+    fs_list = [0.0, 0.05, 0.1, 0.25, 0.5, 1.0, 1e30][:k] + list(rng.random(max(0, k - 7)) * 0.6)
+    dev = torch.device("cuda")
+    t = [torch.from_numpy(a).to(dev) for a in (rgb, depth, alpha)]
+    et = 0.25 if levels != 2 else 0.1
+    frgb, fdep, falp, keep = depth_filter_sweep(*t, fs_list, FilterParams(levels_n=levels,
+                                                                          edge_threshold=et))
+    _, _, _, keep_only = depth_filter_sweep(*t, fs_list, FilterParams(levels_n=levels,
+                                                                      edge_threshold=et),
+                                            outputs=False)
+    assert bool((keep == keep_only).all())
+    picks = range(k) if max(size) < 1000 else [0, 2, 6]
+    for i in picks:
+        r2, d2, a2, k2 = O.depth_filter(rgb, depth, alpha, levels, fs_list[i], et, port)
+        assert np.array_equal(keep[i].cpu().numpy().astype(bool), k2), f"fs={fs_list[i]}"
+        assert np.array_equal(frgb[i].cpu().numpy(), r2)
+        assert np.array_equal(fdep[i].cpu().numpy(), d2)
+        assert np.array_equal(falp[i].cpu().numpy(), a2)
