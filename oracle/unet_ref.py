@@ -139,3 +139,77 @@ class CpuUNet:
         with torch.no_grad():
             y = forward(self.cfg, self.params, x, dtype=torch.float32)
         return y[0, : depth.shape[0]].numpy()
+
+
+# ---------------------------------------------------------------------------
+# Independent scalar restatement of the reference's weight init (checks the
+# product's vectorised paper_2502_11618_b200.unet.init_params):
+#   mulberry32 + Box-Muller + child streams   FE:rng.ts:1-39
+#   FNV-1a layer-name hash                     FE:model/unet.ts:92-99
+#   He-normal kernels, zero bias, BN identity  FE:model/unet.ts:58-86, 100-132
+# Pure-Python integer arithmetic, one draw at a time exactly as the TS loops.
+# ---------------------------------------------------------------------------
+
+def _mul32(a, b):
+    return (a * b) % 4294967296
+
+
+class Mulberry32:
+    def __init__(self, seed):
+        self.s = seed % 4294967296
+
+    def next(self):
+        self.s = (self.s + 0x6D2B79F5) % 4294967296
+        t = self.s
+        t = _mul32(t ^ (t >> 15), t | 1)
+        t = t ^ ((t + _mul32(t ^ (t >> 7), t | 61)) % 4294967296)
+        return (t ^ (t >> 14)) / 4294967296.0
+
+    def normal(self):
+        import math
+
+        u = 0.0
+        while u == 0.0:
+            u = self.next()
+        v = self.next()
+        return math.sqrt(-2.0 * math.log(u)) * math.cos(2.0 * math.pi * v)
+
+    def child(self, tag):
+        return Mulberry32(self.s ^ _mul32((tag + 0x9E3779B9) % 4294967296, 0x85EBCA6B))
+
+
+def fnv1a(name):
+    h = 2166136261
+    for ch in name:
+        h = _mul32(h ^ ord(ch), 16777619)
+    return h
+
+
+def ref_layer_shapes(cfg):
+    """(name, kernel shape, fan_in) of every conv in construction order
+    (FE:model/unet.ts:100-132)."""
+    out = []
+    ci = cfg.inChannels
+    for s in range(cfg.depth):
+        w = cfg.baseWidth * 2 ** s
+        out += [(f"enc{s}_conv1", (3, 3, ci, w), 9 * ci), (f"enc{s}_conv2", (3, 3, w, w), 9 * w)]
+        ci = w
+    bw = cfg.baseWidth * 2 ** cfg.depth
+    out += [("bott_conv1", (3, 3, ci, bw), 9 * ci), ("bott_conv2", (3, 3, bw, bw), 9 * bw)]
+    cu = bw
+    for s in range(cfg.depth - 1, -1, -1):
+        w = cfg.baseWidth * 2 ** s
+        out += [(f"dec{s}_up", (2, 2, w, cu), 4 * cu), (f"dec{s}_conv1", (3, 3, 2 * w, w), 18 * w),
+                (f"dec{s}_conv2", (3, 3, w, w), 9 * w)]
+        cu = w
+    out.append(("final_conv", (1, 1, cfg.baseWidth, cfg.outChannels), cfg.baseWidth))
+    return out
+
+
+def ref_kernel_values(seed, name, fan_in, count):
+    """The first ``count`` He-normal values (flat, row-major) of layer ``name``."""
+    import math
+
+    rng = Mulberry32(seed).child(fnv1a(name))
+    std = math.sqrt(2.0 / fan_in)
+    return np.array([rng.normal() * std for _ in range(count)], np.float64)

@@ -1,3 +1,2 @@
-set -x
-python -m pytest tests/test_gpu_configs.py tests/test_gpu_shard.py tests/test_gpu_filter.py tests/test_gpu_engine.py tests/test_bench_contract.py -x -q > gpurun_out/r02_gpu_tests_4.log 2>&1; tail -15 gpurun_out/r02_gpu_tests_4.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench_v1.json 2> gpurun_out/r02_bench_v1.err; tail -c 4000 gpurun_out/r02_bench_v1.json; tail -5 gpurun_out/r02_bench_v1.err
+python -m pytest tests/test_gpu_configs.py tests/test_gpu_projection.py tests/test_gpu_shard.py -x -q -k "not full_resolution" 2>&1 | tail -2
+for i in 1 2; do python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['stages_ms'], d['roofline']['other']['frac'])"; done

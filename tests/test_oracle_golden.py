@@ -206,3 +206,31 @@ def test_threaded_oracle_matches_single(kern):
     b = O.project(grid.sorted_positions, grid.sorted_colors, s, e, cam, 0.01, kern, workers=5)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_unet_init_matches_independent_restatement():
+    """paper_2502_11618_b200.unet.init_params (vectorised closed-form
+    mulberry32) equals the oracle's one-draw-at-a-time restatement of
+    FE:rng.ts + FE:model/unet.ts: every REDUCED tensor in full, and the first
+    2048 values of every DEFAULT kernel (same seeds, names, shapes, fan-ins).
+    Uniform draws are bit-equal; the normals agree to 2 ulp (numpy's SIMD
+    log/cos vs libm's scalar ones -- V8's Math.log/cos, the reference's, are
+    a third implementation, so the last ulp is unpinnable without node)."""
+    import numpy as np
+
+    from oracle.unet_ref import ref_kernel_values, ref_layer_shapes
+    from paper_2502_11618_b200.unet import DEFAULT_CONFIG, REDUCED_CONFIG, init_params
+
+    for cfg, seed, limit in ((REDUCED_CONFIG, 3, None), (DEFAULT_CONFIG, 7, 2048)):
+        p = init_params(cfg, seed)
+        layers = ref_layer_shapes(cfg)
+        assert {n + ".kernel" for n, _, _ in layers} == {k for k in p if k.endswith(".kernel")}
+        for name, shape, fan_in in layers:
+            k = p[name + ".kernel"]
+            assert k.shape == shape
+            n = k.size if limit is None else min(limit, k.size)
+            ref = ref_kernel_values(seed, name, fan_in, n)
+            np.testing.assert_allclose(k.ravel()[:n], ref, rtol=4.5e-16, atol=0, err_msg=name)
+            assert not p[name + ".bias"].any()
+        for s in range(cfg.depth):
+            assert (p[f"enc{s}_bn1.moving_var"] == 1).all() and (p[f"enc{s}_bn2.gamma"] == 1).all()
