@@ -280,8 +280,11 @@ def build_grid(cloud: PointCloud, cell_size: float, backend=None) -> UniformGrid
         raise InvalidCloudError("empty cloud")
     if cell_size <= 0:
         raise ValueError("cell_size must be > 0")
-    lo = cloud.positions.min(axis=0).astype(np.float64)
-    hi = cloud.positions.max(axis=0).astype(np.float64)
+    pos, col = cloud.device_arrays()
+    # component-wise extent on the device (min/max are exact; numpy's strided
+    # axis-0 reduction takes seconds at 100M points)
+    lo = torch.amin(pos, dim=0).cpu().numpy().astype(np.float64)
+    hi = torch.amax(pos, dim=0).cpu().numpy().astype(np.float64)
     dims_f = np.maximum(np.ceil((hi - lo) / cell_size), 1.0)
     if dims_f.prod() > MAX_CELLS:
         raise InvalidCloudError(
@@ -290,7 +293,6 @@ def build_grid(cloud: PointCloud, cell_size: float, backend=None) -> UniformGrid
     n, n_cells = cloud.count, int(dims.prod())
     lib = _lib.load()
     st = _lib.stream_ptr()
-    pos, col = cloud.device_arrays()
     dev = pos.device
     ids = torch.empty(n, dtype=torch.int64, device=dev)
     _lib.check(lib.ls_assign_cells(pos.data_ptr(), n, lo.ctypes.data, float(cell_size),

@@ -127,3 +127,67 @@ def test_typed_buffer_errors(cu):
         cu.min_pool_2x2(np.zeros((4, 4), np.float64))
     with pytest.raises(ValueError, match="contiguous"):
         cu.min_pool_2x2(np.zeros((4, 8), np.float32)[:, ::2])
+
+
+def test_counting_sort_hand_written_radix_edges(cu, port):
+    """The hand-written stable LSD radix sort behind ls_counting_sort (no CUB):
+    block boundaries (4096 keys), a single key, one hot cell holding most
+    points, and a 2^31-cell grid (4 digit passes) all equal the stable
+    counting sort of the oracle."""
+    rng = np.random.default_rng(17)
+    cases = [(np.zeros(1, np.int64), 3), (rng.integers(0, 9, size=4097), 9),
+             (rng.integers(0, 300, size=8192), 300)]
+    skew = rng.integers(0, 9600, size=3_000_017)
+    skew[rng.random(skew.size) < 0.7] = 4242
+    cases.append((skew, 9600))
+    cases.append((rng.integers(0, 1 << 31, size=70_001), 1 << 31))
+    for ids, n_cells in cases:
+        ids = ids.astype(np.int64)
+        order = np.argsort(ids, kind="stable")
+        a = cu.counting_sort(ids, n_cells)
+        assert np.array_equal(a[1], order), n_cells
+        if n_cells <= 1 << 20:
+            b = port.counting_sort(ids, n_cells)
+            assert np.array_equal(a[0], b[0])
+
+
+def test_morton_order_matches_stable_key_sort():
+    """ls_morton_order (cell id << 30 | in-cell Morton code, hand-written
+    radix sort over 44 key bits): the permutation equals numpy's stable sort
+    of the same keys computed on the host."""
+    import torch
+
+    from paper_2502_11618_b200 import _lib
+
+    rng = np.random.default_rng(23)
+    n = 1_000_003
+    pos = (rng.random((n, 3)) * np.array([40.0, 30.0, 8.0])).astype(np.float32)
+    origin = pos.min(axis=0).astype(np.float64)
+    cell = 1.0
+    dims = np.maximum(np.ceil((pos.max(axis=0).astype(np.float64) - origin) / cell), 1).astype(
+        np.int64)
+    f = (pos.astype(np.float64) - origin) / cell
+    i = np.floor(f).astype(np.int64)
+    t = (f - i) * 1024.0
+    q = np.where(t <= 0, 0, np.where(t >= 1023, 1023, t.astype(np.int64))).astype(np.uint64)
+    ic = np.minimum(np.maximum(i, 0), dims - 1)
+    cid = ((ic[:, 0] * dims[1] + ic[:, 1]) * dims[2] + ic[:, 2]).astype(np.uint64)
+
+    def spread(v):
+        out = np.zeros_like(v)
+        for b in range(10):
+            out |= ((v >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b)
+        return out
+
+    keys = (cid << np.uint64(30)) | spread(q[:, 0]) | (spread(q[:, 1]) << np.uint64(1)) | (
+        spread(q[:, 2]) << np.uint64(2))
+    want = np.argsort(keys, kind="stable")
+    lib = _lib.load()
+    d_pos = torch.from_numpy(pos).cuda()
+    ws_bytes = lib.ls_morton_order_workspace(n, int(dims.prod()))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    order = torch.empty(n, dtype=torch.int64, device="cuda")
+    _lib.check(lib.ls_morton_order(d_pos.data_ptr(), n, origin.ctypes.data, cell,
+                                   np.ascontiguousarray(dims).ctypes.data, order.data_ptr(),
+                                   ws.data_ptr(), ws_bytes, _lib.stream_ptr()), "morton_order")
+    assert np.array_equal(order.cpu().numpy(), want)
