@@ -280,11 +280,17 @@ def build_grid(cloud: PointCloud, cell_size: float, backend=None) -> UniformGrid
         raise InvalidCloudError("empty cloud")
     if cell_size <= 0:
         raise ValueError("cell_size must be > 0")
-    pos, col = cloud.device_arrays()
-    # component-wise extent on the device (min/max are exact; numpy's strided
-    # axis-0 reduction takes seconds at 100M points)
-    lo = torch.amin(pos, dim=0).cpu().numpy().astype(np.float64)
-    hi = torch.amax(pos, dim=0).cpu().numpy().astype(np.float64)
+    # component-wise extent (min/max are exact): on the device when there is
+    # one (numpy's strided axis-0 reduction takes seconds at 100M points), so
+    # the argument checks below still run first on a GPU-less host
+    if torch.cuda.is_available():
+        pos, col = cloud.device_arrays()
+        lo = torch.amin(pos, dim=0).cpu().numpy().astype(np.float64)
+        hi = torch.amax(pos, dim=0).cpu().numpy().astype(np.float64)
+    else:
+        p = cloud.positions
+        lo = np.array([p[:, i].min() for i in range(3)], np.float64)
+        hi = np.array([p[:, i].max() for i in range(3)], np.float64)
     dims_f = np.maximum(np.ceil((hi - lo) / cell_size), 1.0)
     if dims_f.prod() > MAX_CELLS:
         raise InvalidCloudError(
@@ -293,6 +299,7 @@ def build_grid(cloud: PointCloud, cell_size: float, backend=None) -> UniformGrid
     n, n_cells = cloud.count, int(dims.prod())
     lib = _lib.load()
     st = _lib.stream_ptr()
+    pos, col = cloud.device_arrays()
     dev = pos.device
     ids = torch.empty(n, dtype=torch.int64, device=dev)
     _lib.check(lib.ls_assign_cells(pos.data_ptr(), n, lo.ctypes.data, float(cell_size),
