@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=2, help="cpu_baseline / parity frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--views", type=int, default=8, help="camera poses cycled")
+    ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
+                    help="1: every frame is one CUDA-graph launch (FrameRenderer(graph=True))")
     ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
                     help="N>1: point-sharded frames (default; min/sum merges, root-side "
                          "filter + U-Net, round-robin roots) or frame-parallel replicas; the "
@@ -407,7 +409,7 @@ def run_b200(args):
     # single-GPU frames, or frame-parallel replicas (every rank renders its
     # own frames of the whole scan; no data-path collective)
     renderer = FrameRenderer(grid, args.width, args.height, unet=unet,
-                             filtered_outputs=unet is None)
+                             filtered_outputs=unet is None, graph=bool(args.graph))
     view0 = rank * args.steps
     for i in range(args.warmup):
         renderer.enqueue(cams[(view0 + i) % len(cams)])

@@ -226,6 +226,16 @@ int ls_frame_pass2(const ls_scene *scene, const uint32_t *d_keep_bits, const uin
  * d_accum4: n_views x (W*H*4) f32, zero on entry; one ls_frame_finish per view
  *   (at the view's offsets) folds them into frames. */
 #define LS_MAX_VIEWS 8
+/* Re-target a captured frame graph to another camera.  graph / graph_exec
+ * are the cudaGraph_t / cudaGraphExec_t of a stream capture of one fused
+ * frame (ls_cull, ls_tile_worklist, ls_frame_pass1, ls_frame_pass2, the
+ * assembly / filter and U-Net launches); the cull nodes take the new frustum
+ * planes (24 doubles, as ls_cull) and the projection-pass nodes the new
+ * camera.  Returns 0, LS_EINVAL when the graph holds no such node, or a CUDA
+ * error. */
+int ls_frame_graph_set_camera(void *graph, void *graph_exec, const ls_camera *cam,
+                              const double h_planes[24]);
+
 int ls_tile_worklist_views(const ls_scene *scene, const uint32_t *d_keep_bits,
                            int64_t bits_stride, int32_t n_views, uint32_t *d_list,
                            uint32_t *d_status, uint32_t *d_count, void *stream);

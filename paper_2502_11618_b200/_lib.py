@@ -112,6 +112,7 @@ SIGNATURES = {
     "ls_depth_filter_frame": (ctypes.c_int, [_P, _P, _P, _I64, _I64,
                                              ctypes.POINTER(LsFilterParams), _P, _P, _P, _P, _P,
                                              _P]),
+    "ls_frame_graph_set_camera": (ctypes.c_int, [_P, _P, ctypes.POINTER(LsCamera), _P]),
     "ls_filter_sweep_floats": (_I64, [_I64, _I64, _I32, _I32]),
     "ls_depth_filter_sweep": (ctypes.c_int, [_P, _P, _P, _I64, _I64, _I32, _D, _P, _I32, _P,
                                              _P, _P, _P, _P, _P]),

@@ -167,6 +167,14 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace ls
 
+namespace ls {
+// (for ls_frame_graph_set_camera: the captured node to re-target, and the
+// index of its Planes argument)
+const void *cull_kernel() { return (const void *)k_cull; }
+constexpr int kCullPlanesArg = 8;
+int cull_planes_arg() { return kCullPlanesArg; }
+}  // namespace ls
+
 using namespace ls;
 
 extern "C" {

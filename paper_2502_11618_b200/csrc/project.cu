@@ -24,6 +24,9 @@
 
 namespace ls {
 
+const void *cull_kernel();
+int cull_planes_arg();
+
 // ---------------------------------------------------------------------------
 // (i) twins with the reference's range/cache interface
 // ---------------------------------------------------------------------------
@@ -1136,6 +1139,63 @@ int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
     if (rc) return rc;
     return ls_frame_pass2(scene, d_keep_bits, d_list, d_count, cam, eps_rel, d_minz_bits, d_cache,
                           d_accum4, stream);
+}
+
+// Re-target a captured frame graph (stream capture of ls_cull +
+// ls_tile_worklist + ls_frame_pass1/2 + the rest of the frame) to another
+// camera: the k_cull nodes get the new frustum planes and the projection
+// pass nodes the new camera, through cudaGraphExecKernelNodeSetParams; every
+// other node (work list, assembly, filter, U-Net) is camera-independent.
+int ls_frame_graph_set_camera(void *graph, void *graph_exec, const ls_camera *cam,
+                              const double h_planes[24]) {
+    if (!graph || !graph_exec || !camera_ok(cam) || !h_planes) return LS_EINVAL;
+    cudaGraph_t g = (cudaGraph_t)graph;
+    cudaGraphExec_t ge = (cudaGraphExec_t)graph_exec;
+    size_t n = 0;
+    cudaError_t e = cudaGraphGetNodes(g, nullptr, &n);
+    if (e != cudaSuccess) return (int)e;
+    if (n == 0) return LS_EINVAL;
+    cudaGraphNode_t nodes[512];
+    if (n > 512) return LS_EINVAL;
+    e = cudaGraphGetNodes(g, nodes, &n);
+    if (e != cudaSuccess) return (int)e;
+    const ProjCam pc = make_cam(*cam);
+    double planes[24];
+    for (int i = 0; i < 24; ++i) planes[i] = h_planes[i];
+    // (kernel, its parameter count, the index of its camera / planes argument)
+    struct Target {
+        const void *fn;
+        int nargs, arg;
+        const void *val;
+    };
+    const Target targets[] = {
+        {cull_kernel(), 11, cull_planes_arg(), planes},
+        {(const void *)k_frame_pass1, 7, 1, &pc},
+        {(const void *)k_frame_pass1_u32, 7, 1, &pc},
+        {(const void *)k_frame_pass2, 8, 1, &pc},
+        {(const void *)k_frame_pass2_cached, 8, 1, &pc},
+    };
+    int updated = 0;
+    for (size_t i = 0; i < n; ++i) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nodes[i], &t) != cudaSuccess || t != cudaGraphNodeTypeKernel)
+            continue;
+        cudaKernelNodeParams kp;
+        e = cudaGraphKernelNodeGetParams(nodes[i], &kp);
+        if (e != cudaSuccess) return (int)e;
+        for (const Target &tg : targets) {
+            if (kp.func != tg.fn) continue;
+            void *args[16];
+            for (int a = 0; a < tg.nargs; ++a) args[a] = kp.kernelParams[a];
+            args[tg.arg] = const_cast<void *>(tg.val);
+            kp.kernelParams = args;
+            kp.extra = nullptr;
+            e = cudaGraphExecKernelNodeSetParams(ge, nodes[i], &kp);
+            if (e != cudaSuccess) return (int)e;
+            ++updated;
+        }
+    }
+    return updated >= 1 ? 0 : LS_EINVAL;
 }
 
 int ls_tile_worklist_views(const ls_scene *scene, const uint32_t *d_keep_bits,

@@ -39,11 +39,16 @@ def filter_launches(levels_n: int) -> int:
 class FrameRenderer:
     def __init__(self, grid, width: int, height: int, render_params: RenderParams | None = None,
                  filter_params: FilterParams | None = None, unet=None,
-                 filtered_outputs: bool = True, keep_mask: bool = False):
+                 filtered_outputs: bool = True, keep_mask: bool = False,
+                 graph: bool = False):
         """``filtered_outputs=False`` (only with a U-Net): the f32 filtered frame
         (frgb/fdepth/falpha, 17 B/px) is not materialised -- the U-Net reads
         the packed bf16 input the same filter kernel writes.  ``keep_mask``:
-        also write the filter's keep mask (u8, ``self.keep``) every frame."""
+        also write the filter's keep mask (u8, ``self.keep``) every frame.
+        ``graph``: enqueue each frame as ONE CUDA-graph launch (captured once
+        per output slot, re-targeted to every frame's camera by
+        ``ls_frame_graph_set_camera``) instead of ~50 individual launches --
+        for launch-bound small frames; results are identical."""
         import torch
 
         self.device = _lib.device()
@@ -87,6 +92,9 @@ class FrameRenderer:
         self._copy_done = [None, None]
         self._ring = None
         self._exact_bufs = None
+        self.use_graph = bool(graph)
+        self._graphs = [None, None]
+        self._cap_stream = None
 
     @property
     def launches_per_frame(self) -> int:
@@ -113,6 +121,41 @@ class FrameRenderer:
         ``events`` (optional list of 3 CUDA events) marks project / filter /
         U-Net boundaries for per-stage timing.  ``slot`` selects the output
         buffer set (render_stream alternates two)."""
+        if self.use_graph and events is None:
+            self._replay(camera, slot)
+            return
+        self._enqueue_launches(camera, events, slot)
+
+    def _replay(self, camera, slot: int) -> None:
+        """The frame as one graph launch on the current stream."""
+        import torch
+
+        from .geometry import extract_frustum
+
+        g = self._graphs[slot]
+        if g is None:
+            # warm-up frame on the capture stream (allocates the pass-1 cache
+            # and the U-Net's per-stream plans / activations outside the
+            # capture), then the capture itself
+            if self._cap_stream is None:
+                self._cap_stream = torch.cuda.Stream()
+            cap = self._cap_stream
+            cap.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cap):
+                self._enqueue_launches(camera, None, slot)
+            cap.synchronize()
+            g = torch.cuda.CUDAGraph(keep_graph=True)
+            with torch.cuda.graph(g, stream=cap):
+                self._enqueue_launches(camera, None, slot)
+            g.instantiate()
+            self._graphs[slot] = g
+        planes = np.ascontiguousarray(extract_frustum(camera).planes, np.float64)
+        _lib.check(_lib.load().ls_frame_graph_set_camera(
+            g.raw_cuda_graph(), g.raw_cuda_graph_exec(), _lib.make_camera(camera),
+            planes.ctypes.data), "frame_graph_set_camera")
+        g.replay()
+
+    def _enqueue_launches(self, camera, events, slot: int) -> None:
         outs = self._outputs(slot)
         if self.unet is None:
             filtered = outs

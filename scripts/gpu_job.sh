@@ -1,13 +1,5 @@
-python -m pytest tests/test_gpu_kernels.py tests/test_gpu_projection.py tests/test_gpu_configs.py -x -q -k "not full_resolution" 2>&1 | tail -3
-python - <<'PY'
-import time, torch, sys
-sys.path.insert(0, '.')
-from paper_2502_11618_b200 import PointCloud, build_grid
-from paper_2502_11618_b200.scenes import multi_station_hall
-for n in (20_000_000, 100_000_000):
-    pos, col, _ = multi_station_hall(n, device="cuda")
-    c = PointCloud(pos, col); c.device_arrays(); torch.cuda.synchronize()
-    for rep in range(2):
-        t = time.perf_counter(); g = build_grid(c, 1.0); g.scene(); torch.cuda.synchronize()
-        print(n, "build_grid + Morton scene", f"{(time.perf_counter() - t) * 1e3:.1f} ms")
-PY
+python -m pytest tests/test_gpu_engine.py -x -q 2>&1 | tail -2
+for g in 0 1; do
+python bench.py --steps 200 --warmup 10 --points 1000000 --width 512 --height 512 --unet reduced --no-cpu-baseline --graph $g 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C1 graph=$g', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), d['frame_ms'])"
+python bench.py --steps 30 --warmup 5 --no-cpu-baseline --graph $g 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C3 graph=$g', round(d['value'],1), 'e2e', round(d['e2e']['value'],1))"
+done

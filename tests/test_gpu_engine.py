@@ -315,3 +315,45 @@ def test_generate_dataset_deterministic(tmp_path):
     stored = read_frame(tmp_path / "a" / "pairs" / "f1.input")
     assert np.array_equal(stored.depth, pair.input.depth)
     assert np.array_equal(stored.alpha, pair.input.alpha)
+
+
+@pytest.mark.parametrize("with_unet", [False, True])
+def test_graph_frames_equal_launched_frames(with_unet):
+    """FrameRenderer(graph=True): each frame is one CUDA-graph launch
+    re-targeted to the frame's camera (ls_frame_graph_set_camera) -- every
+    frame equals the launch-by-launch frame, through render, render_stream and
+    back-to-back enqueues."""
+    import torch
+
+    from paper_2502_11618_b200 import build_grid
+    from paper_2502_11618_b200.engine import FrameRenderer
+    from paper_2502_11618_b200.unet import UNet
+
+    rng = np.random.default_rng(41)
+    cloud = random_cloud(rng, 250_000, extent=10.0, offset=-5.0)
+    views = [random_view(rng, cloud, width=256, height=192) for _ in range(6)]
+    grid = build_grid(cloud, 1.0)
+    unet = UNet.from_config("reduced", seed=2) if with_unet else None
+    a = FrameRenderer(grid, 256, 192, unet=unet)
+    b = FrameRenderer(grid, 256, 192, unet=unet, graph=True)
+
+    def host(o):
+        return o.copy() if with_unet else (o.rgb.copy(), o.depth.copy(), o.alpha.copy())
+
+    def same(x, y):
+        return np.array_equal(x, y) if with_unet else all(
+            np.array_equal(p, q) for p, q in zip(x, y))
+
+    ref = [host(a.render(v)) for v in views]
+    got = [host(b.render(v)) for v in views]
+    got_stream = [host(o) for o in b.render_stream(views)]
+    for r, g1, g2 in zip(ref, got, got_stream):
+        assert same(r, g1) and same(r, g2)
+    # back-to-back graph frames on one stream, last one compared
+    for v in views:
+        b.enqueue(v)
+    torch.cuda.synchronize()
+    last = b.rgb_out[0, :192].cpu().numpy() if with_unet else b.fdepth.cpu().numpy()
+    want = ref[-1] if with_unet else ref[-1][1]
+    assert np.array_equal(last, want)
+    b.check_flags()
