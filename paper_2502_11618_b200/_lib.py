@@ -20,6 +20,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # with their bounds asserts compiled in.
 LIB_PATH = os.path.join(_HERE, "liblidarsplat_cuda_debug.so"
                         if os.environ.get("LS_DEBUG_BOUNDS") == "1" else "liblidarsplat_cuda.so")
+# experiment builds (scripts/exp/*.sh) point LS_LIB_PATH at their own library
+LIB_PATH = os.environ.get("LS_LIB_PATH") or LIB_PATH
 
 LS_EINVAL = -22
 LS_TILE_POINTS = 128

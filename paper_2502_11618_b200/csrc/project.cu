@@ -552,6 +552,9 @@ __global__ void __launch_bounds__(256) k_frame_pass1_u32(SceneArgs s, ProjCam c,
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const unsigned long long key = (unsigned long long)__double_as_longlong(zc[k]);
+#ifdef LS_EXP_NO_RED1  // timing experiment only (scripts/exp): wrong frames
+            if (key == 1ull)
+#endif
             if (pix[k] != kNoPixel && key < cur[k]) {
                 LS_ASSERT((int64_t)pix[k] < c.w * c.h);
                 red_min_u64(minz + pix[k], key);
@@ -663,6 +666,9 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
         for (int k = 0; k < 4; ++k)
             if (pix[k] != kNoPixel) {
                 LS_ASSERT((int64_t)pix[k] < c.w * c.h);
+#ifdef LS_EXP_NO_RED2  // timing experiment only (scripts/exp): wrong frames
+                if (sum[k][3] == 1000u)
+#endif
                 red_add_v4c(acc + 4 * (size_t)pix[k], (float)sum[k][0], (float)sum[k][1],
                             (float)sum[k][2], (float)sum[k][3]);
             }
