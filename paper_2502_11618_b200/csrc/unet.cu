@@ -1626,7 +1626,16 @@ static bool mt2_enabled() {
     return r == 1;
 }
 
+// A/B knobs of the tile shape (defaults = the product shapes):
+//   LS_CONV_N256=128   256-output-channel layers on 128-column tiles
+//   LS_CONV_MT128=2    128-column tiles with two 128-pixel sub-tiles per item
+static int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+}
+
 static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transposed) {
+    if (bn == 128 && !transposed && env_int("LS_CONV_MT128", 1) == 2) return 2;
     const int mt = default_mt(bn);
     if (bn == 256 && mt == 1 && !transposed && mt2_enabled()) {
         const int items2 = ((w + kTW - 1) / kTW) * ((h + 2 * kTH - 1) / (2 * kTH)) * batch * n_tiles_n;
@@ -1888,6 +1897,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     int bn = n_total >= 256 ? 256 : (n_total >= 128 ? 128 : (n_total >= 64 ? 64 : 32));
     if (n_total % bn) bn = 32;
+    if (bn == 256 && n_total == 256 && !transposed && !d_head_w &&
+        env_int("LS_CONV_N256", 256) == 128)
+        bn = 128;
     {
         // small grids (the 1/16-resolution bottleneck): 128-column tiles when
         // 256-column ones leave SMs idle (LS_CONV_SMALLN=0 keeps 256)
@@ -2034,6 +2046,8 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     LS_CASE(256, 16) LS_CASE(256, 32)
 #undef LS_CASE
     if (pl->bn == 256 && pl->chunk == 32 && pl->mt == 2) return launch_p<256, 32, 2>(pl, st);
+    if (pl->bn == 128 && pl->chunk == 64 && pl->mt == 2) return launch_p<128, 64, 2>(pl, st);
+    if (pl->bn == 128 && pl->chunk == 32 && pl->mt == 2) return launch_p<128, 32, 2>(pl, st);
     if (pl->bn == 256 && pl->chunk == 16 && pl->mt == 2) return launch_p<256, 16, 2>(pl, st);
     return LS_EINVAL;
 }

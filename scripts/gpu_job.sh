@@ -1,2 +1,3 @@
-python -m pytest tests/test_gpu_projection.py tests/test_gpu_configs.py tests/test_gpu_engine.py tests/test_gpu_shard.py -x -q -k "not full_resolution" 2>&1 | tail -2
-for i in 1 2; do python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); s=d['stages_ms']; print(round(d['value'],1), 'pass1', round(s['pass1']*1e3,1), 'pass2', round(s['pass2']*1e3,1), 'frac', round(d['roofline']['other']['frac'],3))"; done
+for cfg in "" "LS_CONV_N256=128" "LS_CONV_N256=128 LS_CONV_MT128=2" "LS_CONV_MT128=2"; do
+  for r in 1 2; do echo "[$cfg] $(env $cfg python scripts/time_unet.py 2>&1 | tail -1)"; done
+done
