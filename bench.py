@@ -426,6 +426,12 @@ def run_b200(args):
 
     rep_ms, rep_clk = _timed(world, frames, None if sharded else ClockSampler(local))
     nst = 5
+    # the instrumented pass launches kernel by kernel (events between stages;
+    # graph mode replays whole frames): warm that path up first, so first-use
+    # plan creation on this stream is not inside a measured stage
+    for cam in seq[:3]:
+        renderer.enqueue(cam, events=[torch.cuda.Event(enable_timing=True) for _ in range(nst)])
+    torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst + 1)] for _ in seq]
     for cam, e in zip(seq, evs):
         e[0].record()
