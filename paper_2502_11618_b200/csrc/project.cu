@@ -184,13 +184,14 @@ constexpr uint32_t kMixed = 0x80000000u;
 __global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *__restrict__ bits,
                                                    uint32_t *__restrict__ list,
                                                    uint32_t *__restrict__ count) {
+    // one list append (atomicAdd) per CTA and 256 tiles, not per warp: the
+    // counter is a single address, so per-warp appends serialise in L2
+    __shared__ uint32_t wcount[8], cta_off;
     pdl_wait();
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31);
-         base < s.n_tiles;
-         base += stride) {
-        const int64_t t = base + lane;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < s.n_tiles;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = base + threadIdx.x;
         bool keep_any = false, cull_any = false;
         if (t < s.n_tiles) {
             const int c0 = __ldg(s.tile_c0 + t), c1 = __ldg(s.tile_c1 + t);
@@ -201,13 +202,24 @@ __global__ void __launch_bounds__(256) k_tile_list(SceneArgs s, const uint32_t *
             }
         }
         const uint32_t vote = __ballot_sync(0xffffffffu, keep_any);
-        if (vote == 0u) continue;
-        uint32_t off = 0;
-        if (lane == 0) off = atomicAdd(count, (uint32_t)__popc(vote));
-        off = __shfl_sync(0xffffffffu, off, 0);
-        LS_ASSERT(off + (uint32_t)__popc(vote) <= (uint32_t)s.n_tiles);
-        if (keep_any)
-            list[off + __popc(vote & ((1u << lane) - 1u))] = (uint32_t)t | (cull_any ? kMixed : 0u);
+        if (lane == 0) wcount[wid] = (uint32_t)__popc(vote);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t c = wcount[w];
+                wcount[w] = tot;  // exclusive warp offsets
+                tot += c;
+            }
+            cta_off = tot ? atomicAdd(count, tot) : 0u;
+        }
+        __syncthreads();
+        if (keep_any) {
+            const uint32_t pos = cta_off + wcount[wid] + __popc(vote & ((1u << lane) - 1u));
+            LS_ASSERT(pos < (uint32_t)s.n_tiles);
+            list[pos] = (uint32_t)t | (cull_any ? kMixed : 0u);
+        }
+        __syncthreads();  // wcount / cta_off are rewritten by the next iteration
     }
     pdl_trigger();
 }
