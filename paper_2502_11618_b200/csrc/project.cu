@@ -709,12 +709,12 @@ __global__ void __launch_bounds__(256) k_tile_list_views(SceneArgs s,
                                                          uint32_t *__restrict__ list,
                                                          uint32_t *__restrict__ status,
                                                          uint32_t *__restrict__ count) {
+    __shared__ uint32_t wcount[8], cta_off;  // one append per CTA (see k_tile_list)
     pdl_wait();
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~int64_t(31);
-         base < s.n_tiles; base += stride) {
-        const int64_t t = base + lane;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < s.n_tiles;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = base + threadIdx.x;
         uint32_t st = 0u;
         if (t < s.n_tiles) {
             const int c0 = __ldg(s.tile_c0 + t), c1 = __ldg(s.tile_c1 + t);
@@ -730,15 +730,24 @@ __global__ void __launch_bounds__(256) k_tile_list_views(SceneArgs s,
             }
         }
         const uint32_t vote = __ballot_sync(0xffffffffu, st != 0u);
-        if (vote == 0u) continue;
-        uint32_t off = 0;
-        if (lane == 0) off = atomicAdd(count, (uint32_t)__popc(vote));
-        off = __shfl_sync(0xffffffffu, off, 0);
+        if (lane == 0) wcount[wid] = (uint32_t)__popc(vote);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < 8; ++w) {
+                const uint32_t c = wcount[w];
+                wcount[w] = tot;
+                tot += c;
+            }
+            cta_off = tot ? atomicAdd(count, tot) : 0u;
+        }
+        __syncthreads();
         if (st != 0u) {
-            const uint32_t at = off + __popc(vote & ((1u << lane) - 1u));
+            const uint32_t at = cta_off + wcount[wid] + __popc(vote & ((1u << lane) - 1u));
             list[at] = (uint32_t)t;
             status[at] = st;
         }
+        __syncthreads();
     }
     pdl_trigger();
 }
