@@ -709,26 +709,28 @@ __global__ void __launch_bounds__(256) k_filter_final_sweep(
     const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
     if (cx >= cw || cy >= ch) return;
-    int64_t q[4];
-    float d[4], c[4][3];
-    uint8_t a[4];
-    int n = 0;
+    const int64_t x = 2 * cx;
+    // both children of a row move as one 8 B (depth, rgb) / 2 B (alpha, keep)
+    // access when the width is even (the common case); else per child
+    const bool pair = x + 1 < fw && (fw & 1) == 0;
+    float d[2][2], c[2][2][3];
+    uint8_t a[2][2];
+    int rows = 0;
+#pragma unroll
     for (int dy = 0; dy < 2; ++dy) {
         const int64_t y = 2 * cy + dy;
         if (y >= fh) break;
+        ++rows;
+        const int64_t p = y * fw + x;
+#pragma unroll
         for (int dx = 0; dx < 2; ++dx) {
-            const int64_t x = 2 * cx + dx;
-            if (x >= fw) break;
-            const int64_t p = y * fw + x;
-            q[n] = p;
-            d[n] = depth[p];
+            const bool in = x + dx < fw;
+            d[dy][dx] = in ? depth[p + dx] : 0.0f;
             if (rgb) {
-                c[n][0] = rgb[3 * p];
-                c[n][1] = rgb[3 * p + 1];
-                c[n][2] = rgb[3 * p + 2];
-                a[n] = alpha[p];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) c[dy][dx][q] = in ? rgb[3 * (p + dx) + q] : 0.0f;
+                a[dy][dx] = in ? alpha[p + dx] : (uint8_t)0;
             }
-            ++n;
         }
     }
     const int64_t hw = fh * fw;
@@ -737,19 +739,46 @@ __global__ void __launch_bounds__(256) k_filter_final_sweep(
         const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
         const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
         const double fs = sw.fs[k];
-        for (int j = 0; j < n; ++j) {
-            const int64_t o = k * hw + q[j];
-            const bool kq = keep_test(sentinel(d[j]), ref, fs);
-            if (keep_out) keep_out[o] = (uint8_t)kq;
-            if (!rgb) continue;
-            const float m = kq ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
-            if (frgb) {
-                frgb[3 * o] = c[j][0] * m;
-                frgb[3 * o + 1] = c[j][1] * m;
-                frgb[3 * o + 2] = c[j][2] * m;
+        for (int dy = 0; dy < rows; ++dy) {
+            const int64_t o = k * hw + (2 * cy + dy) * fw + x;
+            bool kq[2];
+            float m[2];
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                kq[dx] = keep_test(sentinel(d[dy][dx]), ref, fs);
+                m[dx] = kq[dx] ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
             }
-            if (fdepth) fdepth[o] = d[j] * m;
-            if (falpha) falpha[o] = (uint8_t)(a[j] * (uint8_t)kq);
+            if (pair) {
+                if (keep_out) *reinterpret_cast<uchar2 *>(keep_out + o) = make_uchar2(kq[0], kq[1]);
+                if (!rgb) continue;
+                if (frgb) {
+                    float2 *w2 = reinterpret_cast<float2 *>(frgb + 3 * o);
+                    w2[0] = make_float2(c[dy][0][0] * m[0], c[dy][0][1] * m[0]);
+                    w2[1] = make_float2(c[dy][0][2] * m[0], c[dy][1][0] * m[1]);
+                    w2[2] = make_float2(c[dy][1][1] * m[1], c[dy][1][2] * m[1]);
+                }
+                if (fdepth)
+                    *reinterpret_cast<float2 *>(fdepth + o) =
+                        make_float2(d[dy][0] * m[0], d[dy][1] * m[1]);
+                if (falpha)
+                    *reinterpret_cast<uchar2 *>(falpha + o) =
+                        make_uchar2((uint8_t)(a[dy][0] * (uint8_t)kq[0]),
+                                    (uint8_t)(a[dy][1] * (uint8_t)kq[1]));
+                continue;
+            }
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                if (x + dx >= fw) break;
+                if (keep_out) keep_out[o + dx] = (uint8_t)kq[dx];
+                if (!rgb) continue;
+                if (frgb) {
+                    frgb[3 * (o + dx)] = c[dy][dx][0] * m[dx];
+                    frgb[3 * (o + dx) + 1] = c[dy][dx][1] * m[dx];
+                    frgb[3 * (o + dx) + 2] = c[dy][dx][2] * m[dx];
+                }
+                if (fdepth) fdepth[o + dx] = d[dy][dx] * m[dx];
+                if (falpha) falpha[o + dx] = (uint8_t)(a[dy][dx] * (uint8_t)kq[dx]);
+            }
         }
     }
     pdl_trigger();

@@ -27,7 +27,7 @@ ap.add_argument("--batched-projection", type=int, default=1,
                 help="1: one multi-view pass pair per U-Net batch (ls_frame_project_views)")
 a = ap.parse_args()
 
-pos, col, _ = multi_station_hall(a.points)
+pos, col, _ = multi_station_hall(a.points, device="cuda")
 grid = build_grid(PointCloud(pos, col), 1.0)
 scene = grid.scene()
 del pos, col
