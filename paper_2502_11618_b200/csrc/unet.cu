@@ -48,6 +48,11 @@ using namespace ls::umma;
 #ifndef LS_MT256
 #define LS_MT256 1
 #endif
+// epilogue warpgroups that split ONE item's columns when an item fills TMEM
+// (256-column tiles of two sub-tiles: the single-wave deep layers)
+#ifndef LS_SPLIT_GROUPS
+#define LS_SPLIT_GROUPS 3
+#endif
 // k_conv_px2 KX2 epilogue warpgroups (A/B build switch)
 #ifndef LS_KX2_GROUPS
 #define LS_KX2_GROUPS 3
@@ -119,7 +124,11 @@ struct CfgP {
     static constexpr int kMT = MT;
     static constexpr int kItemCols = kMT * BN;                          // TMEM columns per item
     static constexpr int kAcc = 512 / kItemCols >= 4 ? 4 : 512 / kItemCols;
-    static constexpr int kEpiGroups = kAcc >= 4 ? 3 : (kAcc >= 3 ? 2 : 1);
+    // kAcc == 1: the MMA warp cannot run ahead of the epilogue, so several
+    // warpgroups drain the SAME item, each a share of its 32-column groups
+    static constexpr bool kSplit = kAcc == 1 && LS_SPLIT_GROUPS > 1;
+    static constexpr int kEpiGroups =
+        kSplit ? LS_SPLIT_GROUPS : (kAcc >= 4 ? 3 : (kAcc >= 3 ? 2 : 1));
     static constexpr int kThreads = 64 + 128 * kEpiGroups;
     static constexpr int kTmemCols = kAcc * kItemCols <= 32 ? 32 :
                                      (kAcc * kItemCols <= 64 ? 64 :
@@ -267,6 +276,9 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mY,
     const ConvParamsP p) {
     using C = CfgP<BN, CHUNK, MT_>;
+    if constexpr (C::kSplit && !(MODE == kPlain || MODE == kPool)) {
+        __trap();  // never planned: transposed tiles cap at 128 columns, heads use k_conv_px2
+    }
     constexpr int KYS = MODE == kTransposed ? 1 : 3;
     constexpr int MT = C::kMT;
     constexpr int kTileH = kTH * MT;
@@ -301,7 +313,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             }
             for (int a = 0; a < C::kAcc; ++a) {
                 mbar_init(tfull + a, 1);
-                mbar_init(tempty + a, 4);
+                mbar_init(tempty + a, 4 * (C::kSplit ? C::kEpiGroups : 1));
             }
             mbar_init(bres, 1);
             fence_barrier_init();
@@ -434,11 +446,14 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
         const float slope = act_slope(p.act, p.alpha);
         const f32x2 slope2 = f2(slope, slope);
         const float r_cout = 1.0f / (float)p.cout;
-        uint32_t acc = (uint32_t)eg;
+        // items per group: every kEpiGroups-th item, or (kSplit) every item
+        constexpr int kItemGroups = C::kSplit ? 1 : C::kEpiGroups;
+        const int eg_item = C::kSplit ? 0 : eg;
+        uint32_t acc = (uint32_t)eg_item;
         ItemWalk walk;
-        walk.init(p, blockIdx.x + eg * gridDim.x, C::kEpiGroups * gridDim.x);
-        for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
-             item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups, walk.next(p)) {
+        walk.init(p, blockIdx.x + eg_item * gridDim.x, kItemGroups * gridDim.x);
+        for (int item = blockIdx.x + eg_item * gridDim.x; item < p.n_items;
+             item += kItemGroups * gridDim.x, acc += kItemGroups, walk.next(p)) {
             const ItemPos ip = walk.pos(p, kTileH);
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
@@ -563,11 +578,56 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     ++u;
                 }
             };
-            int u0 = 0, g0 = 0, u1 = 0, g1 = 0;
-            adv(u1, g1);
             auto colug = [&](int u, int g) -> uint32_t {
                 return tbase + (uint32_t)(u * BN + g * 32);
             };
+            if constexpr (C::kSplit && (MODE == kPlain || MODE == kPool)) {
+                // (split epilogues keep per-column work only: no head sums, no
+                // staged transposed stores -- those plans never use these tiles)
+                // this group's steps: eg, eg + G, ... (step -> sub-tile, group)
+                constexpr int G = C::kEpiGroups;
+                auto ug = [&](int st, int &u, int &g) {
+                    u = st / ng;
+                    g = st - u * ng;
+                };
+                int st = eg, u = 0, g = 0;
+                if (st >= steps) {
+                    release();
+                } else {
+                    ug(st, u, g);
+                    tmem_ld32_async(colug(u, g), ra);
+                }
+#pragma unroll 1
+                while (st < steps) {
+                    int un = 0, gn = 0;
+                    const int sn = st + G;
+                    tmem_ld_wait(ra);
+                    if (sn < steps) {
+                        ug(sn, un, gn);
+                        tmem_ld32_async(colug(un, gn), rb);
+                    } else {
+                        release();
+                    }
+                    process(u, g, ra);
+                    if (sn >= steps) break;
+                    const int s2 = sn + G;
+                    int u2 = 0, g2 = 0;
+                    tmem_ld_wait(rb);
+                    if (s2 < steps) {
+                        ug(s2, u2, g2);
+                        tmem_ld32_async(colug(u2, g2), ra);
+                    } else {
+                        release();
+                    }
+                    process(un, gn, rb);
+                    st = s2;
+                    u = u2;
+                    g = g2;
+                }
+                continue;
+            }
+            int u0 = 0, g0 = 0, u1 = 0, g1 = 0;
+            adv(u1, g1);
             tmem_ld32_async(colug(0, 0), ra);
 #pragma unroll 1
             for (int s = 0; s < steps; s += 2) {

@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_projection.py tests/test_gpu_configs.py tests/test_gpu_shard.py tests/test_gpu_checked.py -x -q -k "not full_resolution" 2>&1 | tail -2
-for i in 1 2; do python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); s=d['stages_ms']; print(round(d['value'],1), {k: round(v*1e3,1) for k,v in s.items()})"; done
+python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -1
+for v in split1 split2 split3; do for r in 1 2; do echo "$v $(LS_LIB_PATH=scripts/exp/liblidarsplat_$v.so python scripts/time_unet.py | tail -1)"; done; done
