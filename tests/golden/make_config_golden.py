@@ -14,6 +14,7 @@ configurations bench.py measures:
   c3  100M points, 1920x1080, the 8 hall_cameras     (configs[2], N=1 headline)
   c4  400M points, 3840x2160, f=2000, 1 view; keep mask + filtered depth for
       every filter_strength of SURVEY §8(d)'s sweep  (configs[3])
+  c5  50M points, 1920x1080, 8 of the 64 orbit views (configs[4], multi-view)
 
 Per frame: the raw RGBDA frame, the default-filtered frame, the keep mask and
 the U-Net input tensor (bf16 NHWC [r,g,b,d',a,0,0,0], rows padded to 16) the
@@ -45,6 +46,9 @@ CONFIGS = {
     "c2": dict(points=20_000_000, width=1920, height=1080, f=1000.0, views=8, sweep=False),
     "c3": dict(points=100_000_000, width=1920, height=1080, f=1000.0, views=8, sweep=False),
     "c4": dict(points=400_000_000, width=3840, height=2160, f=2000.0, views=1, sweep=True),
+    # configs[4]: the first 8 of the 64 orbit poses (one GPU's views)
+    "c5": dict(points=50_000_000, width=1920, height=1080, f=1000.0, views=8, sweep=False,
+               orbit=64),
 }
 
 
@@ -89,7 +93,7 @@ def render_config(name, cfg, R, nat):
     pos, col, _ = multi_station_hall(cfg["points"])
     scene = digest(pos, col)
     print(f"{name}: scan {time.time() - t0:.0f}s {scene[:16]}", flush=True)
-    cams = hall_cameras(8, cfg["width"], cfg["height"], f=cfg["f"])[: cfg["views"]]
+    cams = hall_cameras(cfg.get("orbit", 8), cfg["width"], cfg["height"], f=cfg["f"])[: cfg["views"]]
     cloud = R.PointCloud(pos, col)
     del pos, col
     t0 = time.time()

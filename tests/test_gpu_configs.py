@@ -13,6 +13,7 @@ compared with the reference's digests (template:
 
   c2  20M points, 1920x1080, 8 views     c3  100M points, 1920x1080, 8 views
   c4  400M points, 3840x2160, 1 view + the filter_strength sweep of SURVEY §8(d)
+  c5  50M points, 1920x1080, 8 orbit views as one multi-view batch
 """
 
 from __future__ import annotations
@@ -194,3 +195,39 @@ def test_c2_default_unet_full_resolution_vs_f64_oracle():
     assert got.shape == (1080, 1920, 3)
     assert err <= 1.5e-2 and p >= 40.0
     assert err <= 2 * max(floor_err, 1e-3)
+
+
+def test_c5_multiview_batch_matches_reference():
+    """configs[4]: 8 orbit views of the 50M-point scan as ONE multi-view batch
+    (ViewBatchRenderer: one read of the culled scan for all 8 views, per-view
+    assembly/filter): every view's raw and filtered frame and keep mask equal
+    the reference's digests."""
+    import torch
+
+    from paper_2502_11618_b200.render import ViewBuffers, project_scene_views
+
+    cfg = CONFIGS["c5"]
+    grid = config_grid("c5")
+    cams = cameras(cfg)
+    w, h, k = cfg["width"], cfg["height"], len(cams)
+    dev = torch.device("cuda")
+    vb = ViewBuffers(w, h, k, dev)
+    filt = (torch.empty((k, h, w, 3), dtype=torch.float32, device=dev),
+            torch.empty((k, h, w), dtype=torch.float32, device=dev),
+            torch.empty((k, h, w), dtype=torch.uint8, device=dev))
+    keep = torch.empty((k, h, w), dtype=torch.uint8, device=dev)
+    from paper_2502_11618_b200 import FilterParams, _lib
+
+    fp = FilterParams()
+    pyr = torch.empty(int(_lib.load().ls_pyramid_floats(h, w, fp.levels_n)),
+                      dtype=torch.float32, device=dev)
+    scene = grid.scene()
+    with scene.lock:
+        project_scene_views(scene, cams, 0.01, vb, cull=True, filter_params=fp, filtered=filt,
+                            keep=keep, pyramid=pyr)
+        torch.cuda.synchronize()
+    assert int(vb.flags.max().item()) == 0
+    for v, fr in enumerate(cfg["frames"]):
+        assert digest(vb.rgb[v], vb.depth[v], vb.alpha[v]) == fr["raw"], f"view {v}: raw"
+        assert digest(filt[0][v], filt[1][v], filt[2][v]) == fr["filtered"], f"view {v}: filtered"
+        assert digest(keep[v]) == fr["keep"], f"view {v}: keep"
