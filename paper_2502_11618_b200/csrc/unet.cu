@@ -184,6 +184,14 @@ __device__ __forceinline__ void act2(f32x2 y, f32x2 slope2, float &a, float &b) 
     b = fmaxf(b, d);
 }
 
+// Output sigmoid (FE:model/grad64.ts:343) with the fast exp / divide: a few
+// ulp of f32 -- far inside the bf16 network's tolerance -- for ~1/3 of the
+// instructions of expf + an IEEE division (which were a quarter of the head
+// layer's issue slots).  exp overflow gives 1/inf = 0, underflow 1/1 = 1.
+__device__ __forceinline__ float sigmoid_fast(float z) {
+    return __fdividef(1.0f, 1.0f + __expf(-z));
+}
+
 __device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
     __nv_bfloat162 x = *reinterpret_cast<__nv_bfloat162 *>(&a);
     __nv_bfloat162 y = *reinterpret_cast<__nv_bfloat162 *>(&b);
@@ -554,7 +562,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                         const int64_t pix = ((int64_t)ip.img * p.h + gy) * p.w + gx;
                         for (int j2 = 0; j2 < p.head_c; ++j2) {
                             const float z = hacc[j2] + __ldg(p.head_b + j2);
-                            p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                            p.head_out[pix * p.head_c + j2] = sigmoid_fast(z);
                         }
                     }
                     hacc[0] = hacc[1] = hacc[2] = hacc[3] = 0.0f;
@@ -937,7 +945,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + gx;
                 for (int j2 = 0; j2 < p.head_c; ++j2) {
                     const float z = hacc[j2] + __ldg(p.head_b + j2);
-                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-z));
+                    p.head_out[pix * p.head_c + j2] = sigmoid_fast(z);
                 }
             }
         }
@@ -1396,14 +1404,31 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             }
             if (MODE == kHead && valid) {
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
+                if (p.head_c == 3) {
+                    // the pair's 6 outputs are contiguous (pix even): 3 x 8 B stores
+                    float o[6];
 #pragma unroll
-                for (int j2 = 0; j2 < 4; ++j2) {
-                    if (j2 >= p.head_c) break;
-                    float h0, h1;
-                    unf2(hacc2[j2], h0, h1);
-                    const float b = __ldg(p.head_b + j2);
-                    p.head_out[pix * p.head_c + j2] = 1.0f / (1.0f + expf(-(h0 + b)));
-                    p.head_out[(pix + 1) * p.head_c + j2] = 1.0f / (1.0f + expf(-(h1 + b)));
+                    for (int j2 = 0; j2 < 3; ++j2) {
+                        float h0, h1;
+                        unf2(hacc2[j2], h0, h1);
+                        const float b = __ldg(p.head_b + j2);
+                        o[j2] = sigmoid_fast(h0 + b);
+                        o[3 + j2] = sigmoid_fast(h1 + b);
+                    }
+                    float2 *dst = reinterpret_cast<float2 *>(p.head_out + pix * 3);
+                    dst[0] = make_float2(o[0], o[1]);
+                    dst[1] = make_float2(o[2], o[3]);
+                    dst[2] = make_float2(o[4], o[5]);
+                } else {
+#pragma unroll
+                    for (int j2 = 0; j2 < 4; ++j2) {
+                        if (j2 >= p.head_c) break;
+                        float h0, h1;
+                        unf2(hacc2[j2], h0, h1);
+                        const float b = __ldg(p.head_b + j2);
+                        p.head_out[pix * p.head_c + j2] = sigmoid_fast(h0 + b);
+                        p.head_out[(pix + 1) * p.head_c + j2] = sigmoid_fast(h1 + b);
+                    }
                 }
             }
             // next item of this group: kEpiGroups buffers further on
