@@ -64,6 +64,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
                                   int32_t head_c, float *d_head_out, int32_t *status);
 int ls_conv_plan_launch(const ls_conv_plan *plan, void *stream);
 
+/* Visit the plan's output tiles in reverse order (last tile first).  Plans of
+ * consecutive layers alternating direction consume their producer's most
+ * recently written -- still L2-resident -- rows first.  Results unchanged. */
+int ls_conv_plan_set_reverse(ls_conv_plan *pl, int32_t reverse);
+
 /* Row bands: restrict a plan to the output rows [row_begin, row_end) of its
  * grid (input rows for transposed convs), row_begin a multiple of
  * ls_conv_plan_tile_rows(plan); the inputs are still read from the whole

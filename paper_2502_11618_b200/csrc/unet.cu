@@ -73,6 +73,7 @@ struct ConvParamsP {
     int batch, h, w;
     int tiles_x, tiles_y, n_tiles_m, n_tiles_n, n_items;
     int ty0;                // first tile row of a row band (ls_conv_plan_set_rows)
+    int reverse;            // walk the tiles bottom-right first (ls_conv_plan_set_reverse)
     int c0, c1, ctot, nq0, nq;
     int kxs, kxps, pad;     // kx taps, kx taps per pipeline stage (1 or kxs)
     int n_total, cout, act;
@@ -268,12 +269,18 @@ struct ItemWalk {
         ty -= c * p.tiles_y;
         img += s_img + c;
     }
+    // tile coordinates in traversal order: reversed plans visit the last tile
+    // first, so a layer consumes its producer's most recently written (still
+    // L2-resident) rows first when consecutive layers alternate direction
+    __device__ int TX(const ConvParamsP &p) const { return p.reverse ? p.tiles_x - 1 - tx : tx; }
+    __device__ int TY(const ConvParamsP &p) const { return p.reverse ? p.tiles_y - 1 - ty : ty; }
+    __device__ int IMG(const ConvParamsP &p) const { return p.reverse ? p.batch - 1 - img : img; }
     __device__ ItemPos pos(const ConvParamsP &p, int tile_h) const {
         ItemPos ip;
         ip.nt = nt;
-        ip.img = img;
-        ip.y0 = (p.ty0 + ty) * tile_h;
-        ip.x0 = tx * kTW;
+        ip.img = IMG(p);
+        ip.y0 = (p.ty0 + TY(p)) * tile_h;
+        ip.x0 = TX(p) * kTW;
         return ip;
     }
 };
@@ -782,7 +789,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
             ItemWalk walk;
             walk.init(p, blockIdx.x, gridDim.x);
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
-                const int img = walk.img, x0 = walk.tx * kKxCols, y0 = (p.ty0 + walk.ty) * kTH;
+                const int img = walk.IMG(p), x0 = walk.TX(p) * kKxCols, y0 = (p.ty0 + walk.TY(p)) * kTH;
                 for (int q = 0; q < p.nq; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
@@ -841,7 +848,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
         walk.init(p, blockIdx.x + eg * gridDim.x, C::kEpiGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += C::kEpiGroups * gridDim.x, acc += C::kEpiGroups, walk.next(p)) {
-            const int img = walk.img, x0 = walk.tx * kKxCols, y0 = (p.ty0 + walk.ty) * kTH;
+            const int img = walk.IMG(p), x0 = walk.TX(p) * kKxCols, y0 = (p.ty0 + walk.TY(p)) * kTH;
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
@@ -1113,8 +1120,8 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             ItemWalk walk;
             walk.init(p, blockIdx.x, gridDim.x);
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
-                const int img = walk.img, px0 = walk.tx * kPxCols - 1,
-                          y0 = (p.ty0 + walk.ty) * kTH;
+                const int img = walk.IMG(p), px0 = walk.TX(p) * kPxCols - 1,
+                          y0 = (p.ty0 + walk.TY(p)) * kTH;
                 for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     mbar_wait(empty + s, ph ^ 1u);
                     mbar_expect_tx(full + s, p.a_tx);
@@ -1229,7 +1236,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
         walk.init(p, blockIdx.x + eg * gridDim.x, kGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
              item += kGroups * gridDim.x, walk.next(p)) {
-            const int img = walk.img, px0 = walk.tx * kPxCols - 1, y0 = (p.ty0 + walk.ty) * kTH;
+            const int img = walk.IMG(p), px0 = walk.TX(p) * kPxCols - 1, y0 = (p.ty0 + walk.TY(p)) * kTH;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
@@ -2138,6 +2145,12 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
 }
 
 void ls_conv_plan_destroy(ls_conv_plan *pl) { delete pl; }
+
+int ls_conv_plan_set_reverse(ls_conv_plan *pl, int32_t reverse) {
+    if (!pl) return LS_EINVAL;
+    pl->p.reverse = reverse ? 1 : 0;
+    return 0;
+}
 
 int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) {
     if (!pl) return LS_EINVAL;

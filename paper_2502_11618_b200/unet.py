@@ -23,6 +23,7 @@ once per resolution (TMA descriptors encoded at plan time).
 from __future__ import annotations
 
 import base64
+import os
 import json
 import math
 from dataclasses import asdict, dataclass
@@ -468,6 +469,12 @@ class UNet:
                 mk(B[("d1", s)], c, None, 0, hs, ws, L[f"dec{s}_conv2"], 2,
                    head=(fc["w"], fc["b"], cfg.outChannels, out))
             cur, ccur = B[("d2", s)], c
+        if nb == 1 and os.environ.get("LS_UNET_ALTERNATE", "1") != "0":
+            # consecutive layers walk their tiles in opposite directions, so each
+            # layer starts on the rows its producer wrote last (still in L2)
+            for i, pl in enumerate(plans):
+                if i % 2:
+                    _lib.check(lib.ls_conv_plan_set_reverse(pl, 1), "conv_plan_set_reverse")
         entry = _Plans(lib, plans)
         self._plans[key] = entry
         return entry

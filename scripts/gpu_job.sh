@@ -1,5 +1,3 @@
-# round-2 checkpoint 2: full GPU suite, default bench (100M), launch list, one --set full of the top kernels
-python -m pytest tests -m gpu -q > gpurun_out/r02_gpu_suite2.log 2>&1; tail -2 gpurun_out/r02_gpu_suite2.log
-python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench_100m_v2.json 2> gpurun_out/r02_bench_100m_v2.err; tail -c 300 gpurun_out/r02_bench_100m_v2.json
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/r02_frame_launches_v2.csv python scripts/profile_frame.py --points 100000000 --frames 3 --unet default > /dev/null 2>&1; echo launches $?
-ncu --set full --import-source on --clock-control none -k regex:"k_conv_px2|k_frame_pass" --launch-skip 6 --launch-count 6 -o gpurun_out/r02_top_full python scripts/profile_frame.py --points 100000000 --frames 3 --unet default > gpurun_out/r02_top_full.log 2>&1; echo full $?
+python -m pytest tests/test_gpu_unet.py tests/test_gpu_engine.py -x -q 2>&1 | tail -1
+for a in 0 1; do for r in 1 2; do echo "alternate=$a $(LS_UNET_ALTERNATE=$a python scripts/time_unet.py | tail -1)"; done; done
+for a in 0 1; do LS_UNET_ALTERNATE=$a python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bench alt=$a', round(d['value'],1), round(d['stages_ms']['unet']*1e3,1))"; done
