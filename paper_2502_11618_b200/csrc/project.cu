@@ -307,13 +307,32 @@ struct TileRing {
     static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8 + 4);
 };
 
+// The scan / cache streams of the passes are read once per frame: tag them
+// L2 evict-first so they do not displace the per-pixel minz / accumulator
+// lines (~50 MB at 1080p) that every candidate's gather and atomic hits.
+// LS_PASS_L2HINT=0 (A/B) drops the hint.
+__device__ __forceinline__ uint64_t stream_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
-                                         uint64_t *bar) {
+                                         uint64_t *bar, uint64_t policy) {
+#ifdef LS_NO_PASS_L2HINT
+    (void)policy;
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
             "r"(umma::smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(umma::smem_u32(bar))
         : "memory");
+#else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(umma::smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(umma::smem_u32(bar)), "l"(policy)
+        : "memory");
+#endif
 }
 
 // What the body of a pass sees for one work item.
@@ -361,6 +380,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         }
         return __shfl_sync(0xffffffffu, ecur, (int)(j & 31));
     };
+    const uint64_t pol = stream_policy();
     auto issue = [&](uint32_t e, int64_t j, int q) {  // lane 0 only
         const int64_t tile = e & ~kMixed;
         ents[q] = e;
@@ -374,10 +394,11 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         umma::mbar_expect_tx(&bars[q], R::kMain + (rgb ? kColBytes : 0));
         uint8_t *dst = ring + q * R::kStage;
         if (MODE == kCacheRgb)
-            bulk_g2s(dst, cache + (w0 + j * nw) * (kCacheBytes / 4), kCacheBytes, &bars[q]);
+            bulk_g2s(dst, cache + (w0 + j * nw) * (kCacheBytes / 4), kCacheBytes, &bars[q], pol);
         else if (MODE != kRgb)
-            bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q]);
-        if (rgb) bulk_g2s(dst + R::kMain, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q]);
+            bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q], pol);
+        if (rgb)
+            bulk_g2s(dst + R::kMain, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q], pol);
     };
     if (lane == 0) {
         for (int q = 0; q < S; ++q) umma::mbar_init(&bars[q], 1);
