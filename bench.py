@@ -323,6 +323,7 @@ def run_sharded(args, grid, unet, cams, rank, world):
         for i in range(n):
             r.enqueue(cams[(k0 + i) % len(cams)])
         main.wait_stream(r.side)
+        main.wait_stream(r.aux)
 
     frames(0, args.warmup)
     torch.cuda.synchronize()

@@ -62,15 +62,16 @@ def merge_minz(minz_bits, group=None):
     return minz_bits
 
 
-def merge_accum(accum, root: int, group=None):
+def merge_accum(accum, root: int, group=None, async_op: bool = False):
     """Reduce SUM of the {r, g, b, count} f32 accumulators to ``root``.  Every
     field is an integer; f32 addition of integers is exact (hence order-free)
     while the sums stay below 2^24, and a sum that reached 2^24 stays >= 2^24,
-    which ls_frame_finish flags."""
+    which ls_frame_finish flags.  ``async_op``: return the collective's work
+    handle without making the current stream wait for it."""
     import torch.distributed as dist
 
-    dist.reduce(accum, dst=root, op=dist.ReduceOp.SUM, group=group)
-    return accum
+    work = dist.reduce(accum, dst=root, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
+    return work if async_op else accum
 
 
 class DistComm:
@@ -85,6 +86,11 @@ class DistComm:
 
     def reduce_sum(self, accum, root: int) -> None:
         merge_accum(accum, root, self.group)
+
+    def reduce_sum_async(self, accum, root: int):
+        """Enqueue the SUM reduce without making the current stream wait; the
+        returned work handle's ``wait()`` orders a later stream after it."""
+        return merge_accum(accum, root, self.group, async_op=True)
 
 
 class ShardedRenderer:
@@ -137,6 +143,7 @@ class ShardedRenderer:
             self.unet_in = torch.zeros((1, uh, w, unet.in_pad), dtype=torch.bfloat16, device=dev)
             self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
         self.side = torch.cuda.Stream()
+        self.aux = torch.cuda.Stream()  # non-root resets behind the async reduce
         self._consumed = [None, None]  # side-stream event: set k finished + reset
         self.frame_index = 0
         self.finished = None  # side-stream event of the last frame this rank finished
@@ -184,21 +191,39 @@ class ShardedRenderer:
             _lib.ptr(frame_cache(sc, camera)), b.accum.data_ptr(), _lib.stream_ptr()),
             "frame_pass2")
 
-    def _finish(self, k, root) -> None:
+    def _finish(self, k, root, work=None) -> None:
         """Root: assemble + filter (+ U-Net) from set k on the side stream.
-        Others: reset set k for the frame after next."""
+        Others: reset set k for the frame after next.  ``work``: the pending
+        (asynchronous) accumulator reduce of set k -- the side stream waits
+        for it, the caller's stream does not, so the reduce overlaps the next
+        frame's cull and pass 1."""
         import torch
 
         b = self.sets[k]
-        if self.rank != root:
-            b.minz.fill_(_lib.INF_BITS)
-            b.accum.zero_()
-            self._consumed[k] = None
-            return
         merged = torch.cuda.Event()
         merged.record(torch.cuda.current_stream())
+        if self.rank != root:
+            if work is None:
+                b.minz.fill_(_lib.INF_BITS)
+                b.accum.zero_()
+                self._consumed[k] = None
+                return
+            # the reset runs on its own stream: the side stream may be busy
+            # with a U-Net this rank is root of, which the next frames' passes
+            # must not wait for
+            self.aux.wait_event(merged)
+            with torch.cuda.stream(self.aux):
+                work.wait()  # the reduce has read this rank's accumulators
+                b.minz.fill_(_lib.INF_BITS)
+                b.accum.zero_()
+                done = torch.cuda.Event()
+                done.record(self.aux)
+                self._consumed[k] = done
+            return
         self.side.wait_event(merged)
         with torch.cuda.stream(self.side):
+            if work is not None:
+                work.wait()
             _lib.check(_lib.load().ls_frame_finish(
                 b.minz.data_ptr(), b.accum.data_ptr(), b.width, b.height,
                 _lib.make_filter(self.fp), b.rgb.data_ptr(), b.depth.data_ptr(),
@@ -224,12 +249,17 @@ class ShardedRenderer:
         self._project_min(camera, k)
         self.comm.all_min(self.sets[k].minz)
         self._accumulate(camera, k)
-        self.comm.reduce_sum(self.sets[k].accum, root)
-        self._finish(k, root)
+        reduce_async = getattr(self.comm, "reduce_sum_async", None)
+        if reduce_async is not None:
+            self._finish(k, root, reduce_async(self.sets[k].accum, root))
+        else:
+            self.comm.reduce_sum(self.sets[k].accum, root)
+            self._finish(k, root)
 
     def synchronize(self) -> None:
         """Wait for this rank's side-stream work (the frames it is root of)."""
         self.side.synchronize()
+        self.aux.synchronize()
 
     def check_flags(self) -> None:
         self.side.synchronize()

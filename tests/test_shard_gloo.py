@@ -48,7 +48,7 @@ def _unpack(packed):
     return packed.astype(np.uint64)
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, async_reduce=False):
     import torch
     import torch.distributed as dist
 
@@ -78,7 +78,11 @@ def _worker(rank, world, port, out):
     port_k.project_accumulate(grid.sorted_colors, ss, ee, pix, z, 0.01, gmin, acc)
     packed = torch.from_numpy(_pack(acc))
     root = 1  # not rank 0 on purpose (round-robin roots)
-    merge_accum(packed, root)
+    if async_reduce:  # ShardedRenderer's form: wait on the handle later
+        work = merge_accum(packed, root, async_op=True)
+        work.wait()
+    else:
+        merge_accum(packed, root)
     if rank == root:
         rgb, depth, alpha = O.assemble(gmin, _unpack(packed.numpy()))
         ref = O.project(grid.sorted_positions, grid.sorted_colors, s, e, cam, 0.01, port_k)
@@ -89,11 +93,12 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("async_reduce", [False, True])
 @pytest.mark.parametrize("world", [2])
-def test_sharded_merge_matches_single_process(world):
+def test_sharded_merge_matches_single_process(world, async_reduce):
     ctx = mp.get_context("spawn")
     out = ctx.Manager().list([None])
-    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), out, async_reduce), nprocs=world, join=True)
     assert out[0] is True
 
 
