@@ -234,3 +234,25 @@ def test_unet_init_matches_independent_restatement():
             assert not p[name + ".bias"].any()
         for s in range(cfg.depth):
             assert (p[f"enc{s}_bn1.moving_var"] == 1).all() and (p[f"enc{s}_bn2.gamma"] == 1).all()
+
+
+def test_f32_division_equals_reference_mean():
+    """k_assemble_pyramid's colour mean: f32(sum / (count * 255)) in f32 IEEE
+    division equals the reference's f32(f64(sum) / (f64(count) * 255.0))
+    (R:render.py:146-161) for every integer sum <= 255 * count < 2^24 --
+    exhaustively for counts up to 1024, and on 2e7 random pairs up to the
+    fast path's bound of 65,793 points per pixel."""
+    import numpy as np
+
+    rng = np.random.default_rng(5)
+    for c in range(1, 1025):
+        x = np.arange(0, 255 * c + 1)
+        got = np.float32(x) / np.float32(c * 255)
+        ref = (x / (c * 255.0)).astype(np.float32)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32)), c
+    for _ in range(4):
+        cnt = rng.integers(1, 65794, size=5_000_000)
+        x = np.minimum((rng.random(cnt.size) * (255 * cnt + 1)).astype(np.int64), 255 * cnt)
+        got = np.float32(x) / np.float32(cnt * 255)
+        ref = (x.astype(np.float64) / (cnt.astype(np.float64) * 255.0)).astype(np.float32)
+        assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
