@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-frames", type=int, default=2, help="cpu_baseline / parity frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--views", type=int, default=8, help="camera poses cycled")
+    ap.add_argument("--sharded-single", action="store_true",
+                    help="test only: run the N>1 point-shard path in a 1-rank NCCL group")
     ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
                     help="1: every frame is one CUDA-graph launch (FrameRenderer(graph=True))")
     ap.add_argument("--mode", choices=["sharded", "replicas"], default="sharded",
@@ -75,6 +77,8 @@ def bench_config(args, world):
     """The config dict both arms print (identical, so the driver can match them)."""
     par = "single" if world == 1 else (f"point-shard{world}" if args.mode == "sharded"
                                       else f"frame-replicas{world}")
+    if getattr(args, "sharded_single", False):
+        par = "point-shard1 (test)"
     return {"workload": workload_name(args), "points": args.points, "width": args.width,
             "height": args.height, "views": args.views, "parallelism": par,
             "l2": "inputs larger than L2 (scan 15 B/pt)"}
@@ -322,6 +326,7 @@ def run_sharded(args, grid, unet, cams, rank, world):
     def frames(k0, n):
         for i in range(n):
             r.enqueue(cams[(k0 + i) % len(cams)])
+        r.flush()  # frames are pipelined by one stage: complete the last one
         main.wait_stream(r.side)
         main.wait_stream(r.aux)
 
@@ -334,16 +339,24 @@ def run_sharded(args, grid, unet, cams, rank, world):
     host = torch.empty((args.height, args.width, 3), dtype=torch.float32, pin_memory=True)
     copies = []
 
+    def copy_out(root):
+        if root == rank:  # behind the frame's finish on the side stream
+            with torch.cuda.stream(r.side):
+                src = r.rgb_out[0, : args.height] if unet is not None else r.frgb
+                host.copy_(src, non_blocking=True)
+                copies.append(1)
+
     def e2e_frames():
+        prev_root = None
         for i in range(args.steps):
             root = r.frame_index % world
-            r.enqueue(cams[(args.warmup + i) % len(cams)])
-            if root == rank:
-                with torch.cuda.stream(r.side):
-                    src = r.rgb_out[0, : args.height] if unet is not None else r.frgb
-                    host.copy_(src, non_blocking=True)
-                    copies.append(1)
-        r.side.synchronize()
+            r.enqueue(cams[(args.warmup + i) % len(cams)])  # completes the previous frame
+            if prev_root is not None:
+                copy_out(prev_root)
+            prev_root = root
+        r.flush()
+        copy_out(prev_root)
+        r.synchronize()
         torch.cuda.synchronize()
 
     if world > 1:
@@ -367,10 +380,18 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded_single:
         import torch.distributed as dist
 
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # comm init lines (nranks) in the log
+        if args.sharded_single and "MASTER_ADDR" not in os.environ:
+            import socket
+
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]),
+                              RANK="0", WORLD_SIZE="1")
+            sk.close()
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     pos, col, cams = make_scene(args, device="cuda")
     cloud = PointCloud(pos, col)
@@ -387,7 +408,7 @@ def run_b200(args):
         n_cand.append(int((e - s).sum()))
     hbm, bf16, bf16s, peak_kind = measured_peaks()
     traffic, traffic_src = traffic_profile()
-    sharded = world > 1 and args.mode == "sharded"
+    sharded = (world > 1 and args.mode == "sharded") or args.sharded_single
     line = {"metric": METRIC, "unit": "frames/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None,
@@ -502,7 +523,7 @@ def run_b200(args):
     if sharded:
         rep.update({"scaling": "weak", "parallelism": f"frame-replicas{world}"})
         line["replicas"] = rep
-        line["projection_roofline_single_rank"] = roofline
+        line["roofline_single_rank"] = roofline
     else:
         line.update(rep)
         line["clocks"] = rep_clk

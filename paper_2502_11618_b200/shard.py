@@ -84,6 +84,12 @@ class DistComm:
     def all_min(self, minz_bits) -> None:
         merge_minz(minz_bits, self.group)
 
+    def all_min_async(self, minz_bits):
+        """All-reduce MIN without making the current stream wait (work handle)."""
+        import torch.distributed as dist
+
+        return dist.all_reduce(minz_bits, op=dist.ReduceOp.MIN, group=self.group, async_op=True)
+
     def reduce_sum(self, accum, root: int) -> None:
         merge_accum(accum, root, self.group)
 
@@ -96,12 +102,18 @@ class DistComm:
 class ShardedRenderer:
     """FrameRenderer over one shard of the scan, merged across ranks.
 
-    Streams: cull, passes and both collectives run on the caller's stream;
-    the root's assemble/filter/U-Net run on a side stream, so the next frame's
-    projection (and its collectives, in which every rank takes part) never
-    waits for a U-Net.  The per-frame pass buffers (minz, accum) alternate
-    between two sets; set k is reused only after the side stream has consumed
-    (and reset) it.
+    Streams: cull and passes run on the caller's stream, the collectives on
+    NCCL's stream; the root's assemble/filter/U-Net run on a side stream, so
+    the next frame's projection (and its collectives, in which every rank
+    takes part) never waits for a U-Net.  Frames are software-pipelined by one
+    stage: ``enqueue(camera_i)`` culls and runs pass 1 of frame i, starts its
+    minz all-reduce asynchronously, and only then runs pass 2 of frame i-1
+    (after waiting for ITS all-reduce) and starts frame i-1's accumulator
+    reduce -- so each MIN all-reduce overlaps the next frame's pass 1 and each
+    SUM reduce the frame after's.  ``flush()`` completes the last frame.  The
+    pass buffers rotate over three sets (a set is reused only after its frame
+    was consumed and reset) and the cull / work-list / pass-1 cache scratch
+    over two.
 
     A frame is three phases around the two collectives -- ``_project_min``
     (cull, work list, pass 1), ``_accumulate`` (pass 2 against the merged
@@ -128,7 +140,9 @@ class ShardedRenderer:
         self.scene = DeviceScene(full.positions[start:end], full.colors[start:end], offs,
                                  grid.origin, grid.cell_size, grid.dims)
         self.scratch = self.scene.scratch  # the shard scene is this renderer's own
-        self.sets = [FrameBuffers(width, height, self.device) for _ in range(2)]
+        # frame i's pass 2 runs after frame i+1's pass 1: two scratch sets
+        self.scratches = [self.scene.scratch, self.scene.new_scratch()]
+        self.sets = [FrameBuffers(width, height, self.device) for _ in range(3)]
         self.bufs = self.sets[0]
         h, w, dev = self.height, self.width, self.device
         self.frgb = torch.empty((h, w, 3), dtype=torch.float32, device=dev)
@@ -144,7 +158,8 @@ class ShardedRenderer:
             self.rgb_out = torch.empty((1, uh, w, 3), dtype=torch.float32, device=dev)
         self.side = torch.cuda.Stream()
         self.aux = torch.cuda.Stream()  # non-root resets behind the async reduce
-        self._consumed = [None, None]  # side-stream event: set k finished + reset
+        self._consumed = [None, None, None]  # event: set k finished + reset
+        self._pending = None  # (camera, set, scratch, root, all-reduce work) of the last frame
         self.frame_index = 0
         self.finished = None  # side-stream event of the last frame this rank finished
 
@@ -164,31 +179,32 @@ class ShardedRenderer:
         stream) until the set's previous frame was consumed."""
         import torch
 
-        k = self.frame_index % 2
+        k = self.frame_index % len(self.sets)
         root = self.frame_index % self.world
         self.frame_index += 1
         if self._consumed[k] is not None:
             torch.cuda.current_stream().wait_event(self._consumed[k])
         return k, root
 
-    def _project_min(self, camera, k) -> None:
-        """Cull this shard's cells, build its work list, pass 1 into set k."""
-        sc, b = self.scene, self.sets[k]
-        bits = sc.cull_bits(extract_frustum(camera).planes).data_ptr()
-        tl, tc = sc.worklist()
-        cache = _lib.ptr(frame_cache(sc, camera))
+    def _project_min(self, camera, k, si: int = 0) -> None:
+        """Cull this shard's cells, build its work list, pass 1 into set k
+        (scratch set si: cull bits, work list, pass-1 cache)."""
+        sc, b, scr = self.scene, self.sets[k], self.scratches[si]
+        bits = sc.cull_bits(extract_frustum(camera).planes, scratch=scr).data_ptr()
+        tl, tc = sc.worklist(scr)
+        cache = _lib.ptr(frame_cache(sc, camera, scr))
         _lib.check(_lib.load().ls_frame_pass1(sc.struct, bits, tl.data_ptr(), tc.data_ptr(),
                                               _lib.make_camera(camera), b.minz.data_ptr(), cache,
                                               _lib.stream_ptr()), "frame_pass1")
 
-    def _accumulate(self, camera, k) -> None:
+    def _accumulate(self, camera, k, si: int = 0) -> None:
         """Pass 2 of this shard against set k's (merged) minimum."""
-        sc, b = self.scene, self.sets[k]
+        sc, b, scr = self.scene, self.sets[k], self.scratches[si]
         _lib.check(_lib.load().ls_frame_pass2(
-            sc.struct, sc.keep_bits.data_ptr(), sc.tile_list.data_ptr(),
-            sc.tile_count.data_ptr(), _lib.make_camera(camera),
+            sc.struct, scr.keep_bits.data_ptr(), scr.tile_list.data_ptr(),
+            scr.tile_count.data_ptr(), _lib.make_camera(camera),
             float(self.rp.zbuffer_epsilon_rel), b.minz.data_ptr(),
-            _lib.ptr(frame_cache(sc, camera)), b.accum.data_ptr(), _lib.stream_ptr()),
+            _lib.ptr(frame_cache(sc, camera, scr)), b.accum.data_ptr(), _lib.stream_ptr()),
             "frame_pass2")
 
     def _finish(self, k, root, work=None) -> None:
@@ -244,11 +260,32 @@ class ShardedRenderer:
             self.finished = fin
 
     def enqueue(self, camera) -> None:
-        """Enqueue one frame (this rank's share) on the current stream."""
+        """Enqueue one frame (this rank's share) on the current stream.  The
+        frame completes on the next ``enqueue`` or on ``flush()``."""
         k, root = self._next()
-        self._project_min(camera, k)
-        self.comm.all_min(self.sets[k].minz)
-        self._accumulate(camera, k)
+        si = (self.frame_index - 1) % 2
+        self._project_min(camera, k, si)
+        all_min_async = getattr(self.comm, "all_min_async", None)
+        if all_min_async is not None:
+            work = all_min_async(self.sets[k].minz)
+        else:
+            self.comm.all_min(self.sets[k].minz)
+            work = None
+        prev, self._pending = self._pending, (camera, k, si, root, work)
+        if prev is not None:
+            self._complete(prev)
+
+    def flush(self) -> None:
+        """Complete the last enqueued frame (its pass 2, reduce and finish)."""
+        if self._pending is not None:
+            prev, self._pending = self._pending, None
+            self._complete(prev)
+
+    def _complete(self, pending) -> None:
+        camera, k, si, root, work = pending
+        if work is not None:
+            work.wait()  # the current stream waits for the frame's MIN all-reduce
+        self._accumulate(camera, k, si)
         reduce_async = getattr(self.comm, "reduce_sum_async", None)
         if reduce_async is not None:
             self._finish(k, root, reduce_async(self.sets[k].accum, root))
@@ -257,12 +294,17 @@ class ShardedRenderer:
             self._finish(k, root)
 
     def synchronize(self) -> None:
-        """Wait for this rank's side-stream work (the frames it is root of)."""
+        """Complete the pending frame and wait for this rank's side-stream work
+        (the frames it is root of) and its resets."""
+        self.flush()
+        import torch
+
+        torch.cuda.current_stream().synchronize()
         self.side.synchronize()
         self.aux.synchronize()
 
     def check_flags(self) -> None:
-        self.side.synchronize()
+        self.synchronize()
         bad = any(int(b.flags.item()) for b in self.sets)
         for b in self.sets:
             b.flags.zero_()

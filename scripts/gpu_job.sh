@@ -1,2 +1,1 @@
-python -m pytest tests/test_gpu_projection.py tests/test_gpu_configs.py tests/test_gpu_filter.py tests/test_gpu_views.py -x -q -k "not full_resolution" 2>&1 | tail -1
-for r in 1 2; do python bench.py --steps 30 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); s=d['stages_ms']; print(round(d['value'],1), {k: round(v*1e3,1) for k,v in s.items()})"; done
+for v in 3 1; do for r in 1 2; do echo "LS_CONV_PX2=$v $(LS_CONV_PX2=$v python scripts/time_unet.py | tail -1)"; done; done

@@ -119,6 +119,7 @@ def test_sharded_renderer_single_rank_group():
         b = FrameRenderer(grid, cam.width, cam.height, unet=unet)
         for v in views:  # root-side work runs on a side stream; compare every frame
             a.enqueue(v)
+            a.flush()  # frames are pipelined by one stage
             b.enqueue(v)
             torch.cuda.synchronize()
             assert torch.equal(a.frgb, b.frgb) and torch.equal(a.falpha, b.falpha)
@@ -164,3 +165,46 @@ def test_sharded_renderer_virtual_ranks(world):
     assert sorted(set(roots)) == list(range(world))
     for r in vs.ranks:
         r.check_flags()
+
+
+def test_sharded_renderer_pipelined_frames_single_rank():
+    """Back-to-back ShardedRenderer frames without flushing in between (each
+    frame's pass 2 runs after the next frame's pass 1, with three pass-buffer
+    sets and two scratch sets in rotation) deliver the FrameRenderer frames:
+    the root's outputs are checked after every second frame and at the end."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from lidarsplat.engine import FrameRenderer
+    from lidarsplat.shard import ShardedRenderer
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        cloud, cam, grid = _frame_setup(seed=9)
+        rng = np.random.default_rng(9)
+        views = [random_view(rng, cloud, width=cam.width, height=cam.height) for _ in range(7)]
+        a = ShardedRenderer(grid, cam.width, cam.height, 0, 1)
+        b = FrameRenderer(grid, cam.width, cam.height)
+        for i, v in enumerate(views):
+            a.enqueue(v)  # completes frame i-1
+            if i % 2 == 1:
+                a.synchronize()  # flushes frame i too
+                b.enqueue(v)
+                torch.cuda.synchronize()
+                assert torch.equal(a.frgb, b.frgb) and torch.equal(a.fdepth, b.fdepth)
+                assert torch.equal(a.falpha, b.falpha)
+        a.synchronize()
+        b.enqueue(views[-1])
+        torch.cuda.synchronize()
+        assert torch.equal(a.frgb, b.frgb) and torch.equal(a.fdepth, b.fdepth)
+        a.check_flags()
+    finally:
+        dist.destroy_process_group()
