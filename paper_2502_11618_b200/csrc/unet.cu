@@ -42,6 +42,11 @@ namespace unet {
 using namespace ls::umma;
 
 // sub-tiles per work item of the 128 / 256-column tiles (A/B build switches)
+#ifdef LS_EXP_NO_GDC
+#define LS_GDC_WAIT() ((void)0)  // timing-only experiment: layers overlap unsafely
+#else
+#define LS_GDC_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
 #ifndef LS_MT128
 #define LS_MT128 1
 #endif
@@ -285,18 +290,33 @@ struct ItemWalk {
     }
 };
 
-template <int BN, int CHUNK, int MODE, int MT_ = default_mt(BN)>
+// PAIR: a cluster of two CTAs on one TPC shares each M = 256 MMA (tcgen05
+// cta_group::2, issued by the leader): CTA r holds the A rows of sub-tile
+// rows [r*8*MT, (r+1)*8*MT) of a (16*MT)-row tile and output columns
+// [r*BN/2, (r+1)*BN/2) of the B tile, and drains its own 128 TMEM lanes x BN
+// columns.  Per SM the tensor core then reads 128 x 16 A + (BN/2) x 16 B per
+// MMA instead of 128 x 16 + BN x 16: the 1-SM 128-column layers were bound
+// by that shared-memory read traffic (A 4 KB + B 4 KB per 64-cycle MMA plus
+// the TMA fills on a 128 B/cycle SRAM).
+template <int BN, int CHUNK, int MODE, int MT_ = default_mt(BN), bool PAIR = false>
 __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mY,
     const ConvParamsP p) {
     using C = CfgP<BN, CHUNK, MT_>;
-    if constexpr (C::kSplit && !(MODE == kPlain || MODE == kPool)) {
+    if constexpr ((C::kSplit && !(MODE == kPlain || MODE == kPool)) ||
+                  (PAIR && (C::kSplit || !(MODE == kPlain || MODE == kPool)))) {
         __trap();  // never planned: transposed tiles cap at 128 columns, heads use k_conv_px2
-    }
+    } else {
     constexpr int KYS = MODE == kTransposed ? 1 : 3;
     constexpr int MT = C::kMT;
-    constexpr int kTileH = kTH * MT;
+    constexpr int kTileH = kTH * MT * (PAIR ? 2 : 1);  // rows per work item (both CTAs)
+    constexpr int kBNL = PAIR ? BN / 2 : BN;            // B columns held by this CTA
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    // work index / stride: pairs walk the items as one unit
+    const int wid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int wstride = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     extern __shared__ uint8_t smem_raw[];
     // 1024-align inside the shared window (keeps the shared address space visible)
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             }
             for (int a = 0; a < C::kAcc; ++a) {
                 mbar_init(tfull + a, 1);
-                mbar_init(tempty + a, 4 * (C::kSplit ? C::kEpiGroups : 1));
+                mbar_init(tempty + a, 4 * (C::kSplit ? C::kEpiGroups : 1) * (PAIR ? 2 : 1));
             }
             mbar_init(bres, 1);
             fence_barrier_init();
@@ -337,7 +357,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             tma_prefetch(&mB);
         }
         __syncwarp();
-        tmem_alloc(tslot, C::kTmemCols);
+        if constexpr (PAIR)
+            tmem_alloc_pair(tslot, C::kTmemCols);
+        else
+            tmem_alloc(tslot, C::kTmemCols);
     } else if (warp >= 2) {
         // stage the epilogue constants (visible after the __syncthreads below)
         const int t = threadIdx.x - 64;
@@ -351,31 +374,46 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                 sconst[2 * p.n_total + i] = p.head_w[i];
     }
     fence_before_sync();
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync_all();  // the peer signals the leader's barriers from here on
+    else
+        __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tslot;
+    // the leader's barriers as shared::cluster addresses (PAIR: both CTAs' TMA
+    // bytes complete on the leader's full / bres barriers, both CTAs' epilogues
+    // release the leader's tempty)
+    const uint32_t c_full = PAIR ? mapa_shared(full, 0) : 0u;
+    const uint32_t c_bres = PAIR ? mapa_shared(bres, 0) : 0u;
+    const uint32_t c_tempty = PAIR ? mapa_shared(tempty, 0) : 0u;
 
     if (warp == 0) {
         if (elect_one()) {
             // ------------------------------ TMA producer ------------------------------
             if (p.resident) {
-                mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk);
+                if (leader)
+                    mbar_expect_tx(bres, (uint32_t)(p.kxs * p.nq) * p.b_blk * (PAIR ? 2u : 1u));
                 for (int q = 0; q < p.nq; ++q)
                     for (int kx = 0; kx < p.kxs; ++kx) {
                         const bool second = q >= p.nq0;
                         const int kc = second ? p.c0 + (q - p.nq0) * CHUNK : q * CHUNK;
-                        tma_load_3d(smem + p.off_b + (q * p.kxs + kx) * p.b_blk, &mB, kc, 0,
-                                    kx * KYS, bres);
+                        if constexpr (PAIR)
+                            tma_load_3d_pair(smem + p.off_b + (q * p.kxs + kx) * p.b_blk, &mB, kc,
+                                             (int)rank * kBNL, kx * KYS, c_bres);
+                        else
+                            tma_load_3d(smem + p.off_b + (q * p.kxs + kx) * p.b_blk, &mB, kc, 0,
+                                        kx * KYS, bres);
                     }
             }
             // the previous layer's activations are complete and visible past here;
             // every global write of this kernel depends on loads issued after it
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            LS_GDC_WAIT();
             int s = 0;
             uint32_t ph = 0;
             ItemWalk walk;
-            walk.init(p, blockIdx.x, gridDim.x);
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
+            walk.init(p, wid, wstride);
+            const int ry = (int)rank * kTH * MT;  // this CTA's first row in the item
+            for (int item = wid; item < p.n_items; item += wstride, walk.next(p)) {
                 const ItemPos ip = walk.pos(p, kTileH);
                 for (int q = 0; q < p.nq; ++q) {
                     const bool second = q >= p.nq0;
@@ -384,31 +422,50 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                     for (int kg = 0; kg < n_kg; ++kg, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                         mbar_wait(empty + s, ph ^ 1u);
                         uint8_t *st = smem + (size_t)s * p.stage_bytes;
-                        mbar_expect_tx(full + s, p.kxps * (p.a_tx + (p.resident ? 0u : p.b_blk)));
+#ifdef LS_EXP_B_ONCE
+                        // timing-only experiment: stream the weights for the first item only
+                        const bool load_b = !p.resident && item == wid;
+#else
+                        const bool load_b = !p.resident;
+#endif
+                        if (leader)
+                            mbar_expect_tx(full + s, p.kxps * (p.a_tx + (load_b ? p.b_blk : 0u)) *
+                                                         (PAIR ? 2u : 1u));
                         for (int k = 0; k < p.kxps; ++k) {
                             const int kx = kg * p.kxps + k;
-                            tma_load_4d(st + k * p.a_bytes, ma, c, ip.x0 + kx - p.pad,
-                                        ip.y0 - p.pad, ip.img, full + s);
-                            if (!p.resident)
-                                tma_load_3d(st + p.kxps * p.a_bytes + k * p.b_blk, &mB,
-                                            (second ? p.c0 : 0) + c, ip.nt * BN, kx * KYS, full + s);
+                            if constexpr (PAIR) {
+                                const uint32_t cb = c_full + 8u * (uint32_t)s;
+                                tma_load_4d_pair(st + k * p.a_bytes, ma, c, ip.x0 + kx - p.pad,
+                                                 ip.y0 + ry - p.pad, ip.img, cb);
+                                if (load_b)
+                                    tma_load_3d_pair(st + p.kxps * p.a_bytes + k * p.b_blk, &mB,
+                                                     (second ? p.c0 : 0) + c,
+                                                     ip.nt * BN + (int)rank * kBNL, kx * KYS, cb);
+                            } else {
+                                tma_load_4d(st + k * p.a_bytes, ma, c, ip.x0 + kx - p.pad,
+                                            ip.y0 - p.pad, ip.img, full + s);
+                                if (load_b)
+                                    tma_load_3d(st + p.kxps * p.a_bytes + k * p.b_blk, &mB,
+                                                (second ? p.c0 : 0) + c, ip.nt * BN, kx * KYS,
+                                                full + s);
+                            }
                         }
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        if (elect_one()) {
+        if (leader && elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
-            const uint32_t idesc = idesc_bf16(128, BN);
+            const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BN);
             const uint64_t dproto = smem_desc(0, C::kRow, C::kLayout);
             const uint32_t dhi = (uint32_t)(dproto >> 32), dlo = (uint32_t)dproto;
             if (p.resident) mbar_wait(bres, 0);
             const uint32_t a_box16 = p.a_bytes >> 4, b_blk16 = p.b_blk >> 4;
             int s = 0;
             uint32_t ph = 0, ab = 0, aph = 0;
-            for (int item = blockIdx.x; item < p.n_items;
-                 item += gridDim.x, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
+            for (int item = wid; item < p.n_items;
+                 item += wstride, ab = ab + 1 == C::kAcc ? 0 : ab + 1, aph ^= ab == 0) {
                 mbar_wait(tempty + ab, aph ^ 1u);
                 fence_after_sync();
                 const uint32_t d0 = tmem + ab * C::kItemCols;
@@ -435,18 +492,28 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                                     for (int j = 0; j < CHUNK / 16; ++j) {
                                         const uint32_t ao =
                                             k * a_box16 + ((u * kTH + ky) * kTW * C::kRow + 32 * j) / 16;
-                                        const uint32_t bo = k * b_blk16 + (ky * BN * C::kRow + 32 * j) / 16;
-                                        mma_bf16(d0 + u * BN, ((uint64_t)dhi << 32) | (a_lo + ao),
-                                                 ((uint64_t)dhi << 32) | (b_lo + bo), idesc,
-                                                 (q | kg | k | ky | j) != 0 ? 1u : 0u);
+                                        const uint32_t bo = k * b_blk16 + (ky * kBNL * C::kRow + 32 * j) / 16;
+                                        const uint64_t ad = ((uint64_t)dhi << 32) | (a_lo + ao);
+                                        const uint64_t bd = ((uint64_t)dhi << 32) | (b_lo + bo);
+                                        const uint32_t acc = (q | kg | k | ky | j) != 0 ? 1u : 0u;
+                                        if constexpr (PAIR)
+                                            mma_bf16_pair(d0 + u * BN, ad, bd, idesc, acc);
+                                        else
+                                            mma_bf16(d0 + u * BN, ad, bd, idesc, acc);
                                     }
                                 }
                             }
                         }
-                        mma_commit(empty + s);
+                        if constexpr (PAIR)
+                            mma_commit_pair(empty + s);
+                        else
+                            mma_commit(empty + s);
                     }
                 }
-                mma_commit(tfull + ab);
+                if constexpr (PAIR)
+                    mma_commit_pair(tfull + ab);
+                else
+                    mma_commit(tfull + ab);
             }
         }
     } else {
@@ -466,9 +533,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
         const int eg_item = C::kSplit ? 0 : eg;
         uint32_t acc = (uint32_t)eg_item;
         ItemWalk walk;
-        walk.init(p, blockIdx.x + eg_item * gridDim.x, kItemGroups * gridDim.x);
-        for (int item = blockIdx.x + eg_item * gridDim.x; item < p.n_items;
-             item += kItemGroups * gridDim.x, acc += kItemGroups, walk.next(p)) {
+        walk.init(p, wid + eg_item * wstride, kItemGroups * wstride);
+        const int ry = (int)rank * kTH * MT;  // this CTA's first row in the item
+        for (int item = wid + eg_item * wstride; item < p.n_items;
+             item += kItemGroups * wstride, acc += kItemGroups, walk.next(p)) {
             const ItemPos ip = walk.pos(p, kTileH);
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
@@ -484,7 +552,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             // one 32-column group: scale/shift/act, bf16 pack, 32 B stores,
             // pooling / head as the mode asks
             auto process = [&](int u, int g, const uint32_t(&rr)[32]) {
-                const int gy = ip.y0 + u * kTH + ty;
+                const int gy = ip.y0 + ry + u * kTH + ty;
                 const bool valid = gx < p.w && gy < p.h;
                 const int n0 = ip.nt * BN + g * 32;
 #pragma unroll
@@ -580,7 +648,12 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             auto release = [&]() {
                 fence_before_sync();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(tempty + ab);
+                if (lane == 0) {
+                    if constexpr (PAIR)
+                        mbar_arrive_cluster(c_tempty + 8u * ab);
+                    else
+                        mbar_arrive(tempty + ab);
+                }
             };
             // two register buffers: group s+1's tcgen05.ld is in flight while
             // group s is processed
@@ -681,8 +754,16 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     if (MODE == kTransposed && p.stage_store && warp >= 2 && (warp & 3) == 0 && lane == 0)
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     fence_before_sync();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+    if constexpr (PAIR) {
+        // the leader's MMAs write the peer's TMEM and the peer's epilogue
+        // arrives on the leader's barriers: neither CTA leaves before both are done
+        cluster_sync_all();
+        if (warp == 0) tmem_dealloc_pair(tmem, C::kTmemCols);
+    } else {
+        __syncthreads();
+        if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+    }
+    }  // (planned modes)
 }
 
 // ---------------------------------------------------------------------------
@@ -783,7 +864,7 @@ __global__ void __launch_bounds__(CfgKx<CHUNK, COUT>::kThreads) k_conv_kx(
                         tma_load_3d(smem + p.off_b + ((q * 3 + ky) * 3 + kx) * p.b_blk, &mB, kc, 0,
                                     kx * 3 + ky, bres);
             }
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            LS_GDC_WAIT();
             int s = 0;
             uint32_t ph = 0;
             ItemWalk walk;
@@ -1114,7 +1195,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                                 tma_load_3d(smem + btile(src, ky, e, t) + r * (C::kBTile / 2), &mB,
                                             src * 32 + 16 * t, 0, kx * 3 + ky, bres);
                             }
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            LS_GDC_WAIT();
             int s = 0;
             uint32_t ph = 0;
             ItemWalk walk;
@@ -1533,6 +1614,7 @@ struct ls_conv_plan {
     int mt;    // k_conv_p: 128-pixel sub-tiles per work item
     int full_tiles_y;  // tile rows of the whole layer (row bands restrict p.ty0 / p.tiles_y)
     int kind;  // 0: k_conv_p, 1: k_conv_kx (kx taps stacked along N), 2: k_conv_px2 (pixel pairs)
+    int pair;  // k_conv_p on CTA pairs (M = 256 cta_group::2 MMAs, cluster of 2)
     size_t smem;
 };
 
@@ -1593,6 +1675,54 @@ static int launch_m(const ls_conv_plan *pl, cudaStream_t st) {
     cfg.numAttrs = 1;
     return (int)cudaLaunchKernelEx(&cfg, k_conv_p<BN, CHUNK, MODE, MT>, pl->a0, pl->a1, pl->b,
                                    pl->y, pl->p);
+}
+
+// CTA-pair launch: clusters of two, at most as many as the device can hold at
+// once (queried per device and kernel; the kernel strides its items by the
+// cluster count it was launched with).
+template <int BN, int CHUNK, int MODE, int MT = 1>
+static int launch_pair_m(const ls_conv_plan *pl, cudaStream_t st) {
+    auto kern = k_conv_p<BN, CHUNK, MODE, MT, true>;
+    static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
+    if (int e = smem_optin(kern, attr_done)) return e;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return (int)e;
+    static std::atomic<int> max_clusters[64];  // per device, 0 = not queried yet
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3((unsigned)CfgP<BN, CHUNK, MT>::kThreads);
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    int mc = max_clusters[dev & 63].load(std::memory_order_relaxed);
+    if (mc <= 0) {
+        cfg.gridDim = dim3((unsigned)pl->grid);
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&mc, kern, &cfg) != cudaSuccess || mc <= 0) {
+            (void)cudaGetLastError();
+            mc = pl->grid / 2;
+        }
+        max_clusters[dev & 63].store(mc, std::memory_order_relaxed);
+    }
+    const int clusters = pl->grid / 2 < mc ? pl->grid / 2 : mc;
+    cfg.gridDim = dim3((unsigned)(2 * clusters));
+    cfg.numAttrs = 2;
+    return (int)cudaLaunchKernelEx(&cfg, kern, pl->a0, pl->a1, pl->b, pl->y, pl->p);
+}
+
+template <int BN, int CHUNK>
+static int launch_pair(const ls_conv_plan *pl, cudaStream_t st) {
+    if (BN == 128 && pl->mt == 2)
+        return pl->mode == kPool ? launch_pair_m<BN, CHUNK, kPool, 2>(pl, st)
+                                 : launch_pair_m<BN, CHUNK, kPlain, 2>(pl, st);
+    return pl->mode == kPool ? launch_pair_m<BN, CHUNK, kPool>(pl, st)
+                             : launch_pair_m<BN, CHUNK, kPlain>(pl, st);
 }
 
 template <int CHUNK, int COUT, int MODE>
@@ -1704,6 +1834,53 @@ static int launch_p(const ls_conv_plan *pl, cudaStream_t st) {
         case kHead: return launch_m<BN, CHUNK, kHead, MT>(pl, st);
         default: return launch_m<BN, CHUNK, kTransposed, MT>(pl, st);
     }
+}
+
+// LS_CONV_PAIR: 0 keeps every k_conv_p layer on single-CTA tiles, 1 (default)
+// pairs the layers where pair_pays(), 2 pairs every eligible layer (A/B).
+static int pair_mode() {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
+        const char *e = getenv("LS_CONV_PAIR");
+        r = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+        v.store(r, std::memory_order_relaxed);
+    }
+    return r;
+}
+static bool pair_enabled() { return pair_mode() != 0; }
+
+static int env_int(const char *name, int dflt);
+
+// smallest column tile on CTA pairs (LS_CONV_PAIR_MINBN, 64 / 128 / 256)
+static int pair_min_bn() {
+    static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
+    int r = v.load(std::memory_order_relaxed);
+    if (r < 0) {
+        r = env_int("LS_CONV_PAIR_MINBN", 128);
+        if (r != 64 && r != 256) r = 128;
+        v.store(r, std::memory_order_relaxed);
+    }
+    return r;
+}
+
+static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transposed);
+
+// Pairs only where their coarser work items do not cost more waves: a pair
+// item (one 128-pixel sub-tile per SM of the pair) runs ~1.3x faster than a
+// single-CTA sub-tile (profiles/README.md, "CTA pairs"), so pair when
+// waves(pairs) <= 1.3 x waves(single) x sub-tiles per single item.  The
+// 1/16-resolution bottleneck (68 rows: 4.25 pair tiles) stays single.
+static bool pair_pays(int bn, int h, int w, int batch, int n_tiles_n) {
+    if (pair_mode() == 2) return true;
+    const int n_sm = current_sm_count();
+    const long long tx = (w + kTW - 1) / kTW;
+    const long long items_p = tx * ((h + 2 * kTH - 1) / (2 * kTH)) * batch * n_tiles_n;
+    const long long waves_p = (items_p + n_sm / 2 - 1) / (n_sm / 2);
+    const int mt = mt_for(bn, h, w, batch, n_tiles_n, false);
+    const long long items_s = tx * ((h + kTH * mt - 1) / (kTH * mt)) * batch * n_tiles_n;
+    const long long waves_s = (items_s + n_sm - 1) / n_sm;
+    return 10 * waves_p <= 13 * waves_s * mt;
 }
 
 // LS_CONV_MT2=0 keeps 256-column tiles at one sub-tile per item (A/B).
@@ -2046,12 +2223,19 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     // one stage), then one kx per stage, then a narrower K chunk, then a
     // narrower column tile.
     int mt = 1;
+    // CTA pairs for the plain / pooling layers with >= 128-column tiles
+    // (LS_CONV_PAIR=0: single-CTA tiles everywhere)
+    bool pair = !transposed && !d_head_w && bn >= pair_min_bn() && pair_enabled() &&
+                pair_pays(bn, h, w, batch, (n_total + bn - 1) / bn);
     for (;;) {
-        mt = mt_for(bn, h, w, batch, (n_total + bn - 1) / bn, transposed != 0);
+        if (bn < pair_min_bn() || chunk < 16) pair = false;
+        mt = pair ? (bn == 128 ? env_int("LS_CONV_PAIR_MT", 1) == 2 ? 2 : 1 : 1)
+                  : mt_for(bn, h, w, batch, (n_total + bn - 1) / bn, transposed != 0);
         const int box_h = kTH * mt + 2 * p.pad;
+        const int tile_h = kTH * mt * (pair ? 2 : 1);
         const uint32_t row = (uint32_t)chunk * 2;
         p.tiles_x = (w + kTW - 1) / kTW;
-        p.tiles_y = (h + kTH * mt - 1) / (kTH * mt);
+        p.tiles_y = (h + tile_h - 1) / tile_h;
         p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
         p.n_tiles_n = (n_total + bn - 1) / bn;
         p.n_items = p.n_tiles_m * p.n_tiles_n;
@@ -2059,7 +2243,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         p.nq = (c0 + c1) / chunk;
         p.a_tx = (uint32_t)(kTW * box_h) * row;
         p.a_bytes = (p.a_tx + 1023u) & ~1023u;
-        p.b_blk = (uint32_t)(kys * bn) * row;
+        p.b_blk = (uint32_t)(kys * (pair ? bn / 2 : bn)) * row;
         const size_t nk = (size_t)p.kxs * p.nq;
         p.resident = (p.n_tiles_n == 1 && nk * p.b_blk <= kResidentMax) ? 1 : 0;
         res_bytes = p.resident ? nk * p.b_blk : 0;
@@ -2099,6 +2283,7 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = bn;
     pl->chunk = chunk;
+    pl->pair = pair ? 1 : 0;
     pl->mode = transposed ? kTransposed : (d_head_w ? kHead : (d_pool ? kPool : kPlain));
     if (p.stage_store && !encode_up_store(&pl->y, d_y, w, h, batch)) {
         delete pl;
@@ -2106,13 +2291,14 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    if (pair) pl->grid = 2 * (p.n_items < n_sm / 2 ? p.n_items : n_sm / 2);
     pl->full_tiles_y = p.tiles_y;
     const int box_h = kTH * mt + 2 * p.pad;
     pl->mt = mt;
     bool ok = encode_act(&pl->a0, d_x0, c0_tensor, w, h, batch, chunk, box_h);
     ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, c1 > 0 ? c1 : c0_tensor, w, h, batch,
                           chunk, box_h);
-    ok = ok && encode_wts(&pl->b, d_w, p.ctot, n_total, p.kxs * kys, chunk, bn, kys);
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, n_total, p.kxs * kys, chunk, pair ? bn / 2 : bn, kys);
     if (!ok) {
         delete pl;
         return fail(LS_EINVAL);
@@ -2125,6 +2311,15 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     if (!pl) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (pl->kind == 2) return launch_px2(pl, st);
+    if (pl->pair) {
+        if (pl->bn == 128 && pl->chunk == 64) return launch_pair<128, 64>(pl, st);
+        if (pl->bn == 128 && pl->chunk == 32) return launch_pair<128, 32>(pl, st);
+        if (pl->bn == 256 && pl->chunk == 32) return launch_pair<256, 32>(pl, st);
+        if (pl->bn == 256 && pl->chunk == 16) return launch_pair<256, 16>(pl, st);
+        if (pl->bn == 64 && pl->chunk == 64) return launch_pair<64, 64>(pl, st);
+        if (pl->bn == 64 && pl->chunk == 32) return launch_pair<64, 32>(pl, st);
+        return LS_EINVAL;
+    }
     if (pl->kind == 1) {
         if (pl->chunk == 16) return launch_kx<16>(pl, st);
         if (pl->chunk == 32) return launch_kx<32>(pl, st);
@@ -2154,7 +2349,7 @@ int ls_conv_plan_set_reverse(ls_conv_plan *pl, int32_t reverse) {
 
 int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) {
     if (!pl) return LS_EINVAL;
-    const int th = pl->kind == 0 ? kTH * pl->mt : kTH;  // rows per tile
+    const int th = pl->kind == 0 ? kTH * pl->mt * (pl->pair ? 2 : 1) : kTH;  // rows per tile
     const int h = pl->p.h;
     if (row_begin < 0 || row_end > h || row_begin >= row_end || row_begin % th) return LS_EINVAL;
     const int t0 = row_begin / th, t1 = (row_end + th - 1) / th;
@@ -2171,7 +2366,7 @@ int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) 
 
 int32_t ls_conv_plan_tile_rows(const ls_conv_plan *pl) {
     if (!pl) return LS_EINVAL;
-    return pl->kind == 0 ? kTH * pl->mt : kTH;
+    return pl->kind == 0 ? kTH * pl->mt * (pl->pair ? 2 : 1) : kTH;
 }
 
 int ls_conv2d(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1, int32_t c1, int32_t batch,

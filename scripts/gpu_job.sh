@@ -1,1 +1,1 @@
-for v in 3 1; do for r in 1 2; do echo "LS_CONV_PX2=$v $(LS_CONV_PX2=$v python scripts/time_unet.py | tail -1)"; done; done
+timeout 900 python -m pytest tests/test_gpu_unet.py tests/test_gpu_configs.py tests/test_gpu_engine.py tests/test_gpu_bridge.py -x -q 2>&1 | tail -3

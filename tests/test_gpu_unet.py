@@ -33,6 +33,12 @@ LAYER_CASES = [
     dict(c0=32, c1=0, cout=32, h=18, w=58, act=2, head=True),
     # odd width: k_conv_px2 does not apply (falls back to k_conv_kx)
     dict(c0=32, c1=0, cout=32, h=9, w=31, act=1),
+    # CTA pairs (>= 128 output columns): resident half-weights, ragged pair
+    # tiles (rows not a multiple of 16), pooling, batches, 256-column tiles
+    dict(c0=64, c1=0, cout=128, h=20, w=40, act=1),
+    dict(c0=128, c1=0, cout=128, h=24, w=48, act=1, pool=True, batch=2),
+    dict(c0=128, c1=0, cout=256, h=17, w=30, act=2),
+    dict(c0=256, c1=0, cout=256, h=16, w=32, act=1, pool=True),
 ]
 
 
