@@ -356,33 +356,36 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         reinterpret_cast<uint64_t *>(smem + (size_t)kPassWarps * S * R::kStage) + wib * S;
     uint32_t *ents =
         reinterpret_cast<uint32_t *>(smem + (size_t)kPassWarps * S * (R::kStage + 8)) + wib * S;
-    const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t n_items = list ? (int64_t)__ldg(count) : s.n_tiles;
+    // Item bookkeeping in 32-bit arithmetic: scenes hold < 2^38 points, so tile
+    // indices, work-list positions and per-warp counts are < 2^31 (scene_ok).
+    const int w0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    const int n_items = list ? (int)__ldg(count) : (int)s.n_tiles;
     if (w0 >= n_items) return;
-    const int64_t nj = (n_items - w0 + nw - 1) / nw;  // this warp's items
+    const int nj = (n_items - w0 + nw - 1) / nw;  // this warp's items
     const bool col_bulk = MODE != kXyz && (reinterpret_cast<uintptr_t>(s.col) & 15) == 0;
-    auto full = [&](int64_t tile) { return (tile + 1) * LS_TILE_POINTS <= s.n; };
+    const uint32_t n_full = (uint32_t)(s.n / LS_TILE_POINTS);  // tiles below hold 128 points
+    auto full = [&](uint32_t tile) { return tile < n_full; };
     // Work-list entries of items [32b, 32b+32) live one per lane (ecur), the
     // next 32 in enext, so the issuing lane never waits on a list load.
-    auto entry_batch = [&](int64_t b) -> uint32_t {
-        const int64_t j = 32 * b + lane;
+    auto entry_batch = [&](int b) -> uint32_t {
+        const int j = 32 * b + lane;
         if (!list) return (uint32_t)(w0 + j * nw);
         return j < nj ? __ldg(list + w0 + j * nw) : 0u;
     };
     uint32_t ecur = entry_batch(0), enext = entry_batch(1);
-    int64_t ebatch = 0;
-    auto entry = [&](int64_t j) -> uint32_t {  // warp-collective, j non-decreasing
+    int ebatch = 0;
+    auto entry = [&](int j) -> uint32_t {  // warp-collective, j non-decreasing
         if ((j >> 5) != ebatch) {
             ecur = enext;
             ++ebatch;
             enext = entry_batch(ebatch + 1);
         }
-        return __shfl_sync(0xffffffffu, ecur, (int)(j & 31));
+        return __shfl_sync(0xffffffffu, ecur, j & 31);
     };
     const uint64_t pol = stream_policy();
-    auto issue = [&](uint32_t e, int64_t j, int q) {  // lane 0 only
-        const int64_t tile = e & ~kMixed;
+    auto issue = [&](uint32_t e, int j, int q) {  // lane 0 only
+        const uint32_t tile = e & ~kMixed;
         ents[q] = e;
         const bool f = full(tile);
         // the cache block is always complete (pass 1 writes all 128 slots)
@@ -394,11 +397,13 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         umma::mbar_expect_tx(&bars[q], R::kMain + (rgb ? kColBytes : 0));
         uint8_t *dst = ring + q * R::kStage;
         if (MODE == kCacheRgb)
-            bulk_g2s(dst, cache + (w0 + j * nw) * (kCacheBytes / 4), kCacheBytes, &bars[q], pol);
+            bulk_g2s(dst, cache + (size_t)(uint32_t)(w0 + j * nw) * (kCacheBytes / 4), kCacheBytes,
+                     &bars[q], pol);
         else if (MODE != kRgb)
-            bulk_g2s(dst, s.pos + tile * 3 * LS_TILE_POINTS, kPosBytes, &bars[q], pol);
+            bulk_g2s(dst, s.pos + (size_t)tile * (3 * LS_TILE_POINTS), kPosBytes, &bars[q], pol);
         if (rgb)
-            bulk_g2s(dst + R::kMain, s.col + tile * 3 * LS_TILE_POINTS, kColBytes, &bars[q], pol);
+            bulk_g2s(dst + R::kMain, s.col + (size_t)tile * (3 * LS_TILE_POINTS), kColBytes,
+                     &bars[q], pol);
     };
     if (lane == 0) {
         for (int q = 0; q < S; ++q) umma::mbar_init(&bars[q], 1);
@@ -409,14 +414,16 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         if (lane == 0) issue(e, q, q);
     }
     __syncwarp();
-    for (int64_t j = 0; j < nj; ++j) {
-        const int q = (int)(j % S);
-        umma::mbar_wait_spin(&bars[q], (uint32_t)((j / S) & 1));
+    int q = 0;
+    uint32_t ph = 0;
+    uint32_t index = (uint32_t)w0;  // work-list position of item j: w0 + j * nw
+    for (int j = 0; j < nj; ++j, index += (uint32_t)nw) {
+        umma::mbar_wait_spin(&bars[q], ph);
         Item it;
         it.e = ents[q];
-        it.index = w0 + j * nw;
-        const int64_t tile = it.e & ~kMixed;
-        it.base = tile * LS_TILE_POINTS + 4 * lane;
+        it.index = index;
+        const uint32_t tile = it.e & ~kMixed;
+        it.base = (int64_t)tile * LS_TILE_POINTS + 4 * lane;
         it.full = full(tile);
         it.st = ring + q * R::kStage;
         uint3 W = make_uint3(0u, 0u, 0u);  // the lane's 12 colour bytes (by value)
@@ -440,6 +447,10 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue(en, j + S, q);
             }
+        }
+        if (++q == S) {
+            q = 0;
+            ph ^= 1u;
         }
     }
 }
