@@ -304,7 +304,7 @@ template <int S, int MODE>
 struct TileRing {
     static constexpr int kMain = MODE == kCacheRgb ? kCacheBytes : (MODE == kRgb ? 0 : kPosBytes);
     static constexpr int kStage = kMain + (MODE == kXyz ? 0 : kColBytes);
-    static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8 + 4);
+    static constexpr size_t kBytes = (size_t)kPassWarps * S * (kStage + 8);  // stages + mbarriers
 };
 
 // The scan / cache streams of the passes are read once per frame: tag them
@@ -354,8 +354,6 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
     uint8_t *ring = smem + (size_t)wib * S * R::kStage;
     uint64_t *bars =
         reinterpret_cast<uint64_t *>(smem + (size_t)kPassWarps * S * R::kStage) + wib * S;
-    uint32_t *ents =
-        reinterpret_cast<uint32_t *>(smem + (size_t)kPassWarps * S * (R::kStage + 8)) + wib * S;
     // Item bookkeeping in 32-bit arithmetic: scenes hold < 2^38 points, so tile
     // indices, work-list positions and per-warp counts are < 2^31 (scene_ok).
     const int w0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -373,20 +371,25 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
         if (!list) return (uint32_t)(w0 + j * nw);
         return j < nj ? __ldg(list + w0 + j * nw) : 0u;
     };
-    uint32_t ecur = entry_batch(0), enext = entry_batch(1);
+    uint32_t ecur = entry_batch(0), enext = entry_batch(1), eprev = 0u;
     int ebatch = 0;
     auto entry = [&](int j) -> uint32_t {  // warp-collective, j non-decreasing
         if ((j >> 5) != ebatch) {
+            eprev = ecur;
             ecur = enext;
             ++ebatch;
             enext = entry_batch(ebatch + 1);
         }
         return __shfl_sync(0xffffffffu, ecur, j & 31);
     };
+    // the entry of an item up to S - 1 < 32 positions behind the last entry()
+    // call (its batch is the current or the previous one)
+    auto entry_back = [&](int j) -> uint32_t {
+        return __shfl_sync(0xffffffffu, (j >> 5) == ebatch ? ecur : eprev, j & 31);
+    };
     const uint64_t pol = stream_policy();
     auto issue = [&](uint32_t e, int j, int q) {  // lane 0 only
         const uint32_t tile = e & ~kMixed;
-        ents[q] = e;
         const bool f = full(tile);
         // the cache block is always complete (pass 1 writes all 128 slots)
         const bool rgb = MODE != kXyz && f && col_bulk;
@@ -420,7 +423,7 @@ __device__ __forceinline__ void for_each_item(const SceneArgs &s, const uint32_t
     for (int j = 0; j < nj; ++j, index += (uint32_t)nw) {
         umma::mbar_wait_spin(&bars[q], ph);
         Item it;
-        it.e = ents[q];
+        it.e = entry_back(j);
         it.index = index;
         const uint32_t tile = it.e & ~kMixed;
         it.base = (int64_t)tile * LS_TILE_POINTS + 4 * lane;
