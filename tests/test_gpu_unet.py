@@ -274,3 +274,25 @@ def test_conv_plan_set_rows_validation():
         assert nz[t:2 * t].all() and not nz[:t].any() and not nz[2 * t:].any()
     finally:
         lib.ls_conv_plan_destroy(pl)
+
+
+def test_cta_pairs_bit_identical(tmp_path):
+    """CTA-pair layers (cta_group::2, M = 256) accumulate every output in the
+    same K order as the single-CTA kernels: the DEFAULT network's output with
+    pairs (LS_CONV_PAIR=2: every eligible layer, including the bottleneck)
+    equals the LS_CONV_PAIR=0 run bit for bit.  The switch is read once per
+    process, so each configuration runs in its own."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("0", "2", "1"):
+        f = tmp_path / f"o{mode}.npy"
+        env = dict(os.environ, LS_CONV_PAIR=mode, H="256", W="480")
+        subprocess.run([sys.executable, os.path.join(root, "scripts", "unet_out.py"), str(f)],
+                       env=env, check=True, timeout=300)
+        outs.append(np.load(f))
+    assert outs[0].shape == (1, 256, 480, 3)
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
