@@ -2166,8 +2166,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     int bn = n_total >= 256 ? 256 : (n_total >= 128 ? 128 : (n_total >= 64 ? 64 : 32));
     if (n_total % bn) bn = 32;
+    // 256-channel layers on 128-column tiles: with CTA pairs (M = 256) the twice
+    // as many items balance better over the SMs (measured 0.810 -> 0.804 ms;
+    // LS_CONV_N256=256 keeps 256-column tiles)
     if (bn == 256 && n_total == 256 && !transposed && !d_head_w &&
-        env_int("LS_CONV_N256", 256) == 128)
+        env_int("LS_CONV_N256", pair_enabled() ? 128 : 256) == 128)
         bn = 128;
     {
         // small grids (the 1/16-resolution bottleneck): 128-column tiles when

@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_projection.py tests/test_gpu_configs.py tests/test_gpu_views.py tests/test_gpu_engine.py tests/test_gpu_kernels.py -x -q 2>&1 | tail -2
-for r in 1 2; do python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); s=d['stages_ms']; print(round(d['value'],1), round(d['e2e']['value'],1), round(d['roofline']['other']['frac'],3), {k: round(v*1e3,1) for k,v in s.items()})"; done
+timeout 600 python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -2
+for r in 1 2; do
+echo "base $(timeout 120 python scripts/time_unet.py | tail -1)"
+done

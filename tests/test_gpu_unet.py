@@ -39,6 +39,7 @@ LAYER_CASES = [
     dict(c0=128, c1=0, cout=128, h=24, w=48, act=1, pool=True, batch=2),
     dict(c0=128, c1=0, cout=256, h=17, w=30, act=2),
     dict(c0=256, c1=0, cout=256, h=16, w=32, act=1, pool=True),
+    dict(c0=64, c1=0, cout=512, h=96, w=128, act=1),  # 256-column pair tiles
     # k_conv_kx (cout = 64, K >= 128) on CTA pairs: two sources, ragged rows, pool
     dict(c0=64, c1=64, cout=64, h=20, w=36, act=2),
     dict(c0=128, c1=0, cout=64, h=16, w=30, act=1, pool=True, batch=2),
