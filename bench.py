@@ -464,7 +464,8 @@ def run_b200(args):
     for e in evs:
         for j, k in enumerate(stage):
             stage[k].append(e[j].elapsed_time(e[j + 1]))
-    stages_ms = {k: float(np.mean(v)) for k, v in stage.items()}
+    # median over the frames: robust to a host hiccup delaying one instrumented frame
+    stages_ms = {k: float(np.median(v)) for k, v in stage.items()}
     ft = np.array([e[0].elapsed_time(e[nst]) for e in evs])
     cand = [n_cand[(view0 + args.warmup + i) % len(cams)] for i in range(args.steps)]
     mean_cand = float(np.mean(cand))
@@ -516,8 +517,8 @@ def run_b200(args):
                         "p95": float(np.percentile(ft, 95)),
                         "source": "instrumented pass, CUDA events around each frame"},
            "stages_note": "per-stage CUDA events from a second, instrumented pass over the "
-                          "same frames; value / ms_per_step come from the uninstrumented "
-                          "timed pass",
+                          "same frames (median over the frames); value / ms_per_step come "
+                          "from the uninstrumented timed pass",
            "roofline": roofline, "e2e": rep_e2e,
            "gpu_launches": renderer.launches_per_frame * args.steps}
     if sharded:
