@@ -375,24 +375,28 @@ __global__ void __launch_bounds__(256) k_assemble_pyramid(
     }
 }
 
-// One thread per COARSE pixel on a 2-D grid (32 x 8 threads per CTA, no
-// index division); FINAL reads the full-resolution frame and, where the
-// thread's two children of a fine row are both inside an even-width image,
-// moves them with 8 B (rgb, depth), 2 B (alpha) and 16 B (U-Net) accesses.
-template <bool FINAL>
-__global__ void __launch_bounds__(256) k_filter_step(
-    const float *__restrict__ coarse, int64_t ch, int64_t cw, const float *__restrict__ fine,
-    int64_t fh, int64_t fw, double fs, double et, float *__restrict__ out,
-    // FINAL-only arguments
-    const float *__restrict__ rgb, const uint8_t *__restrict__ alpha, float *__restrict__ frgb,
-    float *__restrict__ fdepth, uint8_t *__restrict__ falpha, uint8_t *__restrict__ keep_out,
-    __nv_bfloat16 *__restrict__ unet_in, int unet_c, double znear) {
-    pdl_wait();
-    const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
-    if (cx >= cw || cy >= ch) return;
-    const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
-    const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+// Arguments of the final (full-resolution) filter step.
+struct FinalArgs {
+    const float *fine;  // frame depth (0 = empty)
+    int64_t fh, fw;
+    const float *rgb;
+    const uint8_t *alpha;
+    float *frgb, *fdepth;
+    uint8_t *falpha, *keep;
+    __nv_bfloat16 *unet_in;
+    int unet_c;
+    double znear;
+};
+
+// The final step for the 2x2 children of coarse pixel (cy, cx) given its
+// reference depth: keep mask, filtered frame and / or U-Net input.  Where the
+// two children of a fine row are both inside an even-width image they move
+// with 8 B (rgb, depth), 2 B (alpha) and 16 B (U-Net) accesses.
+__device__ __forceinline__ void final_children(const FinalArgs &fa, int64_t cy, int64_t cx,
+                                               double ref, double fs) {
+    const int64_t fh = fa.fh, fw = fa.fw;
+    const float *__restrict__ fine = fa.fine;
+    const float *__restrict__ rgb = fa.rgb;
     const int64_t x = 2 * cx;
     const bool pair = x + 1 < fw && (fw & 1) == 0;
 #pragma unroll
@@ -400,15 +404,6 @@ __global__ void __launch_bounds__(256) k_filter_step(
         const int64_t y = 2 * cy + dy;
         if (y >= fh) break;
         const int64_t p = y * fw + x;
-        if (!FINAL) {
-#pragma unroll
-            for (int dx = 0; dx < 2; ++dx) {
-                if (x + dx >= fw) break;
-                const float f = fine[p + dx];
-                out[p + dx] = keep_test(f, ref, fs) ? f : bilinear_at(coarse, ch, cw, y, x + dx);
-            }
-            continue;
-        }
         if (!pair) {  // odd width or the last column: scalar children
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx) {
@@ -416,24 +411,26 @@ __global__ void __launch_bounds__(256) k_filter_step(
                 const int64_t q = p + dx;
                 const float dq = fine[q];  // frame depth (0 = empty)
                 const bool kq = keep_test(sentinel(dq), ref, fs);
-                if (keep_out) keep_out[q] = (uint8_t)kq;
+                if (fa.keep) fa.keep[q] = (uint8_t)kq;
                 if (!rgb) {  // mask-only, or U-Net-only: clear a rejected non-empty pixel
-                    if (unet_in && !kq && dq > 0.0f)
-                        store_unet_px(unet_in + q * unet_c, unet_c, 0.f, 0.f, 0.f, 0.f, 0.f, znear);
+                    if (fa.unet_in && !kq && dq > 0.0f)
+                        store_unet_px(fa.unet_in + q * fa.unet_c, fa.unet_c, 0.f, 0.f, 0.f, 0.f,
+                                      0.f, fa.znear);
                     continue;
                 }
                 const float m = kq ? 1.0f : 0.0f;  // filtering.py:141-147 f32 0/1 mask
                 const float r = rgb[3 * q] * m, g = rgb[3 * q + 1] * m, b = rgb[3 * q + 2] * m,
                             dd = dq * m;
-                const uint8_t a = (uint8_t)(alpha[q] * (uint8_t)kq);
-                if (frgb) {
-                    frgb[3 * q] = r;
-                    frgb[3 * q + 1] = g;
-                    frgb[3 * q + 2] = b;
+                const uint8_t a = (uint8_t)(fa.alpha[q] * (uint8_t)kq);
+                if (fa.frgb) {
+                    fa.frgb[3 * q] = r;
+                    fa.frgb[3 * q + 1] = g;
+                    fa.frgb[3 * q + 2] = b;
                 }
-                if (fdepth) fdepth[q] = dd;
-                if (falpha) falpha[q] = a;
-                if (unet_in) store_unet_px(unet_in + q * unet_c, unet_c, r, g, b, dd, a, znear);
+                if (fa.fdepth) fa.fdepth[q] = dd;
+                if (fa.falpha) fa.falpha[q] = a;
+                if (fa.unet_in)
+                    store_unet_px(fa.unet_in + q * fa.unet_c, fa.unet_c, r, g, b, dd, a, fa.znear);
             }
             continue;
         }
@@ -446,21 +443,21 @@ __global__ void __launch_bounds__(256) k_filter_step(
             k[dx] = keep_test(sentinel(d[dx]), ref, fs);
             mk[dx] = k[dx] ? 1.0f : 0.0f;
         }
-        if (keep_out) *reinterpret_cast<uchar2 *>(keep_out + p) = make_uchar2(k[0], k[1]);
+        if (fa.keep) *reinterpret_cast<uchar2 *>(fa.keep + p) = make_uchar2(k[0], k[1]);
         if (!rgb) {
-            if (unet_in) {
+            if (fa.unet_in) {
 #pragma unroll
                 for (int dx = 0; dx < 2; ++dx)
                     if (!k[dx] && d[dx] > 0.0f)
-                        store_unet_px(unet_in + (p + dx) * unet_c, unet_c, 0.f, 0.f, 0.f, 0.f, 0.f,
-                                      znear);
+                        store_unet_px(fa.unet_in + (p + dx) * fa.unet_c, fa.unet_c, 0.f, 0.f, 0.f,
+                                      0.f, 0.f, fa.znear);
             }
             continue;
         }
         const float2 *r2 = reinterpret_cast<const float2 *>(rgb + 3 * p);
         const float2 a0 = r2[0], a1 = r2[1], a2 = r2[2];
         const float c[2][3] = {{a0.x, a0.y, a1.x}, {a1.y, a2.x, a2.y}};
-        const uchar2 a2v = *reinterpret_cast<const uchar2 *>(alpha + p);
+        const uchar2 a2v = *reinterpret_cast<const uchar2 *>(fa.alpha + p);
         const uint8_t al[2] = {a2v.x, a2v.y};
         float o[2][4];
         uint8_t oa[2];
@@ -472,19 +469,50 @@ __global__ void __launch_bounds__(256) k_filter_step(
             o[dx][3] = d[dx] * mk[dx];
             oa[dx] = (uint8_t)(al[dx] * (uint8_t)k[dx]);
         }
-        if (frgb) {
-            float2 *w2 = reinterpret_cast<float2 *>(frgb + 3 * p);
+        if (fa.frgb) {
+            float2 *w2 = reinterpret_cast<float2 *>(fa.frgb + 3 * p);
             w2[0] = make_float2(o[0][0], o[0][1]);
             w2[1] = make_float2(o[0][2], o[1][0]);
             w2[2] = make_float2(o[1][1], o[1][2]);
         }
-        if (fdepth) *reinterpret_cast<float2 *>(fdepth + p) = make_float2(o[0][3], o[1][3]);
-        if (falpha) *reinterpret_cast<uchar2 *>(falpha + p) = make_uchar2(oa[0], oa[1]);
-        if (unet_in) {
+        if (fa.fdepth) *reinterpret_cast<float2 *>(fa.fdepth + p) = make_float2(o[0][3], o[1][3]);
+        if (fa.falpha) *reinterpret_cast<uchar2 *>(fa.falpha + p) = make_uchar2(oa[0], oa[1]);
+        if (fa.unet_in) {
 #pragma unroll
             for (int dx = 0; dx < 2; ++dx)
-                store_unet_px(unet_in + (p + dx) * unet_c, unet_c, o[dx][0], o[dx][1], o[dx][2],
-                              o[dx][3], oa[dx], znear);
+                store_unet_px(fa.unet_in + (p + dx) * fa.unet_c, fa.unet_c, o[dx][0], o[dx][1],
+                              o[dx][2], o[dx][3], oa[dx], fa.znear);
+        }
+    }
+}
+
+// One thread per COARSE pixel on a 2-D grid (32 x 8 threads per CTA, no
+// index division); FINAL reads the full-resolution frame (final_children).
+template <bool FINAL>
+__global__ void __launch_bounds__(256) k_filter_step(
+    const float *__restrict__ coarse, int64_t ch, int64_t cw, const float *__restrict__ fine,
+    int64_t fh, int64_t fw, double fs, double et, float *__restrict__ out, FinalArgs fa) {
+    pdl_wait();
+    const int64_t cx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t cy = blockIdx.y * (int64_t)blockDim.y + threadIdx.y;
+    if (cx >= cw || cy >= ch) return;
+    const bool edge = lap_edge(coarse, ch, cw, cy, cx, et);
+    const double ref = parent_ref(coarse, ch, cw, cy, cx, edge);
+    if (FINAL) {
+        final_children(fa, cy, cx, ref, fs);
+    } else {
+        const int64_t x = 2 * cx;
+#pragma unroll
+        for (int dy = 0; dy < 2; ++dy) {
+            const int64_t y = 2 * cy + dy;
+            if (y >= fh) break;
+            const int64_t p = y * fw + x;
+#pragma unroll
+            for (int dx = 0; dx < 2; ++dx) {
+                if (x + dx >= fw) break;
+                const float f = fine[p + dx];
+                out[p + dx] = keep_test(f, ref, fs) ? f : bilinear_at(coarse, ch, cw, y, x + dx);
+            }
         }
     }
     pdl_trigger();
@@ -523,7 +551,8 @@ inline void level_sizes(int64_t H, int64_t W, int L, int64_t *h, int64_t *w) {
 // recompute overlapping halos with the same arithmetic, so the result is the
 // per-step kernels' bit for bit; the L-1 launches (each latency-bound on a
 // small image) become one.
-constexpr int kFuseTX = 32, kFuseTY = 16, kFuseMaxSteps = 4, kFuseBuf = 512;
+// (FINAL: the last non-final level is produced on the tile +- 1, 34 x 18 values)
+constexpr int kFuseTX = 32, kFuseTY = 16, kFuseMaxSteps = 4, kFuseBuf = 640;
 
 struct Rect {
     int y0, y1, x0, x1;  // [y0, y1) x [x0, x1)
@@ -558,8 +587,14 @@ struct FsSweep {
     int64_t out_stride;
 };
 
+// FINAL: the final (full-resolution) step fused in as well -- the last
+// non-final step is produced on the tile +- 1 (the final step's 3x3 stencils)
+// into shared memory, then every level-1 pixel of the tile runs the final
+// step for its 2x2 children (final_children, the arithmetic of
+// k_filter_step<true>), so the whole filter after the pyramid is one launch.
+template <bool FINAL>
 __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *__restrict__ out,
-                                                             FsSweep sw, double et) {
+                                                             FsSweep sw, double et, FinalArgs fa) {
     pdl_wait();
     const double fs = sw.fs[blockIdx.z];
     out += blockIdx.z * sw.out_stride;
@@ -567,14 +602,22 @@ __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *_
     __shared__ double refbuf[kFuseBuf];     // reference depth per parent pixel
     const int L = lv.L, nsteps = L - 1;
     // regions: R[i] = output region of step i+1 (level L-1-i), R[nsteps-1] = this tile
+    // (FINAL: the tile +- 1)
     Rect R[kFuseMaxSteps];
+    Rect t;
+    t.y0 = blockIdx.y * kFuseTY;
+    t.y1 = min(t.y0 + kFuseTY, (int)lv.h[1]);
+    t.x0 = blockIdx.x * kFuseTX;
+    t.x1 = min(t.x0 + kFuseTX, (int)lv.w[1]);
     {
-        Rect t;
-        t.y0 = blockIdx.y * kFuseTY;
-        t.y1 = min(t.y0 + kFuseTY, (int)lv.h[1]);
-        t.x0 = blockIdx.x * kFuseTX;
-        t.x1 = min(t.x0 + kFuseTX, (int)lv.w[1]);
-        R[nsteps - 1] = t;
+        Rect r = t;
+        if (FINAL) {
+            r.y0 = max(t.y0 - 1, 0);
+            r.y1 = min(t.y1 + 1, (int)lv.h[1]);
+            r.x0 = max(t.x0 - 1, 0);
+            r.x1 = min(t.x1 + 1, (int)lv.w[1]);
+        }
+        R[nsteps - 1] = r;
         for (int i = nsteps - 2; i >= 0; --i)  // R[i] lies on level L-1-i
             R[i] = coarse_of(R[i + 1], (int)lv.h[L - 1 - i], (int)lv.w[L - 1 - i]);
     }
@@ -610,12 +653,23 @@ __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *_
             const double ref = refbuf[((y >> 1) - P.y0) * P.w() + ((x >> 1) - P.x0)];
             const float f = fine[(int64_t)y * fw + x];
             const float o = keep_test(f, ref, fs) ? f : bilinear_at_t(getC, ch, cw, y, x);
-            if (last) out[(int64_t)y * fw + x] = o;
-            else ubuf[cur ^ 1][i] = o;
+            if (!last || FINAL) ubuf[cur ^ 1][i] = o;
+            if (last && (!FINAL || (y >= t.y0 && y < t.y1 && x >= t.x0 && x < t.x1)))
+                out[(int64_t)y * fw + x] = o;
         }
         __syncthreads();
         cur ^= 1;
         C = F;
+    }
+    if (FINAL) {
+        // the final step's coarse image is level 1 on C (= the tile +- 1)
+        const int64_t ch = lv.h[1], cw = lv.w[1];
+        const SmemImg getC{ubuf[cur], C};
+        for (int i = threadIdx.x; i < t.h() * t.w(); i += blockDim.x) {
+            const int cy = t.y0 + i / t.w(), cx = t.x0 + i % t.w();
+            const bool edge = lap_edge_t(getC, ch, cw, cy, cx, et);
+            final_children(fa, cy, cx, parent_ref_t(getC, ch, cw, cy, cx, edge), fs);
+        }
     }
     pdl_trigger();
 }
@@ -624,16 +678,20 @@ __global__ void __launch_bounds__(256) k_filter_coarse_fused(Levels lv, float *_
 // must fit the shared buffers: true for kFuseTY x kFuseTX tiles and L <= 5)
 inline bool fused_ok(const Levels &lv) { return lv.L >= 2 && lv.L - 1 <= kFuseMaxSteps; }
 
-// LS_FILTER_FUSED=0 runs one launch per non-final step (A/B measurements).
-inline bool fused_steps_enabled() {
+// LS_FILTER_FUSED (A/B measurements): 0 = one launch per step, 1 (default) =
+// the non-final steps in one launch + the final step, 2 = all steps in one
+// launch (measured slower at 1080p: 807 vs 813 frames/s -- the fused final
+// step runs 2048 pixels per 256-thread CTA after the coarse steps, the
+// separate one 4 pixels per thread over the whole frame).
+inline int fused_mode() {
     static std::atomic<int> v{-1};  // set-once cache, relaxed is enough
     int r = v.load(std::memory_order_relaxed);
     if (r < 0) {
         const char *e = getenv("LS_FILTER_FUSED");
-        r = (e && e[0] == '0') ? 0 : 1;
+        r = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
         v.store(r, std::memory_order_relaxed);
     }
-    return r == 1;
+    return r;
 }
 
 // Pyramid + steps over an existing sentinel-able depth image.  `lvl` holds
@@ -647,15 +705,22 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
     const float *coarse = lv.img[L - 1];  // pyr.levels[0]
     float *up = up_base;
     int first = 1;
-    if (fused_ok(lv) && fused_steps_enabled()) {
+    const FinalArgs fa{full_fine, H, W, rgb, alpha, frgb, fdepth, falpha, keep, unet_in, unet_c, znear};
+    if (fused_ok(lv) && fused_mode() >= 1) {
         // steps 1..L-1 in one launch; its output sits where step L-1 would write
+        // (mode 2: the final step in the same launch)
         for (int i = 1; i < L - 1; ++i) up += lv.h[L - i] * lv.w[L - i];
         const dim3 g((unsigned)((lv.w[1] + kFuseTX - 1) / kFuseTX),
                      (unsigned)((lv.h[1] + kFuseTY - 1) / kFuseTY));
         FsSweep sw{};
         sw.fs[0] = fs;
-        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up, sw, et);
+        const bool all = fused_mode() == 2;
+        cudaError_t e = all ? launch_pdl(k_filter_coarse_fused<true>, g, dim3(256), 0, st, lv, up,
+                                         sw, et, fa)
+                            : launch_pdl(k_filter_coarse_fused<false>, g, dim3(256), 0, st, lv, up,
+                                         sw, et, FinalArgs{});
         if (e != cudaSuccess) return (int)e;
+        if (all) return 0;
         coarse = up;
         up += lv.h[1] * lv.w[1];
         first = L;
@@ -666,15 +731,13 @@ int run_filter_steps(const Levels &lv, float *up_base, const float *full_fine, i
         if (i < L) {
             const float *fine = lv.img[L - i - 1];
             cudaError_t e = launch_pdl(k_filter_step<false>, step_grid2(ch, cw), dim3(32, 8), 0, st,
-                                       coarse, ch, cw, fine, fh, fw, fs, et, up, nullptr, nullptr,
-                                       nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0);
+                                       coarse, ch, cw, fine, fh, fw, fs, et, up, FinalArgs{});
             if (e != cudaSuccess) return (int)e;
             coarse = up;
             up += fh * fw;
         } else {
             cudaError_t e = launch_pdl(k_filter_step<true>, step_grid2(ch, cw), dim3(32, 8), 0, st,
-                                       coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, rgb,
-                                       alpha, frgb, fdepth, falpha, keep, unet_in, unet_c, znear);
+                                       coarse, ch, cw, full_fine, fh, fw, fs, et, keep_as_out, fa);
             if (e != cudaSuccess) return (int)e;
         }
     }
@@ -1008,8 +1071,8 @@ int ls_depth_filter_sweep(const float *d_rgb, const float *d_depth, const uint8_
         sw.out_stride = lv.h[1] * lv.w[1];
         const dim3 g((unsigned)((lv.w[1] + kFuseTX - 1) / kFuseTX),
                      (unsigned)((lv.h[1] + kFuseTY - 1) / kFuseTY), (unsigned)n_strengths);
-        cudaError_t e = launch_pdl(k_filter_coarse_fused, g, dim3(256), 0, st, lv, up_base, sw,
-                                   edge_threshold);
+        cudaError_t e = launch_pdl(k_filter_coarse_fused<false>, g, dim3(256), 0, st, lv, up_base,
+                                   sw, edge_threshold, FinalArgs{});
         if (e != cudaSuccess) return (int)e;
         coarse = up_base;
         cstride = sw.out_stride;
