@@ -1330,8 +1330,10 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             __nv_bfloat16 *const pbase =
                 MODE == kPool ? p.pool + (((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp) * 32
                               : nullptr;
-            f32x2 hacc2[4] = {0ull, 0ull, 0ull, 0ull};  // head sums {pixel 2j, 2j+1}
-            float vkeep[16];   // pixel 2j's activations for the pair-wise head
+            // head sums per pixel and output as {even channels, odd channels}
+            // partials: the activations come out of the packed epilogue math as
+            // channel pairs, so each FFMA2 takes them as they are
+            f32x2 hsum[2][4] = {{0ull, 0ull, 0ull, 0ull}, {0ull, 0ull, 0ull, 0ull}};
             uint32_t keep[8];  // pixel 2j's packed half for the horizontal pool
             // 16-column groups in the order (px0, ch 0-15), (px1, 0-15), (px0, 16-31),
             // (px1, 16-31); group g+1's tcgen05.ld is in flight while g is processed
@@ -1363,27 +1365,16 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             auto emit = [&](int g, const float(&v)[16]) {
                 const int px = g & 1, n = (g >> 1) * 16;
                 if (MODE == kHead) {
-                    // both pixels of the pair at once: one FFMA2 per channel and
-                    // head output, weights read once (each pixel's sum keeps the
-                    // scalar loop's order)
-                    if (px == 0) {
+                    // one FFMA2 per channel pair and head output (weights from the
+                    // constant bank as pairs)
 #pragma unroll
-                        for (int i = 0; i < 16; ++i) vkeep[i] = v[i];
-                    } else {
+                    for (int j2 = 0; j2 < 4; ++j2) {
+                        if (j2 >= p.head_c) break;
+                        const float *wp = p.pc_head + j2 * 32 + n;
 #pragma unroll
-                        for (int j2 = 0; j2 < 4; ++j2) {
-                            if (j2 >= p.head_c) break;
-                            const float *wp = p.pc_head + j2 * 32 + n;  // constant bank
-#pragma unroll
-                            for (int q4 = 0; q4 < 4; ++q4) {
-                                const float wv[4] = {wp[4 * q4], wp[4 * q4 + 1], wp[4 * q4 + 2],
-                                                     wp[4 * q4 + 3]};
-#pragma unroll
-                                for (int k = 0; k < 4; ++k)
-                                    hacc2[j2] = fma2(f2(wv[k], wv[k]),
-                                                     f2(vkeep[4 * q4 + k], v[4 * q4 + k]), hacc2[j2]);
-                            }
-                        }
+                        for (int i = 0; i < 8; ++i)
+                            hsum[px][j2] = fma2(f2(wp[2 * i], wp[2 * i + 1]),
+                                                f2(v[2 * i], v[2 * i + 1]), hsum[px][j2]);
                     }
                     if (!p.y && !p.y_f32) return;
                 }
@@ -1497,11 +1488,12 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                     float o[6];
 #pragma unroll
                     for (int j2 = 0; j2 < 3; ++j2) {
-                        float h0, h1;
-                        unf2(hacc2[j2], h0, h1);
+                        float e0, o0, e1, o1;
+                        unf2(hsum[0][j2], e0, o0);
+                        unf2(hsum[1][j2], e1, o1);
                         const float b = __ldg(p.head_b + j2);
-                        o[j2] = sigmoid_fast(h0 + b);
-                        o[3 + j2] = sigmoid_fast(h1 + b);
+                        o[j2] = sigmoid_fast((e0 + o0) + b);
+                        o[3 + j2] = sigmoid_fast((e1 + o1) + b);
                     }
                     float2 *dst = reinterpret_cast<float2 *>(p.head_out + pix * 3);
                     dst[0] = make_float2(o[0], o[1]);
@@ -1511,11 +1503,12 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
 #pragma unroll
                     for (int j2 = 0; j2 < 4; ++j2) {
                         if (j2 >= p.head_c) break;
-                        float h0, h1;
-                        unf2(hacc2[j2], h0, h1);
+                        float e0, o0, e1, o1;
+                        unf2(hsum[0][j2], e0, o0);
+                        unf2(hsum[1][j2], e1, o1);
                         const float b = __ldg(p.head_b + j2);
-                        p.head_out[pix * p.head_c + j2] = sigmoid_fast(h0 + b);
-                        p.head_out[(pix + 1) * p.head_c + j2] = sigmoid_fast(h1 + b);
+                        p.head_out[pix * p.head_c + j2] = sigmoid_fast((e0 + o0) + b);
+                        p.head_out[(pix + 1) * p.head_c + j2] = sigmoid_fast((e1 + o1) + b);
                     }
                 }
             }

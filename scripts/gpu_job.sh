@@ -1,2 +1,1 @@
-s0=$(date +%s); python bench.py > gpurun_out/r02_bench_default.json 2> gpurun_out/r02_bench_default.err; echo wall $(( $(date +%s) - s0 )) s; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_default.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['steps'], d['warmup'], d['roofline']['frac'], d['roofline']['other']['frac'])"
-s0=$(date +%s); python bench.py --impl reference > gpurun_out/r02_ref_default.json 2> gpurun_out/r02_ref_default.err; echo wall $(( $(date +%s) - s0 )) s; tail -c 300 gpurun_out/r02_ref_default.json
+for r in 1 2 3; do echo "new $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "old $(LS_LIB_PATH=scripts/exp/liblidarsplat_old.so timeout 120 python scripts/time_unet.py | tail -1)"; done
