@@ -94,7 +94,7 @@ struct ConvParamsP {
     // k_conv_px2: the 32 columns' BN scale / shift as kernel parameters (copied at
     // plan creation) -- the epilogue reads them as constant-bank operands instead
     // of shared-memory loads, which competed with the MMA operand reads in L1
-    float pc_scale[32], pc_shift[32];
+    float pc_scale[64], pc_shift[64];
     float pc_head[4 * 32];  // k_conv_px2 head: the final 1x1 conv's weights [head_c][32]
     int resident;           // weights resident in smem
     int stages;
@@ -1091,17 +1091,28 @@ struct CfgPx {
 // MMAs' extra operand reads lose.
 // epilogue warpgroups: KX2 items hold 128 TMEM columns and their epilogue
 // more live registers (three groups: 448 threads, up to 144 registers)
-template <bool G3>
-__host__ __device__ constexpr int px_groups() { return G3 ? LS_KX2_GROUPS : CfgPx::kEpiGroups; }
+template <bool G3, int CO = 32>
+__host__ __device__ constexpr int px_groups() {
+    return G3 ? (CO == 64 ? 2 : LS_KX2_GROUPS) : CfgPx::kEpiGroups;
+}
 
-template <int MODE, bool C8, bool KX2 = false>
-__global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
+// KX2 with 64 channels (CO = 64 outputs, CI = 32 or 64 inputs; the half-
+// resolution enc1 / dec1 layers): TMEM item [spill-left | out(2j) | out(2j+1) |
+// spill-right] x 64 = 256 columns (2 buffers), N = 192 MMAs, B tiles of 192 rows.
+// With CI = 64 a pair's two pixels are 128 B rows of two TMA boxes (a 5-D view
+// [c][element][pair][row][image] of the NHWC tensor, one box per element).
+template <int MODE, bool C8, bool KX2 = false, int CO = 32, int CI = 32>
+__global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
+    static_assert(CO == 32 || (KX2 && MODE != kHead), "64-channel pixel pairs: KX2, no head");
+    static_assert(CI == 32 || (KX2 && CO == 64), "64-channel inputs: KX2 64-channel form");
     using C = CfgPx;
-    constexpr int kN = KX2 ? 128 : C::kN;       // TMEM columns per item
-    constexpr int kAcc = KX2 ? 4 : C::kAcc;
-    constexpr int kGroups = px_groups<KX2 || C8>();
+    constexpr int kN = KX2 ? 4 * CO : C::kN;     // TMEM columns per item
+    constexpr int kAcc = KX2 ? 512 / kN : C::kAcc;
+    constexpr int kGroups = px_groups<KX2 || C8, CO>();
+    constexpr int kT = CI / 16;                   // K16 steps per element and source
+    constexpr uint32_t kBT = 3u * CO * 32u;       // KX2 B tile [W(2) ; W(1) ; W(0)] bytes
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const uint32_t sbase = smem_u32(smem);
@@ -1174,15 +1185,15 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             if (C8) {
                 mbar_arrive(bres);  // B tiles were built before the block barrier
             } else if (KX2) {
-                // tile (src, ky, t): rows [W(2) ; W(1) ; W(0)], 3 KB
-                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2) * 3072u);
+                // tile (src, ky, t): rows [W(2) ; W(1) ; W(0)], kBT bytes
+                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * kT) * kBT);
                 for (int src = 0; src < nsrc; ++src)
                     for (int ky = 0; ky < 3; ++ky)
-                        for (int t = 0; t < 2; ++t)
+                        for (int t = 0; t < kT; ++t)
                             for (int r = 0; r < 3; ++r)
-                                tma_load_3d(smem + p.off_b + ((src * 3 + ky) * 2 + t) * 3072 +
-                                                r * 1024,
-                                            &mB, src * 32 + 16 * t, 0, (2 - r) * 3 + ky, bres);
+                                tma_load_3d(smem + p.off_b + ((src * 3 + ky) * kT + t) * kBT +
+                                                r * (CO * 32),
+                                            &mB, src * CI + 16 * t, 0, (2 - r) * 3 + ky, bres);
             } else {
                 mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
             }
@@ -1205,9 +1216,16 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                           y0 = (p.ty0 + walk.TY(p)) * kTH;
                 for (int q = 0; q < nsrc; ++q, s = s + 1 == S ? 0 : s + 1, ph ^= s == 0) {
                     mbar_wait(empty + s, ph ^ 1u);
-                    mbar_expect_tx(full + s, p.a_tx);
-                    tma_load_4d(smem + C::kRingPad + (size_t)s * p.stage_bytes, q ? &mA1 : &mA0, 0,
-                                px0, y0 - 1, img, full + s);
+                    uint8_t *st = smem + C::kRingPad + (size_t)s * p.stage_bytes;
+                    if constexpr (CI == 64) {
+                        // element 0 / element 1 boxes of the pair-split 5-D view
+                        mbar_expect_tx(full + s, 2u * p.a_tx);
+                        tma_load_5d(st, q ? &mA1 : &mA0, 0, 0, px0, y0 - 1, img, full + s);
+                        tma_load_5d(st + p.a_bytes, q ? &mA1 : &mA0, 0, 1, px0, y0 - 1, img, full + s);
+                    } else {
+                        mbar_expect_tx(full + s, p.a_tx);
+                        tma_load_4d(st, q ? &mA1 : &mA0, 0, px0, y0 - 1, img, full + s);
+                    }
                 }
             }
         }
@@ -1215,7 +1233,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
         if (elect_one()) {
             // ------------------------------- MMA issuer -------------------------------
             const uint32_t id64 = idesc_bf16(128, 64), id32 = idesc_bf16(128, 32);
-            const uint32_t id96 = idesc_bf16(128, 96);
+            // KX2 MMA shapes: 3, 2 and 1 output blocks of CO columns
+            const uint32_t idN3 = idesc_bf16(128, 3 * CO), idN2 = idesc_bf16(128, 2 * CO),
+                           idN1 = idesc_bf16(128, CO);
             const uint64_t aproto = smem_desc(0, kARow, C8 ? kSwizzle32B : kSwizzle128B);
             const uint64_t bproto = smem_desc(0, 32, kSwizzle32B);
             const uint32_t ahi = (uint32_t)(aproto >> 32), alo = (uint32_t)aproto;
@@ -1235,30 +1255,35 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                         alo + ((sbase + C::kRingPad + (uint32_t)s * p.stage_bytes) >> 4);
                     const uint32_t b_lo = blo + ((sbase + btile(q, 0, 0, 0)) >> 4);
                     if constexpr (KX2) {
-                        const uint32_t bk = blo + ((sbase + p.off_b + (uint32_t)q * 6 * 3072u) >> 4);
+                        const uint32_t bk =
+                            blo + ((sbase + p.off_b + (uint32_t)q * 3 * kT * kBT) >> 4);
 #pragma unroll
                         for (int ky = 0; ky < 3; ++ky) {
 #pragma unroll
-                            for (int t = 0; t < 2; ++t) {
+                            for (int t = 0; t < kT; ++t) {
                                 const uint32_t arow = (uint32_t)(ky * kTW) * C::kRow;
+                                // CI = 32: both elements in one 128 B pair row; CI = 64:
+                                // element 1 in the second box of the stage
                                 const uint32_t a_e0 = (arow + 32 * t) / 16;
-                                const uint32_t a_e1 = (arow + 64 + 32 * t) / 16;
-                                const uint32_t bt = (uint32_t)((ky * 2 + t) * 3072) / 16;
+                                const uint32_t a_e1 =
+                                    (CI == 64 ? p.a_bytes + arow + 32 * t : arow + 64 + 32 * t) / 16;
+                                const uint32_t bt = (uint32_t)((ky * kT + t) * kBT) / 16;
                                 const bool first = (q | ky | t) == 0;
                                 // element 0 -> [spill-left | out(2j) | out(2j+1)]
                                 mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e0),
-                                         ((uint64_t)bhi << 32) | (bk + bt), id96, first ? 0u : 1u);
+                                         ((uint64_t)bhi << 32) | (bk + bt), idN3, first ? 0u : 1u);
                                 if (first) {
-                                    // element 1's first step: columns 32..95 accumulate onto
-                                    // element 0's, 96..127 (spill-right) start fresh
-                                    mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
-                                             ((uint64_t)bhi << 32) | (bk + bt), id64, 1u);
-                                    mma_bf16(d0 + 96, ((uint64_t)ahi << 32) | (a_lo + a_e1),
-                                             ((uint64_t)bhi << 32) | (bk + bt + 2048 / 16), id32, 0u);
+                                    // element 1's first step: columns CO..3CO-1 accumulate onto
+                                    // element 0's, 3CO..4CO-1 (spill-right) start fresh
+                                    mma_bf16(d0 + CO, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt), idN2, 1u);
+                                    mma_bf16(d0 + 3 * CO, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt + 2 * CO * 32 / 16), idN1,
+                                             0u);
                                 } else {
                                     // element 1 -> [out(2j) | out(2j+1) | spill-right]
-                                    mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
-                                             ((uint64_t)bhi << 32) | (bk + bt), id96, 1u);
+                                    mma_bf16(d0 + CO, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                             ((uint64_t)bhi << 32) | (bk + bt), idN3, 1u);
                                 }
                             }
                         }
@@ -1326,9 +1351,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
             // this lane's first output pixel and the item's store bases (one 64-bit
             // address computation per item instead of one per 16-channel store)
             const int64_t pix0 = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
-            __nv_bfloat16 *const ybase = p.y ? p.y + pix0 * 32 : nullptr;
+            __nv_bfloat16 *const ybase = p.y ? p.y + pix0 * CO : nullptr;
             __nv_bfloat16 *const pbase =
-                MODE == kPool ? p.pool + (((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp) * 32
+                MODE == kPool ? p.pool + (((int64_t)img * (p.h / 2) + gy / 2) * (p.w / 2) + gp) * CO
                               : nullptr;
             // head sums per pixel and output as {even channels, odd channels}
             // partials: the activations come out of the packed epilogue math as
@@ -1382,8 +1407,8 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
 #pragma unroll
                 for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
                 if (valid) {
-                    // element offsets from the item's per-lane base (cout = 32)
-                    if (p.y) st_global_v8(ybase + px * 32 + n, pk);
+                    // element offsets from the item's per-lane base (cout = CO)
+                    if (p.y) st_global_v8(ybase + px * CO + n, pk);
                     if (p.y_f32) {
                         const int64_t pix = pix0 + px;
                         float4 *dst = reinterpret_cast<float4 *>(p.y_f32 + pix * p.cout + n);
@@ -1417,15 +1442,15 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8>()) k_conv_px2(
                 // 16-channel block n: out(2j) = own + left lane's spill-right,
                 // out(2j+1) = own + right lane's spill-left
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
+                for (int h2 = 0; h2 < CO / 16; ++h2) {
                     const uint32_t n = 16u * h2;
                     uint32_t sl[16], o0[16], o1[16], sr[16];
                     tmem_ld16_async(tbase + n, sl);
-                    tmem_ld16_async(tbase + 32u + n, o0);
-                    tmem_ld16_async(tbase + 64u + n, o1);
-                    tmem_ld16_async(tbase + 96u + n, sr);
+                    tmem_ld16_async(tbase + (uint32_t)CO + n, o0);
+                    tmem_ld16_async(tbase + (uint32_t)(2 * CO) + n, o1);
+                    tmem_ld16_async(tbase + (uint32_t)(3 * CO) + n, sr);
                     tmem_ld_wait4(sl, o0, o1, sr);
-                    if (h2 == 1) {  // item fully read -> hand the TMEM buffer back
+                    if (h2 == CO / 16 - 1) {  // item fully read -> hand the TMEM buffer back
                         fence_before_sync();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(tempty + ab);
@@ -1562,6 +1587,22 @@ static bool encode_act(CUtensorMap *map, const void *base, int c, int w, int h, 
     cuuint32_t es[4] = {1, 1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides,
               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(chunk * 2),
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 64-channel NHWC activations as pixel pairs split by element: a 5-D view
+// [c = 64][element = 2][pair = w/2][row][image], box {64, 1, 16, box_h, 1}
+// (one 128 B operand row per pair and element, 128 B swizzle)
+static bool encode_act_pairsplit(CUtensorMap *map, const void *base, int w, int h, int batch,
+                                 int box_h) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[5] = {64, 2, (cuuint64_t)(w / 2), (cuuint64_t)h, (cuuint64_t)batch};
+    cuuint64_t strides[4] = {128, 256, (cuuint64_t)w * 128, (cuuint64_t)h * w * 128};
+    cuuint32_t box[5] = {64, 1, (cuuint32_t)kTW, (cuuint32_t)box_h, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(base), dims, strides,
+              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1750,13 +1791,13 @@ static int launch_kx(const ls_conv_plan *pl, cudaStream_t st) {
     return pl->p.cout == 32 ? launch_kx_c<CHUNK, 32>(pl, st) : launch_kx_c<CHUNK, 64>(pl, st);
 }
 
-template <int MODE, bool C8, bool KX2 = false>
+template <int MODE, bool C8, bool KX2 = false, int CO = 32, int CI = 32>
 static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
-    if (int e = smem_optin(k_conv_px2<MODE, C8, KX2>, attr_done)) return e;
+    if (int e = smem_optin(k_conv_px2<MODE, C8, KX2, CO, CI>, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8>()));
+    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8, CO>()));
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -1764,11 +1805,19 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8, KX2>, pl->a0, pl->a1, pl->b, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8, KX2, CO, CI>, pl->a0, pl->a1, pl->b,
+                                   pl->p);
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
     if (pl->chunk == 16) return launch_px2_m<kPlain, true>(pl, st);  // e0c1: plain only
+    if (pl->mt == 3 && pl->bn == 64) {  // KX2, 64 output channels (chunk 64 / 128: 32 / 64 inputs)
+        if (pl->chunk == 128)
+            return pl->mode == kPool ? launch_px2_m<kPool, false, true, 64, 64>(pl, st)
+                                     : launch_px2_m<kPlain, false, true, 64, 64>(pl, st);
+        return pl->mode == kPool ? launch_px2_m<kPool, false, true, 64, 32>(pl, st)
+                                 : launch_px2_m<kPlain, false, true, 64, 32>(pl, st);
+    }
     if (pl->mt == 3) {  // KX2 variant
         switch (pl->mode) {
             case kPlain: return launch_px2_m<kPlain, false, true>(pl, st);
@@ -1914,7 +1963,8 @@ static bool chunk_ok(int c) { return c == 16 || c == 32 || (c > 0 && c % 64 == 0
 
 // Plan of a 32 -> 32 (or [32, 32] -> 32) 3x3 layer on k_conv_px2 (null when
 // it does not apply: odd width).
-static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint16_t *d_x1, int c1, int batch,
+static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint16_t *d_x1, int c1,
+                              int cout, int batch,
                               int h, int w, const uint16_t *d_w, const float *d_scale,
                               const float *d_shift, int act, float alpha, uint16_t *d_y,
                               float *d_y_f32, uint16_t *d_pool, const float *d_head_w,
@@ -1929,12 +1979,18 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.h = h;
     p.w = w;
     const bool c8 = c0 == 8;
-    p.c0 = c8 ? 16 : 32;
+    // KX2 64-channel form: cout 64, inputs of 32 or 64 channels (one source)
+    if (cout != 32 && !(kx2 && cout == 64 && c1 == 0 && (c0 == 32 || c0 == 64))) {
+        delete pl;
+        return nullptr;
+    }
+    const bool ci64 = c0 == 64;
+    p.c0 = c8 ? 16 : c0;
     p.c1 = c1;
     p.ctot = p.c0 + c1;
     p.wts = d_w;
-    if (cudaMemcpy(p.pc_scale, d_scale, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
-        cudaMemcpy(p.pc_shift, d_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+    if (cudaMemcpy(p.pc_scale, d_scale, cout * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(p.pc_shift, d_shift, cout * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
         (d_head_w && cudaMemcpy(p.pc_head, d_head_w, (size_t)head_c * 32 * sizeof(float),
                                 cudaMemcpyDeviceToHost) != cudaSuccess)) {
         delete pl;
@@ -1943,8 +1999,8 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.kxs = 3;
     p.kxps = 1;
     p.pad = 1;
-    p.n_total = 32;
-    p.cout = 32;
+    p.n_total = cout;
+    p.cout = cout;
     p.act = act;
     p.alpha = alpha;
     p.scale = d_scale;
@@ -1968,37 +2024,47 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.a_bytes = (p.a_tx + 1023u) & ~1023u;
     p.b_blk = CfgPx::kBTile;
     p.resident = 1;
+    // KX2 B tiles: per (source, ky, K16 step) 3 x cout rows x 32 B
     const size_t res_bytes = c8 ? (size_t)3 * 4096
-                                : (kx2 ? (size_t)p.nq * 6 * 3072 : (size_t)p.nq * 12 * CfgPx::kBTile);
+                                : (kx2 ? (size_t)p.nq * 3 * (p.c0 / 16) * 3 * cout * 32
+                                       : (size_t)p.nq * 12 * CfgPx::kBTile);
     const size_t const_bytes =
-        ((size_t)(2 * 32 + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
+        ((size_t)(2 * cout + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
     const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
-    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.a_bytes) : 0;
+    const uint32_t stage_bytes = (ci64 ? 2u : 1u) * p.a_bytes;  // 64-ch inputs: two element boxes
+    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
     if (stages < 3) {
         delete pl;
         return nullptr;
     }
     if (stages > 8) stages = 8;
     p.stages = stages;
-    p.stage_bytes = p.a_bytes;
+    p.stage_bytes = stage_bytes;
     p.off_b = (uint32_t)(CfgPx::kRingPad + stages * p.stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
     p.off_bar = p.off_pool;
     pl->smem = 1024 + p.off_bar + 512;
-    pl->bn = 32;
-    pl->chunk = c8 ? 16 : 64;
+    pl->bn = cout;
+    pl->chunk = c8 ? 16 : 2 * c0;  // pair-row channels (128: two 64-channel element boxes)
     pl->kind = 2;
     pl->mt = kx2 && !c8 ? 3 : 1;  // 3 marks the KX2 variant
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
     const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
     pl->full_tiles_y = p.tiles_y;
-    // the NHWC tensors read as (W/2) pair pixels of 2*c channels
+    // the NHWC tensors read as (W/2) pair pixels of 2*c channels (64-channel
+    // inputs: one box per element)
     const int pc = c8 ? 16 : 64;
-    bool ok = encode_act(&pl->a0, d_x0, pc, w / 2, h, batch, pc, kTH + 2);
-    ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, pc, w / 2, h, batch, pc, kTH + 2);
-    ok = ok && encode_wts(&pl->b, d_w, p.ctot, 32, 9, 16, 32, 1);
+    bool ok;
+    if (ci64) {
+        ok = encode_act_pairsplit(&pl->a0, d_x0, w, h, batch, kTH + 2);
+        pl->a1 = pl->a0;
+    } else {
+        ok = encode_act(&pl->a0, d_x0, pc, w / 2, h, batch, pc, kTH + 2);
+        ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, pc, w / 2, h, batch, pc, kTH + 2);
+    }
+    ok = ok && encode_wts(&pl->b, d_w, p.ctot, cout, 9, 16, cout, 1);
     if (!ok) {
         delete pl;
         return nullptr;
@@ -2134,11 +2200,16 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     const int kx2_mode = kx2_setting();
     const bool kx2 = cout == 32 && c0_tensor == 32 && (c1 == 0 || c1 == 32) &&
                      (kx2_mode == 2 || (kx2_mode == 1 && c1 == 32));
-    const bool px2_fit = kx2 || (cout == 32 && c1 == 0 &&
+    // 64-channel single-source layers (enc1 conv1 / conv2, dec1 conv2) on the
+    // KX2 pixel-pair form (LS_CONV_KX2_64=0: k_conv_p)
+    const bool kx2_64 = cout == 64 && c1 == 0 && (c0_tensor == 32 || c0_tensor == 64) &&
+                        !d_head_w && env_int("LS_CONV_KX2_64", 1) != 0;
+    const bool px2_fit = kx2 || kx2_64 || (cout == 32 && c1 == 0 &&
                          ((c0_tensor == 32 && (px2_mask() & 1)) ||
                           (c0_tensor == 8 && !d_pool && !d_head_w && (px2_mask() & 2))));
     if (!transposed && px2_fit) {
-        ls_conv_plan *pp = plan_px2(kx2, d_x0, c0_tensor, d_x1, c1, batch, h, w, d_w, d_scale, d_shift, act,
+        ls_conv_plan *pp = plan_px2(kx2 || kx2_64, d_x0, c0_tensor, d_x1, c1, cout, batch, h, w,
+                                    d_w, d_scale, d_shift, act,
                                     alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
                                     d_head_out);
         if (pp) {

@@ -1,1 +1,5 @@
-for r in 1 2 3; do echo "new $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "old $(LS_LIB_PATH=scripts/exp/liblidarsplat_old.so timeout 120 python scripts/time_unet.py | tail -1)"; done
+timeout 600 python -m pytest tests/test_gpu_unet.py -x -q -k "layer" 2>&1 | tail -3
+timeout 600 python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -1
+for r in 1 2; do echo "kx2_64 $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "base $(LS_CONV_KX2_64=0 timeout 120 python scripts/time_unet.py | tail -1)"; done
+M=gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,sm__cycles_active.avg,smsp__cycles_active.avg
+N=1 timeout 300 ncu --metrics $M --clock-control none -k regex:k_conv -c 22 --csv python scripts/time_unet.py > gpurun_out/m_kx264.csv 2>/dev/null

@@ -40,9 +40,15 @@ LAYER_CASES = [
     dict(c0=128, c1=0, cout=256, h=17, w=30, act=2),
     dict(c0=256, c1=0, cout=256, h=16, w=32, act=1, pool=True),
     dict(c0=64, c1=0, cout=512, h=96, w=128, act=1),  # 256-column pair tiles
-    # k_conv_kx (cout = 64, K >= 128) on CTA pairs: two sources, ragged rows, pool
+    # k_conv_kx (cout = 64, K >= 128): two sources, ragged rows
     dict(c0=64, c1=64, cout=64, h=20, w=36, act=2),
     dict(c0=128, c1=0, cout=64, h=16, w=30, act=1, pool=True, batch=2),
+    # 64-channel KX2 pixel pairs (32 / 64 inputs): ragged tiles (50 pairs), rows
+    # not a multiple of 8, pool, batches; odd width falls back to k_conv_p
+    dict(c0=32, c1=0, cout=64, h=20, w=100, act=1, batch=2),
+    dict(c0=64, c1=0, cout=64, h=18, w=58, act=2),
+    dict(c0=64, c1=0, cout=64, h=10, w=36, act=1, pool=True, batch=3),
+    dict(c0=64, c1=0, cout=64, h=9, w=31, act=1),
 ]
 
 
