@@ -62,6 +62,10 @@ using namespace ls::umma;
 #ifndef LS_KX2_GROUPS
 #define LS_KX2_GROUPS 3
 #endif
+// k_conv_px2 KX2 epilogue warpgroups with 64 output channels (A/B build switch)
+#ifndef LS_KX2_64_GROUPS
+#define LS_KX2_64_GROUPS 2
+#endif
 // k_conv_kx (cout = 32): issue the second 16-channel half's TMEM loads before
 // processing the first (A/B build switch)
 #ifndef LS_KX_PIPE
@@ -1093,7 +1097,7 @@ struct CfgPx {
 // more live registers (three groups: 448 threads, up to 144 registers)
 template <bool G3, int CO = 32>
 __host__ __device__ constexpr int px_groups() {
-    return G3 ? (CO == 64 ? 2 : LS_KX2_GROUPS) : CfgPx::kEpiGroups;
+    return G3 ? (CO == 64 ? LS_KX2_64_GROUPS : LS_KX2_GROUPS) : CfgPx::kEpiGroups;
 }
 
 // KX2 with 64 channels (CO = 64 outputs, CI = 32 or 64 inputs; the half-
@@ -1111,6 +1115,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
     constexpr int kN = KX2 ? 4 * CO : C::kN;     // TMEM columns per item
     constexpr int kAcc = KX2 ? 512 / kN : C::kAcc;
     constexpr int kGroups = px_groups<KX2 || C8, CO>();
+    // an epilogue group waits on an accumulator's tfull parity at most one phase
+    // ahead only if groups <= buffers (3 groups on 2 buffers read stale items)
+    static_assert(!KX2 || kGroups <= kAcc, "KX2: epilogue warpgroups <= TMEM buffers");
     constexpr int kT = CI / 16;                   // K16 steps per element and source
     constexpr uint32_t kBT = 3u * CO * 32u;       // KX2 B tile [W(2) ; W(1) ; W(0)] bytes
     extern __shared__ uint8_t smem_raw[];
