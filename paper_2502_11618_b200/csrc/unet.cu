@@ -1109,11 +1109,13 @@ template <int MODE, bool C8, bool KX2 = false, int CO = 32, int CI = 32>
 __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
     const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
-    static_assert(CO == 32 || (KX2 && MODE != kHead), "64-channel pixel pairs: KX2, no head");
-    static_assert(CI == 32 || (KX2 && CO == 64), "64-channel inputs: KX2 64-channel form");
+    static_assert(CO == 32 || (!C8 && MODE != kHead), "64-channel pixel pairs: no head");
+    static_assert(CI == 32 || (!C8 && CO == 64), "64-channel inputs: 64-channel forms only");
     using C = CfgPx;
-    constexpr int kN = KX2 ? 4 * CO : C::kN;     // TMEM columns per item
-    constexpr int kAcc = KX2 ? 512 / kN : C::kAcc;
+    // TMEM columns per item: KX2 [sl | o0 | o1 | sr] x CO, neighbour-row [o0 | o1] x CO
+    constexpr int kN = KX2 ? 4 * CO : (C8 ? C::kN : 2 * CO);
+    constexpr int kAcc = KX2 ? 512 / kN : (CO == 64 ? 4 : C::kAcc);
+    constexpr uint32_t kBTn = 2u * CO * 32u;      // neighbour-row B tile [W(1+e) ; W(e)] bytes
     constexpr int kGroups = px_groups<KX2 || C8, CO>();
     // an epilogue group waits on an accumulator's tfull parity at most one phase
     // ahead only if groups <= buffers (3 groups on 2 buffers read stale items)
@@ -1182,7 +1184,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
     // B tile (source s, ky, element e, channel block t): rows 0-31 = W(kx=1+e),
     // rows 32-63 = W(kx=e), 16 channels each
     auto btile = [&](int src, int ky, int e, int t) -> uint32_t {
-        return p.off_b + (uint32_t)((((src * 3 + ky) * 2 + e) * 2 + t)) * C::kBTile;
+        return p.off_b + (uint32_t)((((src * 3 + ky) * 2 + e) * kT + t)) * kBTn;
     };
     constexpr uint32_t kARow = C8 ? 32u : C::kRow;
 
@@ -1202,16 +1204,16 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                                                 r * (CO * 32),
                                             &mB, src * CI + 16 * t, 0, (2 - r) * 3 + ky, bres);
             } else {
-                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * 2) * C::kBTile);
+                mbar_expect_tx(bres, (uint32_t)(nsrc * 3 * 2 * kT) * kBTn);
             }
             for (int src = 0; src < ((C8 || KX2) ? 0 : nsrc); ++src)
                 for (int ky = 0; ky < 3; ++ky)
                     for (int e = 0; e < 2; ++e)
-                        for (int t = 0; t < 2; ++t)
+                        for (int t = 0; t < kT; ++t)
                             for (int r = 0; r < 2; ++r) {
                                 const int kx = r == 0 ? 1 + e : e;
-                                tma_load_3d(smem + btile(src, ky, e, t) + r * (C::kBTile / 2), &mB,
-                                            src * 32 + 16 * t, 0, kx * 3 + ky, bres);
+                                tma_load_3d(smem + btile(src, ky, e, t) + r * (kBTn / 2), &mB,
+                                            src * CI + 16 * t, 0, kx * 3 + ky, bres);
                             }
             LS_GDC_WAIT();
             int s = 0;
@@ -1310,23 +1312,26 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
 #pragma unroll
                     for (int ky = 0; ky < 3; ++ky) {
 #pragma unroll
-                        for (int t = 0; t < 2; ++t) {
+                        for (int t = 0; t < kT; ++t) {
                             // A: operand row (ky*16 + pair), K offset e*64 B + t*32 B
+                            // (64-channel inputs: element e in box e of the stage)
                             const uint32_t arow = (uint32_t)(ky * kTW) * C::kRow;
-                            const uint32_t a_e0 = (arow + 32 * t) / 16, a_e1 = (arow + 64 + 32 * t) / 16;
-                            const uint32_t b_e0 = ((ky * 2 + 0) * 2 + t) * C::kBTile / 16;
-                            const uint32_t b_e1 = ((ky * 2 + 1) * 2 + t) * C::kBTile / 16;
+                            const uint32_t a_e0 = (arow + 32 * t) / 16;
+                            const uint32_t a_e1 =
+                                (CI == 64 ? p.a_bytes + arow + 32 * t : arow + 64 + 32 * t) / 16;
+                            const uint32_t b_e0 = ((ky * 2 + 0) * kT + t) * kBTn / 16;
+                            const uint32_t b_e1 = ((ky * 2 + 1) * kT + t) * kBTn / 16;
                             const uint32_t first = (q | ky | t) == 0 ? 0u : 1u;
                             mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e0),
-                                     ((uint64_t)bhi << 32) | (b_lo + b_e0), id64, first);
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e0), idN2, first);
                             mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e1),
-                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), id64, 1u);
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), idN2, 1u);
                             // x(2j-1) -> out(2j): previous row's element 1, W(kx=0)
                             mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e1 - C::kRow / 16),
-                                     ((uint64_t)bhi << 32) | (b_lo + b_e0 + C::kBTile / 32), id32, 1u);
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e0 + kBTn / 32), idN1, 1u);
                             // x(2j+2) -> out(2j+1): next row's element 0, W(kx=2)
-                            mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e0 + C::kRow / 16),
-                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), id32, 1u);
+                            mma_bf16(d0 + CO, ((uint64_t)ahi << 32) | (a_lo + a_e0 + C::kRow / 16),
+                                     ((uint64_t)bhi << 32) | (b_lo + b_e1), idN1, 1u);
                         }
                     }
                     }
@@ -1370,7 +1375,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
             // 16-column groups in the order (px0, ch 0-15), (px1, 0-15), (px0, 16-31),
             // (px1, 16-31); group g+1's tcgen05.ld is in flight while g is processed
             uint32_t ra[16], rb[16];
-            auto col = [&](int g) -> uint32_t { return tbase + (uint32_t)((g & 1) * 32 + (g >> 1) * 16); };
+            auto col = [&](int g) -> uint32_t { return tbase + (uint32_t)((g & 1) * CO + (g >> 1) * 16); };
             // BN fold + activation of 16 channels of NP pixels (constants read once)
             auto bnact = [&](int n, const uint32_t(&r0)[16], const uint32_t(&r1)[16],
                              float(&v0)[16], float(&v1)[16], int np) {
@@ -1492,25 +1497,30 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
             tmem_ld16_async(col(1), rb);
             tmem_ld_wait16(ra);
             tmem_ld_wait16(rb);
-            tmem_ld16_async(col(2), rc);
-            tmem_ld16_async(col(3), rd);
-            {
+#pragma unroll
+            for (int blk = 0; blk < CO / 16; ++blk) {
+                // (blocks alternate between the (ra, rb) and (rc, rd) registers)
+                uint32_t(&c0)[16] = (blk & 1) ? rc : ra;
+                uint32_t(&c1)[16] = (blk & 1) ? rd : rb;
+                uint32_t(&n0)[16] = (blk & 1) ? ra : rc;
+                uint32_t(&n1)[16] = (blk & 1) ? rb : rd;
+                if (blk + 1 < CO / 16) {
+                    tmem_ld16_async(col(2 * blk + 2), n0);
+                    tmem_ld16_async(col(2 * blk + 3), n1);
+                } else {
+                    // item fully read -> hand the TMEM buffer back
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty + ab);
+                }
                 float v0[16], v1[16];
-                bnact(0, ra, rb, v0, v1, 2);
-                emit(0, v0);
-                emit(1, v1);
-            }
-            tmem_ld_wait16(rc);
-            tmem_ld_wait16(rd);
-            // item fully read -> hand the TMEM buffer back
-            fence_before_sync();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + ab);
-            {
-                float v0[16], v1[16];
-                bnact(16, rc, rd, v0, v1, 2);
-                emit(2, v0);
-                emit(3, v1);
+                bnact(16 * blk, c0, c1, v0, v1, 2);
+                emit(2 * blk, v0);
+                emit(2 * blk + 1, v1);
+                if (blk + 1 < CO / 16) {
+                    tmem_ld_wait16(n0);
+                    tmem_ld_wait16(n1);
+                }
             }
             }
             if (MODE == kHead && valid) {
@@ -1818,6 +1828,13 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
     if (pl->chunk == 16) return launch_px2_m<kPlain, true>(pl, st);  // e0c1: plain only
+    if (pl->mt == 1 && pl->bn == 64) {  // neighbour-row pairs, 64 output channels
+        if (pl->chunk == 128)
+            return pl->mode == kPool ? launch_px2_m<kPool, false, false, 64, 64>(pl, st)
+                                     : launch_px2_m<kPlain, false, false, 64, 64>(pl, st);
+        return pl->mode == kPool ? launch_px2_m<kPool, false, false, 64, 32>(pl, st)
+                                 : launch_px2_m<kPlain, false, false, 64, 32>(pl, st);
+    }
     if (pl->mt == 3 && pl->bn == 64) {  // KX2, 64 output channels (chunk 64 / 128: 32 / 64 inputs)
         if (pl->chunk == 128)
             return pl->mode == kPool ? launch_px2_m<kPool, false, true, 64, 64>(pl, st)
@@ -1986,8 +2003,9 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.h = h;
     p.w = w;
     const bool c8 = c0 == 8;
-    // KX2 64-channel form: cout 64, inputs of 32 or 64 channels (one source)
-    if (cout != 32 && !(kx2 && cout == 64 && c1 == 0 && (c0 == 32 || c0 == 64))) {
+    // 64-channel forms (KX2 or neighbour-row): cout 64, inputs of 32 or 64
+    // channels (one source)
+    if (cout != 32 && !(cout == 64 && c1 == 0 && (c0 == 32 || c0 == 64))) {
         delete pl;
         return nullptr;
     }
@@ -2031,10 +2049,11 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.a_bytes = (p.a_tx + 1023u) & ~1023u;
     p.b_blk = CfgPx::kBTile;
     p.resident = 1;
-    // KX2 B tiles: per (source, ky, K16 step) 3 x cout rows x 32 B
+    // KX2 B tiles: per (source, ky, K16 step) 3 x cout rows x 32 B; neighbour-row
+    // tiles: per (source, ky, element, K16 step) 2 x cout rows x 32 B
     const size_t res_bytes = c8 ? (size_t)3 * 4096
                                 : (kx2 ? (size_t)p.nq * 3 * (p.c0 / 16) * 3 * cout * 32
-                                       : (size_t)p.nq * 12 * CfgPx::kBTile);
+                                       : (size_t)p.nq * 3 * 2 * (p.c0 / 16) * 2 * cout * 32);
     const size_t const_bytes =
         ((size_t)(2 * cout + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
     const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
@@ -2215,7 +2234,14 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
                          ((c0_tensor == 32 && (px2_mask() & 1)) ||
                           (c0_tensor == 8 && !d_pool && !d_head_w && (px2_mask() & 2))));
     if (!transposed && px2_fit) {
-        ls_conv_plan *pp = plan_px2(kx2 || kx2_64, d_x0, c0_tensor, d_x1, c1, cout, batch, h, w,
+        // 64-channel layers: the neighbour-row form (4 TMEM buffers of 128 columns)
+        // for 32-channel inputs, whose short K loop leaves the 2-buffer KX2 form
+        // waiting on its accumulator round trip (e1c1 35.8 -> 30.5 us), KX2 for
+        // 64-channel inputs (e1c2 43.4 vs 49.7, d1c2 41.0 vs 42.5 us).
+        // LS_CONV_PX64: 0 = KX2 always, 1 = neighbour-row always, 2 = by input
+        const int px64 = env_int("LS_CONV_PX64", 2);
+        const bool nbr64 = kx2_64 && (px64 == 1 || (px64 == 2 && c0_tensor == 32));
+        ls_conv_plan *pp = plan_px2(kx2 || (kx2_64 && !nbr64), d_x0, c0_tensor, d_x1, c1, cout, batch, h, w,
                                     d_w, d_scale, d_shift, act,
                                     alpha, d_y, d_y_f32, d_pool, d_head_w, d_head_b, head_c,
                                     d_head_out);
