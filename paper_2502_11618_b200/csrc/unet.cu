@@ -1165,7 +1165,14 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
             for (int i = t; i < 3 * 128 * 2; i += kEpiThreads) {
                 const int ky = i / 256, r = (i >> 1) & 127, hf = i & 1;
                 int kx = -1, co = r & 31;
-                if (r < 32) kx = hf ? 2 : 1;          // out(2j)   <- [x(2j) | x(2j+1)]
+                if (KX2) {
+                    // one N = 128 tile [spill-left | out(2j) | out(2j+1) | spill-right]
+                    // against the pair [x(2j) | x(2j+1)]
+                    if (r < 32) kx = hf ? -1 : 2;         // -> out(2j-1): x(2j) with W(2)
+                    else if (r < 64) kx = hf ? 2 : 1;     // -> out(2j)
+                    else if (r < 96) kx = hf ? 1 : 0;     // -> out(2j+1)
+                    else kx = hf ? 0 : -1;                // -> out(2j+2): x(2j+1) with W(0)
+                } else if (r < 32) kx = hf ? 2 : 1;   // out(2j)   <- [x(2j) | x(2j+1)]
                 else if (r < 64) kx = hf ? 1 : 0;     // out(2j+1) <- [x(2j) | x(2j+1)]
                 else if (r < 96) kx = hf ? 0 : -1;    // out(2j)   <- x(2j-1) (element 1)
                 else kx = hf ? -1 : 2;                // out(2j+1) <- x(2j+2) (element 0)
@@ -1263,7 +1270,18 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                     const uint32_t a_lo =
                         alo + ((sbase + C::kRingPad + (uint32_t)s * p.stage_bytes) >> 4);
                     const uint32_t b_lo = blo + ((sbase + btile(q, 0, 0, 0)) >> 4);
-                    if constexpr (KX2) {
+                    if constexpr (C8 && KX2) {
+                        // 8-channel input, spill-column form: ONE N = 128 MMA per ky
+                        // (the pair's 16 channels are one K16 step)
+#pragma unroll
+                        for (int ky = 0; ky < 3; ++ky) {
+                            const uint32_t ar = (uint32_t)(ky * kTW) * kARow / 16;
+                            const uint32_t bt = (uint32_t)ky * 4096 / 16;
+                            mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + ar),
+                                     ((uint64_t)bhi << 32) | (b_lo + bt), idesc_bf16(128, 128),
+                                     ky ? 1u : 0u);
+                        }
+                    } else if constexpr (KX2) {
                         const uint32_t bk =
                             blo + ((sbase + p.off_b + (uint32_t)q * 3 * kT * kBT) >> 4);
 #pragma unroll
@@ -1827,7 +1845,9 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
-    if (pl->chunk == 16) return launch_px2_m<kPlain, true>(pl, st);  // e0c1: plain only
+    if (pl->chunk == 16)  // e0c1: plain only (mt 3: the spill-column form)
+        return pl->mt == 3 ? launch_px2_m<kPlain, true, true>(pl, st)
+                           : launch_px2_m<kPlain, true>(pl, st);
     if (pl->mt == 1 && pl->bn == 64) {  // neighbour-row pairs, 64 output channels
         if (pl->chunk == 128)
             return pl->mode == kPool ? launch_px2_m<kPool, false, false, 64, 64>(pl, st)
@@ -2074,7 +2094,10 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     pl->bn = cout;
     pl->chunk = c8 ? 16 : 2 * c0;  // pair-row channels (128: two 64-channel element boxes)
     pl->kind = 2;
-    pl->mt = kx2 && !c8 ? 3 : 1;  // 3 marks the KX2 variant
+    // 3 marks the KX2 (spill-column) variant; the 8-channel layer stays on the
+    // neighbour-row form unless LS_CONV_C8KX2=1 (one N = 128 MMA per ky instead of
+    // three, but the spill-column epilogue: e0c1 47 -> 52 us, measured slower)
+    pl->mt = (kx2 && !c8) || (c8 && env_int("LS_CONV_C8KX2", 0) == 1) ? 3 : 1;
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
     const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;

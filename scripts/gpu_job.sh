@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_unet.py tests/test_gpu_configs.py -x -q -k "not c4 and not c5" 2>&1 | tail -1
-for r in 1 2; do echo "by-input $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "kx2 $(LS_CONV_PX64=0 timeout 120 python scripts/time_unet.py | tail -1)"; done
+timeout 900 python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -1
+for r in 1 2; do echo "c8kx2 $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "c8nbr $(LS_CONV_C8KX2=0 timeout 120 python scripts/time_unet.py | tail -1)"; done
+M=gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,sm__cycles_active.avg,smsp__cycles_active.avg
+N=1 timeout 300 ncu --metrics $M --clock-control none -k regex:k_conv -c 2 --csv python scripts/time_unet.py > gpurun_out/m_c8kx2.csv 2>/dev/null
