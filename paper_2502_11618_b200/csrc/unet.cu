@@ -587,11 +587,19 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
 #pragma unroll
                     for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
                     if (MODE == kTransposed && p.stage_store) {
-                        // staging tile row (2*ty + dy)*16 + tx, 128 B per row holding
-                        // [dx][32 channels]; 16 B chunks XOR-swizzled by row (TMA 128 B)
-                        const int dd = n >> 5, dy = dd >> 1, dx = dd & 1;
-                        const int r = (2 * ty + dy) * kTW + tx;
-                        const int c = dx * 4 + ((n & 31) >> 3);
+                        // cout 32: staging tile row (2*ty + dy)*16 + tx, 128 B per row
+                        // holding [dx][32 channels]; cout 64 (the item covers one dy =
+                        // its n-tile): row (ty*16 + tx)*2 + dx holding 64 channels.
+                        // 16 B chunks XOR-swizzled by row (TMA 128 B)
+                        int r, c;
+                        if (p.cout == 64) {
+                            r = (ty * kTW + tx) * 2 + ((n >> 6) & 1);
+                            c = (n & 63) >> 3;
+                        } else {
+                            const int dd = n >> 5, dy = dd >> 1, dx = dd & 1;
+                            r = (2 * ty + dy) * kTW + tx;
+                            c = dx * 4 + ((n & 31) >> 3);
+                        }
                         uint8_t *row = smem + p.off_stage + (uint32_t)eg * 32768u + r * 128;
                         *reinterpret_cast<uint4 *>(row + ((c ^ (r & 7)) << 4)) =
                             make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -747,8 +755,12 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 named_bar_sync(1 + eg, 128);
                 if (quarter == 0 && lane == 0) {
-                    tma_store_5d(&mY, smem + p.off_stage + (uint32_t)eg * 32768u, 0, ip.x0, 0,
-                                 ip.y0, ip.img);
+                    if (p.cout == 64)  // [c][dx][j][dy][image * h_in + i], dy = n-tile
+                        tma_store_5d(&mY, smem + p.off_stage + (uint32_t)eg * 32768u, 0, 0, ip.x0,
+                                     ip.nt, ip.img * p.h + ip.y0);
+                    else
+                        tma_store_5d(&mY, smem + p.off_stage + (uint32_t)eg * 32768u, 0, ip.x0, 0,
+                                     ip.y0, ip.img);
                     tma_store_wait_read();
                 }
                 named_bar_sync(1 + eg, 128);
@@ -1671,6 +1683,22 @@ static bool encode_up_store(CUtensorMap *map, void *base, int w_in, int h_in, in
               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output of a transposed conv with 64 channels as [c][dx][j][dy][image*h_in + i]
+// (output pixel (2i+dy, 2j+dx)), box {64, 2, 16, 1, 8}: one 8x16-input-pixel
+// item's output rows of one parity dy (= its 128-column n-tile), 128 B swizzle.
+static bool encode_up_store64(CUtensorMap *map, void *base, int w_in, int h_in, int batch) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t row = (cuuint64_t)2 * w_in * 128;  // one output row, bytes
+    cuuint64_t dims[5] = {64, 2, (cuuint64_t)w_in, 2, (cuuint64_t)batch * h_in};
+    cuuint64_t strides[4] = {128, 256, row, 2 * row};
+    cuuint32_t box[5] = {64, 2, (cuuint32_t)kTW, 1, (cuuint32_t)kTH};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace unet
 }  // namespace ls
 
@@ -2341,7 +2369,10 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     int stages = 0;
     // staged TMA stores for 32-channel transposed convs (LS_CONV_UPSTORE=0: off)
     const char *ue = getenv("LS_CONV_UPSTORE");
-    const bool want_stage = transposed && cout == 32 && d_y && !d_y_f32 && !(ue && ue[0] == '0');
+    // (cout 64: the staged box spans the image boundary when rows are ragged, so
+    // batches need h % 8 == 0)
+    const bool want_stage = transposed && d_y && !d_y_f32 && !(ue && ue[0] == '0') &&
+                            (cout == 32 || (cout == 64 && (batch == 1 || h % kTH == 0)));
     // Fit >= 3 pipeline stages: first try whole-chunk stages (all kx boxes in
     // one stage), then one kx per stage, then a narrower K chunk, then a
     // narrower column tile.
@@ -2408,7 +2439,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     pl->chunk = chunk;
     pl->pair = pair ? 1 : 0;
     pl->mode = transposed ? kTransposed : (d_head_w ? kHead : (d_pool ? kPool : kPlain));
-    if (p.stage_store && !encode_up_store(&pl->y, d_y, w, h, batch)) {
+    if (p.stage_store && !(cout == 64 ? encode_up_store64(&pl->y, d_y, w, h, batch)
+                                      : encode_up_store(&pl->y, d_y, w, h, batch))) {
         delete pl;
         return fail(LS_EINVAL);
     }

@@ -52,16 +52,16 @@ def conv_case(c0, c1, cout, h, w, act, pool=False, head=False, batch=1, seed=0):
     return out
 
 
-def convT_case(cin, cout, h, w, seed=0):
+def convT_case(cin, cout, h, w, seed=0, batch=1):
     g = torch.Generator(device="cpu").manual_seed(seed)
-    x = torch.randn(1, h, w, cin, generator=g).to(dev, torch.bfloat16)
+    x = torch.randn(batch, h, w, cin, generator=g).to(dev, torch.bfloat16)
     k = (torch.randn(2, 2, cout, cin, generator=g) * (2.0 / (4 * cin)) ** 0.5)
     wt = k.reshape(4 * cout, cin).to(dev, torch.bfloat16)
     b = torch.randn(cout, generator=g) * 0.1
     shift = b.repeat(4).to(dev)
     scale = torch.ones(4 * cout, device=dev)
-    y = torch.empty(1, 2 * h, 2 * w, cout, dtype=torch.bfloat16, device=dev)
-    rc = lib.ls_conv_transpose2x2(x.data_ptr(), cin, 1, h, w, wt.data_ptr(), cout,
+    y = torch.empty(batch, 2 * h, 2 * w, cout, dtype=torch.bfloat16, device=dev)
+    rc = lib.ls_conv_transpose2x2(x.data_ptr(), cin, batch, h, w, wt.data_ptr(), cout,
                                   scale.data_ptr(), shift.data_ptr(), y.data_ptr(), 0)
     torch.cuda.synchronize()
     assert rc == 0, rc

@@ -73,7 +73,12 @@ def test_conv_layer_vs_torch(case):
         assert out["head_err"] <= 1e-5
 
 
-@pytest.mark.parametrize("shape", [(512, 256, 8, 16), (64, 32, 32, 64), (128, 64, 16, 40)])
+# (cin, cout, h, w[, batch]): 32- and 64-channel outputs take the staged TMA
+# store (64: one output-row parity per n-tile), ragged rows, batches (64 with
+# ragged rows and batch > 1: lane stores)
+@pytest.mark.parametrize("shape", [(512, 256, 8, 16), (64, 32, 32, 64), (128, 64, 16, 40),
+                                   (128, 64, 13, 40), (128, 64, 16, 24, 2), (128, 64, 13, 24, 2),
+                                   (64, 32, 13, 24, 2)])
 def test_conv_transpose_vs_torch(shape):
     import os
     import sys
@@ -81,7 +86,7 @@ def test_conv_transpose_vs_torch(shape):
     sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "scripts"))
     from check_conv import convT_case
 
-    out = convT_case(*shape)
+    out = convT_case(*shape[:4], batch=shape[4] if len(shape) > 4 else 1)
     assert out["bf16_err"] <= 2 ** -7 * max(out["ref_max"], 1.0)
 
 
