@@ -83,6 +83,7 @@ struct ConvParamsP {
     int tiles_x, tiles_y, n_tiles_m, n_tiles_n, n_items;
     int ty0;                // first tile row of a row band (ls_conv_plan_set_rows)
     int reverse;            // walk the tiles bottom-right first (ls_conv_plan_set_reverse)
+    int pair_h;             // CTA pairs side by side (16-column offset) instead of stacked
     int c0, c1, ctot, nq0, nq;
     int kxs, kxps, pad;     // kx taps, kx taps per pipeline stage (1 or kxs)
     int n_total, cout, act;
@@ -284,12 +285,12 @@ struct ItemWalk {
     __device__ int TX(const ConvParamsP &p) const { return p.reverse ? p.tiles_x - 1 - tx : tx; }
     __device__ int TY(const ConvParamsP &p) const { return p.reverse ? p.tiles_y - 1 - ty : ty; }
     __device__ int IMG(const ConvParamsP &p) const { return p.reverse ? p.batch - 1 - img : img; }
-    __device__ ItemPos pos(const ConvParamsP &p, int tile_h) const {
+    __device__ ItemPos pos(const ConvParamsP &p, int tile_h, int tile_w = kTW) const {
         ItemPos ip;
         ip.nt = nt;
         ip.img = IMG(p);
         ip.y0 = (p.ty0 + TY(p)) * tile_h;
-        ip.x0 = TX(p) * kTW;
+        ip.x0 = TX(p) * tile_w;
         return ip;
     }
 };
@@ -314,7 +315,10 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
     } else {
     constexpr int KYS = MODE == kTransposed ? 1 : 3;
     constexpr int MT = C::kMT;
-    constexpr int kTileH = kTH * MT * (PAIR ? 2 : 1);  // rows per work item (both CTAs)
+    // rows / columns per work item (both CTAs of a pair: stacked rows, or side by
+    // side columns when p.pair_h)
+    const int kTileH = kTH * MT * (PAIR && !p.pair_h ? 2 : 1);
+    const int kTileW = kTW * (PAIR && p.pair_h ? 2 : 1);
     constexpr int kBNL = PAIR ? BN / 2 : BN;            // B columns held by this CTA
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
@@ -416,9 +420,11 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
             uint32_t ph = 0;
             ItemWalk walk;
             walk.init(p, wid, wstride);
-            const int ry = (int)rank * kTH * MT;  // this CTA's first row in the item
+            // this CTA's first row / column in the item
+            const int ry = PAIR && !p.pair_h ? (int)rank * kTH * MT : 0;
+            const int rx = PAIR && p.pair_h ? (int)rank * kTW : 0;
             for (int item = wid; item < p.n_items; item += wstride, walk.next(p)) {
-                const ItemPos ip = walk.pos(p, kTileH);
+                const ItemPos ip = walk.pos(p, kTileH, kTileW);
                 for (int q = 0; q < p.nq; ++q) {
                     const bool second = q >= p.nq0;
                     const int c = (second ? q - p.nq0 : q) * CHUNK;
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
                             const int kx = kg * p.kxps + k;
                             if constexpr (PAIR) {
                                 const uint32_t cb = c_full + 8u * (uint32_t)s;
-                                tma_load_4d_pair(st + k * p.a_bytes, ma, c, ip.x0 + kx - p.pad,
+                                tma_load_4d_pair(st + k * p.a_bytes, ma, c, ip.x0 + rx + kx - p.pad,
                                                  ip.y0 + ry - p.pad, ip.img, cb);
                                 if (load_b)
                                     tma_load_3d_pair(st + p.kxps * p.a_bytes + k * p.b_blk, &mB,
@@ -538,15 +544,16 @@ __global__ void __launch_bounds__(threads_for<BN, CHUNK, MT_>()) k_conv_p(
         uint32_t acc = (uint32_t)eg_item;
         ItemWalk walk;
         walk.init(p, wid + eg_item * wstride, kItemGroups * wstride);
-        const int ry = (int)rank * kTH * MT;  // this CTA's first row in the item
+        const int ry = PAIR && !p.pair_h ? (int)rank * kTH * MT : 0;  // this CTA's first
+        const int rx = PAIR && p.pair_h ? (int)rank * kTW : 0;          // row / column
         for (int item = wid + eg_item * wstride; item < p.n_items;
              item += kItemGroups * wstride, acc += kItemGroups, walk.next(p)) {
-            const ItemPos ip = walk.pos(p, kTileH);
+            const ItemPos ip = walk.pos(p, kTileH, kTileW);
             const uint32_t ab = acc % C::kAcc, aph = (acc / C::kAcc) & 1u;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             const uint32_t tbase = tmem + ab * C::kItemCols + ((uint32_t)(quarter * 32) << 16);
-            const int gx = ip.x0 + tx;
+            const int gx = ip.x0 + rx + tx;
             // 32-column groups of this item that hold real columns (n_total may
             // end mid-tile, or be 16 mod 32)
             const int rem = p.n_total - ip.nt * BN;
@@ -1985,11 +1992,25 @@ static int mt_for(int bn, int h, int w, int batch, int n_tiles_n, bool transpose
 // single-CTA sub-tile (profiles/README.md, "CTA pairs"), so pair when
 // waves(pairs) <= 1.3 x waves(single) x sub-tiles per single item.  The
 // 1/16-resolution bottleneck (68 rows: 4.25 pair tiles) stays single.
+// Pair tiles: 16 x 16 pixels (the two CTAs' 8-row tiles stacked) or 8 x 32 (side
+// by side); the orientation with fewer items wins (the 1/16-resolution
+// bottleneck, 68 x 120: 40 stacked vs 36 side-by-side tiles).
+static long long pair_items(int h, int w, int batch, int n_tiles_n, bool side) {
+    const long long tx = side ? (w + 2 * kTW - 1) / (2 * kTW) : (w + kTW - 1) / kTW;
+    const long long ty = side ? (h + kTH - 1) / kTH : (h + 2 * kTH - 1) / (2 * kTH);
+    return tx * ty * batch * n_tiles_n;
+}
+static bool pair_side(int h, int w, int batch, int n_tiles_n) {
+    const int e = env_int("LS_CONV_PAIR_SIDE", 2);  // A/B: 0 stacked, 1 side by side
+    if (e != 2) return e == 1;
+    return pair_items(h, w, batch, n_tiles_n, true) < pair_items(h, w, batch, n_tiles_n, false);
+}
+
 static bool pair_pays(int bn, int h, int w, int batch, int n_tiles_n) {
     if (pair_mode() == 2) return true;
     const int n_sm = current_sm_count();
     const long long tx = (w + kTW - 1) / kTW;
-    const long long items_p = tx * ((h + 2 * kTH - 1) / (2 * kTH)) * batch * n_tiles_n;
+    const long long items_p = pair_items(h, w, batch, n_tiles_n, pair_side(h, w, batch, n_tiles_n));
     const long long waves_p = (items_p + n_sm / 2 - 1) / (n_sm / 2);
     const int mt = mt_for(bn, h, w, batch, n_tiles_n, false);
     const long long items_s = tx * ((h + kTH * mt - 1) / (kTH * mt)) * batch * n_tiles_n;
@@ -2386,9 +2407,11 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         mt = pair ? (bn == 128 ? env_int("LS_CONV_PAIR_MT", 1) == 2 ? 2 : 1 : 1)
                   : mt_for(bn, h, w, batch, (n_total + bn - 1) / bn, transposed != 0);
         const int box_h = kTH * mt + 2 * p.pad;
-        const int tile_h = kTH * mt * (pair ? 2 : 1);
+        p.pair_h = pair && pair_side(h, w, batch, (n_total + bn - 1) / bn) ? 1 : 0;
+        const int tile_h = kTH * mt * (pair && !p.pair_h ? 2 : 1);
+        const int tile_w = kTW * (p.pair_h ? 2 : 1);
         const uint32_t row = (uint32_t)chunk * 2;
-        p.tiles_x = (w + kTW - 1) / kTW;
+        p.tiles_x = (w + tile_w - 1) / tile_w;
         p.tiles_y = (h + tile_h - 1) / tile_h;
         p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
         p.n_tiles_n = (n_total + bn - 1) / bn;
@@ -2504,7 +2527,7 @@ int ls_conv_plan_set_reverse(ls_conv_plan *pl, int32_t reverse) {
 
 int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) {
     if (!pl) return LS_EINVAL;
-    const int th = pl->kind == 0 ? kTH * pl->mt * (pl->pair ? 2 : 1) : kTH;  // rows per tile
+    const int th = pl->kind == 0 ? kTH * pl->mt * (pl->pair && !pl->p.pair_h ? 2 : 1) : kTH;
     const int h = pl->p.h;
     if (row_begin < 0 || row_end > h || row_begin >= row_end || row_begin % th) return LS_EINVAL;
     const int t0 = row_begin / th, t1 = (row_end + th - 1) / th;
@@ -2521,7 +2544,7 @@ int ls_conv_plan_set_rows(ls_conv_plan *pl, int32_t row_begin, int32_t row_end) 
 
 int32_t ls_conv_plan_tile_rows(const ls_conv_plan *pl) {
     if (!pl) return LS_EINVAL;
-    return pl->kind == 0 ? kTH * pl->mt * (pl->pair ? 2 : 1) : kTH;
+    return pl->kind == 0 ? kTH * pl->mt * (pl->pair && !pl->p.pair_h ? 2 : 1) : kTH;
 }
 
 int ls_conv2d(const uint16_t *d_x0, int32_t c0, const uint16_t *d_x1, int32_t c1, int32_t batch,
