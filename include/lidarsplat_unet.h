@@ -64,6 +64,20 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
                                   int32_t head_c, float *d_head_out, int32_t *status);
 int ls_conv_plan_launch(const ls_conv_plan *plan, void *stream);
 
+/* dec0_up fused into dec0_conv1 (unet.ts:170-181: upsample -> concat [up, skip]
+ * -> conv 3x3): y = act(scale * conv3x3([up, skip]) + shift) with
+ * up = convTranspose2x2(x) + up_shift computed per tile on the tensor core and
+ * never stored.  x: [batch][h/2][w/2][64] bf16; up_w: [4*32][64] (row
+ * (dy*2 + dx)*32 + o, as ls_conv_plan_create's transposed layout); up_shift:
+ * 32 (the bias; scale 1, no activation); skip: [batch][h][w][32]; w: the 3x3
+ * weights [tap][32][64] over [up, skip]; y: [batch][h][w][32].  h, w even.
+ * Results equal the unfused pair of plans bit for bit. */
+ls_conv_plan *ls_conv_plan_create_upfused(const uint16_t *d_x, const uint16_t *d_up_w,
+                                          const float *d_up_shift, const uint16_t *d_skip,
+                                          int32_t batch, int32_t h, int32_t w, const uint16_t *d_w,
+                                          const float *d_scale, const float *d_shift, int32_t act,
+                                          float alpha, uint16_t *d_y, int32_t *status);
+
 /* Visit the plan's output tiles in reverse order (last tile first).  Plans of
  * consecutive layers alternating direction consume their producer's most
  * recently written -- still L2-resident -- rows first.  Results unchanged. */

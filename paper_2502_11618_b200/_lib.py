@@ -126,6 +126,8 @@ SIGNATURES = {
     "ls_conv_plan_destroy": (None, [_P]),
     "ls_conv_plan_set_rows": (ctypes.c_int, [_P, _I32, _I32]),
     "ls_conv_plan_set_reverse": (ctypes.c_int, [_P, _I32]),
+    "ls_conv_plan_create_upfused": (_P, [_P, _P, _P, _P, _I32, _I32, _I32, _P, _P, _P, _I32,
+                                         ctypes.c_float, _P, _P]),
     "ls_conv_plan_tile_rows": (_I32, [_P]),
     "ls_conv2d": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _P,
                                  _I32, _F, _P, _P, _P, _P, _P, _I32, _P, _P]),

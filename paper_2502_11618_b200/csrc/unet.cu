@@ -101,6 +101,7 @@ struct ConvParamsP {
     // of shared-memory loads, which competed with the MMA operand reads in L1
     float pc_scale[64], pc_shift[64];
     float pc_head[4 * 32];  // k_conv_px2 head: the final 1x1 conv's weights [head_c][32]
+    float pc_upb[32];       // k_conv_upfuse: the fused transposed conv's bias
     int resident;           // weights resident in smem
     int stages;
     uint32_t a_bytes;       // one A box footprint (1024-aligned)
@@ -1604,6 +1605,352 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
 }
 
+// ---------------------------------------------------------------------------
+// dec0_up fused into dec0_conv1 (FE:model/unet.ts:170-181: upsample, concat
+// [up, skip], conv1).  Per item the 2x2 transposed conv of the half-resolution
+// dec1 output runs on the tensor core (M = 128 half-resolution pixels of an
+// 8-row x 16-column box, N = 128 = (dy, dx, co), K = 64), and a transform
+// warpgroup adds its bias, rounds to bf16 -- the values the unfused up tensor
+// would hold -- and writes them pixel-shuffled straight into the KX2 A operand
+// of source 0 (10 rows x 16 pairs x 128 B, 128 B swizzle), zero outside the
+// image (the conv's "same" padding of the up tensor).  The 134 MB up tensor is
+// neither written nor read.  Source 1 (skip) and the epilogue are the KX2
+// form's; per item the MMA thread issues skip's MMAs, then the next item's up
+// MMAs, then source 0's, so the transform overlaps tensor work.
+// Ring order per item: [dec1 box, skip box]; TMEM columns 0..383 hold three
+// 128-column KX2 accumulators, 384..511 the up accumulator.
+constexpr int kUpGroups = 3;
+constexpr uint32_t kUpBox = 10u * 16u * 128u;  // source-0 A box (20 KB)
+
+__global__ void __launch_bounds__(64 + 128 * (kUpGroups + 1)) k_conv_upfuse(
+    const __grid_constant__ CUtensorMap mD1, const __grid_constant__ CUtensorMap mSkip,
+    const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mU,
+    const ConvParamsP p) {
+    using C = CfgPx;
+    constexpr int kN = 128, kAcc = 3, kGroups = kUpGroups;
+    constexpr uint32_t kUpCol = 384;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const uint32_t sbase = smem_u32(smem);
+    const int S = p.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + p.off_bar);
+    uint64_t *empty = full + S;
+    uint64_t *tfull = empty + S;
+    uint64_t *tempty = tfull + kAcc;
+    uint64_t *bres = tempty + kAcc;
+    uint64_t *upready = bres + 1, *upfree = upready + 1;
+    uint64_t *a0ready = upfree + 1, *a0free = a0ready + 2;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(a0free + 2);
+    uint8_t *abox = smem + p.off_stage;  // two source-0 A boxes
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int s = 0; s < S; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, 1);
+            }
+            for (int a = 0; a < kAcc; ++a) {
+                mbar_init(tfull + a, 1);
+                mbar_init(tempty + a, 4);
+            }
+            mbar_init(bres, 1);
+            mbar_init(upready, 1);
+            mbar_init(upfree, 4);
+            for (int k = 0; k < 2; ++k) {
+                mbar_init(a0ready + k, 4);
+                mbar_init(a0free + k, 1);
+            }
+            fence_barrier_init();
+            tma_prefetch(&mD1);
+            tma_prefetch(&mSkip);
+            tma_prefetch(&mB);
+            tma_prefetch(&mU);
+        }
+        __syncwarp();
+        tmem_alloc(tslot, C::kTmemCols);
+    }
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            // ------------------------------ TMA producer ------------------------------
+            // resident: d0c1 KX2 tiles (src, ky, t) [W(2) ; W(1) ; W(0)] and the
+            // up weights [(dy, dx, co) = 128 rows][64 channels]
+            mbar_expect_tx(bres, 12u * 3072u + 16384u);
+            for (int src = 0; src < 2; ++src)
+                for (int ky = 0; ky < 3; ++ky)
+                    for (int t = 0; t < 2; ++t)
+                        for (int r = 0; r < 3; ++r)
+                            tma_load_3d(smem + p.off_b + ((src * 3 + ky) * 2 + t) * 3072 + r * 1024,
+                                        &mB, src * 32 + 16 * t, 0, (2 - r) * 3 + ky, bres);
+            tma_load_3d(smem + p.off_b + 12 * 3072, &mU, 0, 0, 0, bres);
+            LS_GDC_WAIT();
+            int s = 0;
+            uint32_t ph = 0;
+            ItemWalk walk;
+            walk.init(p, blockIdx.x, gridDim.x);
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p)) {
+                const int img = walk.IMG(p), px0 = walk.TX(p) * kPxCols - 1,
+                          y0 = (p.ty0 + walk.TY(p)) * kTH;
+                // dec1 rows y0/2 - 1 .. y0/2 + 6 (the up rows y0 - 1 .. y0 + 8 come
+                // from y0/2 - 1 .. y0/2 + 4), columns px0 .. px0 + 15
+                mbar_wait(empty + s, ph ^ 1u);
+                mbar_expect_tx(full + s, 16384u);
+                tma_load_4d(smem + C::kRingPad + (size_t)s * p.stage_bytes, &mD1, 0, px0, y0 / 2 - 1,
+                            img, full + s);
+                s = s + 1 == S ? 0 : s + 1;
+                ph ^= s == 0;
+                mbar_wait(empty + s, ph ^ 1u);
+                mbar_expect_tx(full + s, p.a_tx);
+                tma_load_4d(smem + C::kRingPad + (size_t)s * p.stage_bytes, &mSkip, 0, px0, y0 - 1,
+                            img, full + s);
+                s = s + 1 == S ? 0 : s + 1;
+                ph ^= s == 0;
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            // ------------------------------- MMA issuer -------------------------------
+            const uint32_t id64 = idesc_bf16(128, 64), id32 = idesc_bf16(128, 32);
+            const uint32_t id96 = idesc_bf16(128, 96), id128 = idesc_bf16(128, 128);
+            const uint64_t a128 = smem_desc(0, 128, kSwizzle128B);
+            const uint64_t b32 = smem_desc(0, 32, kSwizzle32B);
+            const uint32_t ahi = (uint32_t)(a128 >> 32), alo = (uint32_t)a128;
+            const uint32_t bhi = (uint32_t)(b32 >> 32), blo = (uint32_t)b32;
+            mbar_wait(bres, 0);
+            // ring slot q of the CTA's sequence: item n's dec1 box is slot 2n, its
+            // skip box slot 2n + 1 (the producer's order); slots are consumed
+            // slightly out of order (the next item's dec1 box before this item's
+            // skip box), so stage and phase come from the slot index
+            auto stage_of = [&](int q) { return q % S; };
+            auto phase_of = [&](int q) { return (uint32_t)(q / S) & 1u; };
+            uint32_t upph = 0;
+            // up MMAs of item n (dec1 box in slot 2n)
+            auto up_mma = [&](int n) {
+                const int st = stage_of(2 * n);
+                mbar_wait(full + st, phase_of(2 * n));
+                fence_after_sync();
+                const uint32_t a_lo = alo + ((sbase + C::kRingPad + (uint32_t)st * p.stage_bytes) >> 4);
+                const uint32_t b_lo = alo + ((sbase + p.off_b + 12u * 3072u) >> 4);
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    mma_bf16(tmem + kUpCol, ((uint64_t)ahi << 32) | (a_lo + 2u * t),
+                             ((uint64_t)ahi << 32) | (b_lo + 2u * t), id128, t ? 1u : 0u);
+                mma_commit(empty + st);
+                mma_commit(upready);
+            };
+            // KX2 MMAs of one source (A at a_lo, B tiles of source src); first:
+            // the accumulator's first K step
+            auto kx2_mma = [&](uint32_t d0, uint32_t a_lo, int src, bool first_src) {
+                const uint32_t bk = blo + ((sbase + p.off_b + (uint32_t)src * 6u * 3072u) >> 4);
+#pragma unroll
+                for (int ky = 0; ky < 3; ++ky) {
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        const uint32_t arow = (uint32_t)(ky * kTW) * 128u;
+                        const uint32_t a_e0 = (arow + 32 * t) / 16, a_e1 = (arow + 64 + 32 * t) / 16;
+                        const uint32_t bt = (uint32_t)((ky * 2 + t) * 3072) / 16;
+                        const bool first = first_src && (ky | t) == 0;
+                        mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + a_e0),
+                                 ((uint64_t)bhi << 32) | (bk + bt), id96, first ? 0u : 1u);
+                        if (first) {
+                            mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                     ((uint64_t)bhi << 32) | (bk + bt), id64, 1u);
+                            mma_bf16(d0 + 96, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                     ((uint64_t)bhi << 32) | (bk + bt + 2048 / 16), id32, 0u);
+                        } else {
+                            mma_bf16(d0 + 32, ((uint64_t)ahi << 32) | (a_lo + a_e1),
+                                     ((uint64_t)bhi << 32) | (bk + bt), id96, 1u);
+                        }
+                    }
+                }
+            };
+            uint32_t ab = 0, aph = 0;
+            int n = 0;
+            if ((int)blockIdx.x < p.n_items) up_mma(0);
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++n,
+                     ab = ab + 1 == kAcc ? 0 : ab + 1, aph ^= ab == 0) {
+                mbar_wait(tempty + ab, aph ^ 1u);
+                fence_after_sync();
+                const uint32_t d0 = tmem + ab * kN;
+                // the next item's up MMAs once the transform has read this item's
+                if (item + (int)gridDim.x < p.n_items) {
+                    mbar_wait(upfree, upph);
+                    upph ^= 1u;
+                    fence_after_sync();
+                    up_mma(n + 1);
+                }
+                // source 0 from the transform's box first (the unfused layer's K
+                // order: [up, skip]), then source 1 (skip) from slot 2n + 1
+                const int k = n & 1;
+                mbar_wait(a0ready + k, (uint32_t)(n >> 1) & 1u);
+                fence_after_sync();
+                kx2_mma(d0, alo + ((sbase + p.off_stage + (uint32_t)k * kUpBox) >> 4), 0, true);
+                mma_commit(a0free + k);
+                const int st = stage_of(2 * n + 1);
+                mbar_wait(full + st, phase_of(2 * n + 1));
+                fence_after_sync();
+                kx2_mma(d0, alo + ((sbase + C::kRingPad + (uint32_t)st * p.stage_bytes) >> 4), 1, false);
+                mma_commit(empty + st);
+                mma_commit(tfull + ab);
+            }
+        }
+    } else if (warp >= 2 + 4 * kGroups) {
+        // ------------------------------ up transform ------------------------------
+        const int quarter = warp & 3;
+        const int l = quarter * 32 + lane;  // dec1 pixel (r, j) of the item's 8 x 16 box
+        const int r = l >> 4, j = l & 15;
+        const int wp = p.w >> 1;
+        uint32_t upph = 0;
+        int n = 0;
+        ItemWalk walk;
+        walk.init(p, blockIdx.x, gridDim.x);
+        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, walk.next(p), ++n) {
+            const int px0 = walk.TX(p) * kPxCols - 1, y0 = (p.ty0 + walk.TY(p)) * kTH;
+            const int k = n & 1;
+            mbar_wait(upready, upph);
+            upph ^= 1u;
+            fence_after_sync();
+            // (dy, dx) blocks of 32 columns; this buffer k was last read by the
+            // MMAs of item n - 2
+            mbar_wait(a0free + k, ((uint32_t)(n >> 1) & 1u) ^ 1u);
+            const uint32_t tb = tmem + kUpCol + ((uint32_t)(quarter * 32) << 16);
+            uint8_t *box = abox + k * kUpBox;
+            const bool colok = px0 + j >= 0 && px0 + j < wp;
+            uint32_t ra[32], rb[32];
+            tmem_ld32_async(tb, ra);
+#pragma unroll
+            for (int dd = 0; dd < 4; ++dd) {
+                uint32_t(&cur)[32] = (dd & 1) ? rb : ra;
+                uint32_t(&nxt)[32] = (dd & 1) ? ra : rb;
+                tmem_ld_wait(cur);
+                if (dd + 1 < 4) {
+                    tmem_ld32_async(tb + 32u * (dd + 1), nxt);
+                } else {
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(upfree);
+                }
+                const int dy = dd >> 1, dx = dd & 1;
+                const int b = 2 * r + dy - 1;  // box row (up row y0 - 1 + b)
+                if (b < 0 || b > 9) continue;
+                const int y = y0 - 1 + b;
+                const bool zero = !colok || y < 0 || y >= p.h;
+                const int row = b * 16 + j;
+                uint8_t *rp = box + row * 128;
+#pragma unroll
+                for (int c8 = 0; c8 < 4; ++c8) {  // 8 channels per 16 B chunk
+                    uint32_t w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int c = c8 * 8 + 2 * q;
+                        const float v0 = zero ? 0.0f : __uint_as_float(cur[c]) + p.pc_upb[c];
+                        const float v1 = zero ? 0.0f : __uint_as_float(cur[c + 1]) + p.pc_upb[c + 1];
+                        w[q] = pack_bf16(v0, v1);
+                    }
+                    const int chunk = dx * 4 + c8;
+                    *reinterpret_cast<uint4 *>(rp + ((chunk ^ (row & 7)) << 4)) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(a0ready + k);
+        }
+    } else {
+        // --------------------------------- epilogue ---------------------------------
+        const int eg = (warp - 2) >> 2;
+        const int quarter = warp & 3;
+        const int m = quarter * 32 + lane;
+        const int tp = m % kTW, ty = m / kTW;
+        const float slope = act_slope(p.act, p.alpha);
+        const f32x2 slope2 = f2(slope, slope);
+        const int wp = p.w >> 1;
+        uint32_t ab = (uint32_t)eg % kAcc, aph = ((uint32_t)eg / kAcc) & 1u;
+        ItemWalk walk;
+        walk.init(p, blockIdx.x + eg * gridDim.x, kGroups * gridDim.x);
+        for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
+             item += kGroups * gridDim.x, walk.next(p)) {
+            const int img = walk.IMG(p), px0 = walk.TX(p) * kPxCols - 1,
+                      y0 = (p.ty0 + walk.TY(p)) * kTH;
+            mbar_wait(tfull + ab, aph);
+            fence_after_sync();
+            const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
+            const int gp = px0 + tp, gy = y0 + ty;
+            const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
+            const int64_t pix0 = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
+            __nv_bfloat16 *const ybase = p.y + pix0 * 32;
+#pragma unroll
+            for (int h2 = 0; h2 < 2; ++h2) {
+                const uint32_t n = 16u * h2;
+                uint32_t sl[16], o0[16], o1[16], sr[16];
+                tmem_ld16_async(tbase + n, sl);
+                tmem_ld16_async(tbase + 32u + n, o0);
+                tmem_ld16_async(tbase + 64u + n, o1);
+                tmem_ld16_async(tbase + 96u + n, sr);
+                tmem_ld_wait4(sl, o0, o1, sr);
+                if (h2 == 1) {
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(tempty + ab);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    float a0, a1, b0, b1;
+                    unf2(add2(f2(__uint_as_float(o0[i]), __uint_as_float(o0[i + 1])),
+                              f2(__shfl_up_sync(0xffffffffu, __uint_as_float(sr[i]), 1),
+                                 __shfl_up_sync(0xffffffffu, __uint_as_float(sr[i + 1]), 1))),
+                         a0, a1);
+                    unf2(add2(f2(__uint_as_float(o1[i]), __uint_as_float(o1[i + 1])),
+                              f2(__shfl_down_sync(0xffffffffu, __uint_as_float(sl[i]), 1),
+                                 __shfl_down_sync(0xffffffffu, __uint_as_float(sl[i + 1]), 1))),
+                         b0, b1);
+                    o0[i] = __float_as_uint(a0);
+                    o0[i + 1] = __float_as_uint(a1);
+                    o1[i] = __float_as_uint(b0);
+                    o1[i + 1] = __float_as_uint(b1);
+                }
+#pragma unroll
+                for (int px = 0; px < 2; ++px) {
+                    const uint32_t(&rr)[16] = px ? o1 : o0;
+                    float v[16];
+#pragma unroll
+                    for (int i4 = 0; i4 < 4; ++i4) {
+                        const float *sc = p.pc_scale + n + 4 * i4;
+                        const float *sh = p.pc_shift + n + 4 * i4;
+                        const f32x2 sc2[2] = {f2(sc[0], sc[1]), f2(sc[2], sc[3])};
+                        const f32x2 sh2[2] = {f2(sh[0], sh[1]), f2(sh[2], sh[3])};
+#pragma unroll
+                        for (int jp = 0; jp < 2; ++jp) {
+                            const int i = 4 * i4 + 2 * jp;
+                            act2(fma2(f2(__uint_as_float(rr[i]), __uint_as_float(rr[i + 1])), sc2[jp],
+                                      sh2[jp]),
+                                 slope2, v[i], v[i + 1]);
+                        }
+                    }
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+                    if (valid) st_global_v8(ybase + px * 32 + n, pk);
+                }
+            }
+#pragma unroll 1
+            for (int kk = 0; kk < kGroups; ++kk) {
+                ab = ab + 1 == kAcc ? 0 : ab + 1;
+                aph ^= ab == 0;
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
+}
+
 // ------------------------------------------------------------------ host ---
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -1877,6 +2224,22 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     cfg.numAttrs = 1;
     return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8, KX2, CO, CI>, pl->a0, pl->a1, pl->b,
                                    pl->p);
+}
+
+static int launch_upfuse(const ls_conv_plan *pl, cudaStream_t st) {
+    static std::atomic<uint64_t> attr_done{0};  // per-device bits (idempotent races)
+    if (int e = smem_optin(k_conv_upfuse, attr_done)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)pl->grid);
+    cfg.blockDim = dim3((unsigned)(64 + 128 * (kUpGroups + 1)));
+    cfg.dynamicSmemBytes = pl->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_upfuse, pl->a0, pl->a1, pl->b, pl->y, pl->p);
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
@@ -2489,6 +2852,7 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
     if (!pl) return LS_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     if (pl->kind == 2) return launch_px2(pl, st);
+    if (pl->kind == 3) return launch_upfuse(pl, st);
     if (pl->pair) {
         if (pl->bn == 128 && pl->chunk == 64) return launch_pair<128, 64>(pl, st);
         if (pl->bn == 128 && pl->chunk == 32) return launch_pair<128, 32>(pl, st);
@@ -2518,6 +2882,95 @@ int ls_conv_plan_launch(const ls_conv_plan *pl, void *stream) {
 }
 
 void ls_conv_plan_destroy(ls_conv_plan *pl) { delete pl; }
+
+ls_conv_plan *ls_conv_plan_create_upfused(const uint16_t *d_x, const uint16_t *d_up_w,
+                                          const float *d_up_shift, const uint16_t *d_skip,
+                                          int32_t batch, int32_t h, int32_t w, const uint16_t *d_w,
+                                          const float *d_scale, const float *d_shift, int32_t act,
+                                          float alpha, uint16_t *d_y, int32_t *status) {
+    using namespace ls::unet;
+    auto fail = [&](int32_t e) -> ls_conv_plan * {
+        if (status) *status = e;
+        return nullptr;
+    };
+    if (!d_x || !d_up_w || !d_up_shift || !d_skip || !d_w || !d_scale || !d_shift || !d_y ||
+        batch < 1 || h < 2 || w < 2 || (h % 2) || (w % 2) || (act != LS_ACT_NONE && act != LS_ACT_RELU &&
+                                                        act != LS_ACT_LEAKY))
+        return fail(LS_EINVAL);
+    ls_conv_plan *pl = new (std::nothrow) ls_conv_plan();
+    if (!pl) return fail(LS_EINVAL);
+    ConvParamsP &p = pl->p;
+    p = ConvParamsP{};
+    p.batch = batch;
+    p.h = h;
+    p.w = w;
+    p.c0 = 32;
+    p.c1 = 32;
+    p.ctot = 64;
+    p.nq0 = 1;
+    p.nq = 2;
+    p.kxs = 3;
+    p.kxps = 1;
+    p.pad = 1;
+    p.n_total = 32;
+    p.cout = 32;
+    p.act = act;
+    p.alpha = alpha;
+    p.scale = d_scale;
+    p.shift = d_shift;
+    p.y = reinterpret_cast<__nv_bfloat16 *>(d_y);
+    if (cudaMemcpy(p.pc_scale, d_scale, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(p.pc_shift, d_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(p.pc_upb, d_up_shift, 32 * sizeof(float), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        delete pl;
+        return fail(LS_EINVAL);
+    }
+    p.tiles_x = (w / 2 + kPxCols - 1) / kPxCols;
+    p.tiles_y = (h + kTH - 1) / kTH;
+    p.n_tiles_m = p.tiles_x * p.tiles_y * batch;
+    p.n_tiles_n = 1;
+    p.n_items = p.n_tiles_m;
+    p.a_tx = kUpBox;  // the skip box; the dec1 box is 16 KB
+    p.a_bytes = kUpBox;
+    p.stage_bytes = kUpBox;
+    p.resident = 1;
+    const size_t res_bytes = 12 * 3072 + 16384;  // KX2 tiles of both sources + up weights
+    const size_t boxes = 2 * (size_t)kUpBox;     // the transform's two source-0 boxes
+    const size_t fixed = CfgPx::kRingPad + boxes + res_bytes + 512;
+    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.stage_bytes) : 0;
+    stages &= ~1;  // two ring stages per item
+    if (stages < 4) {
+        delete pl;
+        return fail(LS_EINVAL);
+    }
+    if (stages > 8) stages = 8;
+    p.stages = stages;
+    p.off_stage = (uint32_t)(CfgPx::kRingPad + stages * p.stage_bytes);
+    p.off_b = (uint32_t)(p.off_stage + boxes);
+    p.off_const = (uint32_t)(p.off_b + res_bytes);
+    p.off_pool = p.off_const;
+    p.off_bar = p.off_pool;
+    pl->smem = 1024 + p.off_bar + 512;
+    pl->bn = 32;
+    pl->chunk = 64;
+    pl->kind = 3;
+    pl->mt = 1;
+    pl->mode = kPlain;
+    const int n_sm = current_sm_count();
+    pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
+    pl->full_tiles_y = p.tiles_y;
+    // dec1 output [n][h/2][w/2][64] as boxes {64, 16, 8}; skip as pair pixels
+    bool ok = encode_act(&pl->a0, d_x, 64, w / 2, h / 2, batch, 64, 8);
+    ok = ok && encode_act(&pl->a1, d_skip, 64, w / 2, h, batch, 64, kTH + 2);
+    ok = ok && encode_wts(&pl->b, d_w, 64, 32, 9, 16, 32, 1);
+    ok = ok && encode_wts(&pl->y, d_up_w, 64, 128, 1, 64, 128, 1);
+    if (!ok) {
+        delete pl;
+        return fail(LS_EINVAL);
+    }
+    if (status) *status = 0;
+    return pl;
+}
 
 int ls_conv_plan_set_reverse(ls_conv_plan *pl, int32_t reverse) {
     if (!pl) return LS_EINVAL;

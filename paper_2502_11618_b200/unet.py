@@ -280,13 +280,17 @@ class UNet:
 
     @property
     def launches(self) -> int:
-        return 5 * self.cfg.depth + 2  # unbanded; see launches_for(h, w, batch)
+        # unbanded; see launches_for(h, w, batch).  dec0_up runs inside dec0_conv1
+        # (_upfuse) unless LS_UNET_UPFUSE=0
+        return 5 * self.cfg.depth + 2 - (1 if _upfuse(1) else 0)
 
     def launches_for(self, h: int, w: int, batch: int = 1) -> int:
         """Conv launches of one forward at this size (full-resolution row bands
         multiply the 5 full-resolution layers' launches)."""
         nb = _full_res_bands(batch, h, w)
-        return 5 * self.cfg.depth + 2 + (5 * (nb - 1) if nb > 1 else 0)
+        if nb > 1:
+            return 5 * self.cfg.depth + 2 + 5 * (nb - 1)
+        return 5 * self.cfg.depth + 2 - (1 if _upfuse(nb) else 0)
 
     def flops(self, width: int, height: int) -> float:
         return unet_flops(self.cfg, width, height)
@@ -460,9 +464,24 @@ class UNet:
                     mk(B[("d1", 0)], c, None, 0, hs, ws, L["dec0_conv2"], 2,
                        head=(fc["w"], fc["b"], cfg.outChannels, out), rows=(b0, b1))
                 continue
-            mk(cur, ccur, None, 0, hs // 2, ws // 2, L[f"dec{s}_up"], 0, y=B[("up", s)],
-               transposed=True)
-            mk(B[("up", s)], c, B[("skip", s)], c, hs, ws, L[f"dec{s}_conv1"], 2, y=B[("d1", s)])
+            if s == 0 and _upfuse(nb) and c == 32 and ccur == 64:
+                # dec0_up computed per tile inside dec0_conv1 (the up tensor is
+                # never materialised; results identical)
+                st = ctypes.c_int32(0)
+                lu, l1 = L["dec0_up"], L["dec0_conv1"]
+                pl = lib.ls_conv_plan_create_upfused(
+                    cur.data_ptr(), lu["w"].data_ptr(), lu["shift"].data_ptr(),
+                    B[("skip", 0)].data_ptr(), batch, hs, ws, l1["w"].data_ptr(),
+                    l1["scale"].data_ptr(), l1["shift"].data_ptr(), 2, DECODER_LEAK,
+                    B[("d1", 0)].data_ptr(), ctypes.byref(st))
+                if not pl:
+                    raise RuntimeError(f"fused up/conv plan failed ({st.value})")
+                plans.append(pl)
+            else:
+                mk(cur, ccur, None, 0, hs // 2, ws // 2, L[f"dec{s}_up"], 0, y=B[("up", s)],
+                   transposed=True)
+                mk(B[("up", s)], c, B[("skip", s)], c, hs, ws, L[f"dec{s}_conv1"], 2,
+                   y=B[("d1", s)])
             if s > 0:
                 mk(B[("d1", s)], c, None, 0, hs, ws, L[f"dec{s}_conv2"], 2, y=B[("d2", s)])
             else:
@@ -486,6 +505,12 @@ class UNet:
 
 
 import ctypes  # noqa: E402  (used by the plan helpers above)
+
+
+def _upfuse(nb: int) -> bool:
+    """dec0_up fused into dec0_conv1 (LS_UNET_UPFUSE=0: two launches; row
+    bands keep the unfused pair)."""
+    return nb == 1 and os.environ.get("LS_UNET_UPFUSE", "1") != "0"
 
 
 def _full_res_bands(batch: int, h: int, w: int) -> int:

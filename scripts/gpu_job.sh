@@ -1,9 +1,4 @@
-# round-2 final checkpoint: GPU suite, smoke, bench x2 (100M, driver flags), 20M, C1, reference arm, launch list
-python -m pytest tests -m gpu -q > gpurun_out/r02_gpu_suite9.log 2>&1; tail -2 gpurun_out/r02_gpu_suite9.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-for i in 1 2; do python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02_bench_100m_v8_$i.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_100m_v8_$i.json').read().strip().splitlines()[-1]); print('100M', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), round(d['roofline']['frac'],3), round(d['roofline']['other']['frac'],3), d['parity']['bit_exact'], d['parity'].get('unet_max_abs'), d['clocks']['sm_mhz'], d['clocks']['reasons'], {k: round(v*1e3,1) for k,v in d['stages_ms'].items()})"; done
-python bench.py --steps 20 --warmup 5 --points 20000000 --no-cpu-baseline > gpurun_out/r02_bench_20m_v8.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_20m_v8.json').read().strip().splitlines()[-1]); print('20M', round(d['value'],1), round(d['e2e']['value'],1))"
-python bench.py --steps 200 --warmup 10 --points 1000000 --width 512 --height 512 --unet reduced > gpurun_out/r02_bench_c1_v8.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_c1_v8.json').read().strip().splitlines()[-1]); print('C1', round(d['value'],1), round(d['e2e']['value'],1))"
-python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02_ref_v8.json 2>/dev/null; tail -c 250 gpurun_out/r02_ref_v8.json
-for r in 1 2; do timeout 120 python scripts/time_unet.py | tail -1; done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_bench_launches_v8.csv -k "regex:k_|radix" python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1; echo launches $?
+timeout 900 python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -2
+for r in 1 2; do echo "fused $(timeout 120 python scripts/time_unet.py | tail -1)"; echo "unfused $(LS_UNET_UPFUSE=0 timeout 120 python scripts/time_unet.py | tail -1)"; done
+M=gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,lts__t_bytes.sum,sm__cycles_active.avg,smsp__cycles_active.avg
+N=1 timeout 300 ncu --metrics $M --clock-control none -k regex:k_conv -c 21 --csv python scripts/time_unet.py > gpurun_out/m_upfuse.csv 2>/dev/null

@@ -248,7 +248,7 @@ def test_full_res_row_bands_identical(monkeypatch):
     monkeypatch.setenv("LS_UNET_BANDS", "4")
     net = UNet.from_config("default", seed=6)
     b = _run_device(net, x, 8)
-    assert net.launches_for(256, 160) == net.launches + 15
+    assert net.launches_for(256, 160) == 5 * net.cfg.depth + 2 + 15  # bands keep dec0_up apart
     assert np.array_equal(a, b)
 
 
@@ -308,3 +308,25 @@ def test_cta_pairs_bit_identical(tmp_path):
         outs.append(np.load(f))
     assert outs[0].shape == (1, 256, 480, 3)
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_fused_up_conv_bit_identical(tmp_path):
+    """dec0_up computed per tile inside dec0_conv1 (ls_conv_plan_create_upfused:
+    the up tensor never stored) equals the two-plan path bit for bit -- the
+    transposed conv's MMA, bias and bf16 rounding are the same operations, the
+    zero padding of the up tensor is written explicitly.  Sizes with ragged
+    pair tiles (240 / 2 = 120 pairs = 8.6 tiles) and the bench's own."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for h, w in ((128, 240), (1088, 1920)):
+        outs = []
+        for mode in ("0", "1"):
+            f = tmp_path / f"o{mode}_{h}.npy"
+            env = dict(os.environ, LS_UNET_UPFUSE=mode, H=str(h), W=str(w))
+            subprocess.run([sys.executable, os.path.join(root, "scripts", "unet_out.py"), str(f)],
+                           env=env, check=True, timeout=300)
+            outs.append(np.load(f))
+        assert np.array_equal(outs[0], outs[1]), (h, w)
