@@ -1619,10 +1619,18 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
 // MMAs, then source 0's, so the transform overlaps tensor work.
 // Ring order per item: [dec1 box, skip box]; TMEM columns 0..383 hold three
 // 128-column KX2 accumulators, 384..511 the up accumulator.
-constexpr int kUpGroups = 3;
+// epilogue warpgroups and transform warpgroups (1: all four (dy, dx) blocks; 2:
+// one dy each) -- A/B build switches
+#ifndef LS_UPF_EPI
+#define LS_UPF_EPI 2
+#endif
+#ifndef LS_UPF_XF
+#define LS_UPF_XF 2
+#endif
+constexpr int kUpGroups = LS_UPF_EPI, kUpXf = LS_UPF_XF;
 constexpr uint32_t kUpBox = 10u * 16u * 128u;  // source-0 A box (20 KB)
 
-__global__ void __launch_bounds__(64 + 128 * (kUpGroups + 1)) k_conv_upfuse(
+__global__ void __launch_bounds__(64 + 128 * (kUpGroups + kUpXf)) k_conv_upfuse(
     const __grid_constant__ CUtensorMap mD1, const __grid_constant__ CUtensorMap mSkip,
     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mU,
     const ConvParamsP p) {
@@ -1657,9 +1665,9 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + 1)) k_conv_upfuse(
             }
             mbar_init(bres, 1);
             mbar_init(upready, 1);
-            mbar_init(upfree, 4);
+            mbar_init(upfree, 4 * kUpXf);
             for (int k = 0; k < 2; ++k) {
-                mbar_init(a0ready + k, 4);
+                mbar_init(a0ready + k, 4 * kUpXf);
                 mbar_init(a0free + k, 1);
             }
             fence_barrier_init();
@@ -1803,6 +1811,7 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + 1)) k_conv_upfuse(
     } else if (warp >= 2 + 4 * kGroups) {
         // ------------------------------ up transform ------------------------------
         const int quarter = warp & 3;
+        const int xg = (warp - 2 - 4 * kGroups) >> 2;  // transform group: dy blocks
         const int l = quarter * 32 + lane;  // dec1 pixel (r, j) of the item's 8 x 16 box
         const int r = l >> 4, j = l & 15;
         const int wp = p.w >> 1;
@@ -1823,13 +1832,16 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + 1)) k_conv_upfuse(
             uint8_t *box = abox + k * kUpBox;
             const bool colok = px0 + j >= 0 && px0 + j < wp;
             uint32_t ra[32], rb[32];
-            tmem_ld32_async(tb, ra);
+            constexpr int kDd = 4 / kUpXf;     // (dy, dx) blocks per group
+            const int dd0 = xg * kDd;
+            tmem_ld32_async(tb + 32u * dd0, ra);
 #pragma unroll
-            for (int dd = 0; dd < 4; ++dd) {
-                uint32_t(&cur)[32] = (dd & 1) ? rb : ra;
-                uint32_t(&nxt)[32] = (dd & 1) ? ra : rb;
+            for (int di = 0; di < kDd; ++di) {
+                const int dd = dd0 + di;
+                uint32_t(&cur)[32] = (di & 1) ? rb : ra;
+                uint32_t(&nxt)[32] = (di & 1) ? ra : rb;
                 tmem_ld_wait(cur);
-                if (dd + 1 < 4) {
+                if (di + 1 < kDd) {
                     tmem_ld32_async(tb + 32u * (dd + 1), nxt);
                 } else {
                     fence_before_sync();
@@ -2231,7 +2243,7 @@ static int launch_upfuse(const ls_conv_plan *pl, cudaStream_t st) {
     if (int e = smem_optin(k_conv_upfuse, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)(64 + 128 * (kUpGroups + 1)));
+    cfg.blockDim = dim3((unsigned)(64 + 128 * (kUpGroups + kUpXf)));
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];

@@ -1,5 +1,2 @@
-python -m pytest tests -m gpu -q > gpurun_out/r02_gpu_suite10.log 2>&1; tail -2 gpurun_out/r02_gpu_suite10.log
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-for i in 1 2; do python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02_bench_100m_v9_$i.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_100m_v9_$i.json').read().strip().splitlines()[-1]); print('100M', round(d['value'],1), 'e2e', round(d['e2e']['value'],1), round(d['roofline']['frac'],3), round(d['roofline']['other']['frac'],3), d['parity']['bit_exact'], d['parity'].get('unet_max_abs'), d['gpu_launches'], d['clocks']['sm_mhz'], d['clocks']['reasons'], {k: round(v*1e3,1) for k,v in d['stages_ms'].items()})"; done
-python bench.py --steps 20 --warmup 5 --points 20000000 --no-cpu-baseline > gpurun_out/r02_bench_20m_v9.json 2>/dev/null; python -c "import json; d=json.loads(open('gpurun_out/r02_bench_20m_v9.json').read().strip().splitlines()[-1]); print('20M', round(d['value'],1), round(d['e2e']['value'],1))"
-for r in 1 2; do timeout 120 python scripts/time_unet.py | tail -1; done
+timeout 900 python -m pytest tests/test_gpu_unet.py -x -q 2>&1 | tail -1
+for r in 1 2; do echo "$(timeout 120 python scripts/time_unet.py | tail -1)"; done
