@@ -330,3 +330,18 @@ def test_fused_up_conv_bit_identical(tmp_path):
                            env=env, check=True, timeout=300)
             outs.append(np.load(f))
         assert np.array_equal(outs[0], outs[1]), (h, w)
+    # a batch of 3 (every layer's item walk crosses images): fused == unfused,
+    # and image 0 of the batch == the single-image run of the same input
+    outs = []
+    for mode in ("0", "1"):
+        f = tmp_path / f"b{mode}.npy"
+        env = dict(os.environ, LS_UNET_UPFUSE=mode, H="128", W="240", B="3")
+        subprocess.run([sys.executable, os.path.join(root, "scripts", "unet_out.py"), str(f)],
+                       env=env, check=True, timeout=300)
+        outs.append(np.load(f))
+    assert outs[0].shape == (3, 128, 240, 3)
+    assert np.array_equal(outs[0], outs[1])
+    f = tmp_path / "single.npy"  # the first draws of the seeded generator: image 0's input
+    subprocess.run([sys.executable, os.path.join(root, "scripts", "unet_out.py"), str(f)],
+                   env=dict(os.environ, H="128", W="240", B="1"), check=True, timeout=300)
+    assert np.array_equal(np.load(f)[0], outs[1][0])
