@@ -106,6 +106,17 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap *map, const void 
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+// shared -> global tensor store (bulk group), 4-D box at the given coordinates
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *map, const void *src, int c0,
+                                             int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::
+            "l"(reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // wait until every committed bulk store has finished READING shared memory
 __device__ __forceinline__ void tma_store_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

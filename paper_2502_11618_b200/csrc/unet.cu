@@ -42,6 +42,14 @@ namespace unet {
 using namespace ls::umma;
 
 // sub-tiles per work item of the 128 / 256-column tiles (A/B build switches)
+// timing experiments only (scripts/exp builds; wrong outputs): pixel-pair stores
+// almost never issued (the math stays live), C8 MMAs per item (0..3 ky rows)
+#ifndef LS_EXP_PX_STORE_GUARD
+#define LS_EXP_PX_STORE_GUARD
+#endif
+#ifndef LS_EXP_PX_C8_KY
+#define LS_EXP_PX_C8_KY 3
+#endif
 #ifdef LS_EXP_NO_GDC
 #define LS_GDC_WAIT() ((void)0)  // timing-only experiment: layers overlap unsafely
 #else
@@ -61,6 +69,10 @@ using namespace ls::umma;
 // k_conv_px2 KX2 epilogue warpgroups (A/B build switch)
 #ifndef LS_KX2_GROUPS
 #define LS_KX2_GROUPS 3
+#endif
+// k_conv_px2 epilogue warpgroups of the 8-channel neighbour-row layer, e0c1 (A/B build switch)
+#ifndef LS_C8_GROUPS
+#define LS_C8_GROUPS 3
 #endif
 // k_conv_px2 KX2 epilogue warpgroups with 64 output channels (A/B build switch)
 #ifndef LS_KX2_64_GROUPS
@@ -1115,9 +1127,10 @@ struct CfgPx {
 // MMAs' extra operand reads lose.
 // epilogue warpgroups: KX2 items hold 128 TMEM columns and their epilogue
 // more live registers (three groups: 448 threads, up to 144 registers)
-template <bool G3, int CO = 32>
+template <bool G3, int CO = 32, bool C8NBR = false>
 __host__ __device__ constexpr int px_groups() {
-    return G3 ? (CO == 64 ? LS_KX2_64_GROUPS : LS_KX2_GROUPS) : CfgPx::kEpiGroups;
+    return C8NBR ? LS_C8_GROUPS
+                 : G3 ? (CO == 64 ? LS_KX2_64_GROUPS : LS_KX2_GROUPS) : CfgPx::kEpiGroups;
 }
 
 // KX2 with 64 channels (CO = 64 outputs, CI = 32 or 64 inputs; the half-
@@ -1126,9 +1139,10 @@ __host__ __device__ constexpr int px_groups() {
 // With CI = 64 a pair's two pixels are 128 B rows of two TMA boxes (a 5-D view
 // [c][element][pair][row][image] of the NHWC tensor, one box per element).
 template <int MODE, bool C8, bool KX2 = false, int CO = 32, int CI = 32>
-__global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_px2(
+__global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2>()) k_conv_px2(
     const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
-    const __grid_constant__ CUtensorMap mB, const ConvParamsP p) {
+    const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mY,
+    const ConvParamsP p) {
     static_assert(CO == 32 || (!C8 && MODE != kHead), "64-channel pixel pairs: no head");
     static_assert(CI == 32 || (!C8 && CO == 64), "64-channel inputs: 64-channel forms only");
     using C = CfgPx;
@@ -1136,7 +1150,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
     constexpr int kN = KX2 ? 4 * CO : (C8 ? C::kN : 2 * CO);
     constexpr int kAcc = KX2 ? 512 / kN : (CO == 64 ? 4 : C::kAcc);
     constexpr uint32_t kBTn = 2u * CO * 32u;      // neighbour-row B tile [W(1+e) ; W(e)] bytes
-    constexpr int kGroups = px_groups<KX2 || C8, CO>();
+    constexpr int kGroups = px_groups<KX2 || C8, CO, C8 && !KX2>();
     // an epilogue group waits on an accumulator's tfull parity at most one phase
     // ahead only if groups <= buffers (3 groups on 2 buffers read stale items)
     static_assert(!KX2 || kGroups <= kAcc, "KX2: epilogue warpgroups <= TMEM buffers");
@@ -1259,8 +1273,13 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                         tma_load_5d(st, q ? &mA1 : &mA0, 0, 0, px0, y0 - 1, img, full + s);
                         tma_load_5d(st + p.a_bytes, q ? &mA1 : &mA0, 0, 1, px0, y0 - 1, img, full + s);
                     } else {
+#ifdef LS_EXP_PX_NOTMA  // timing experiment only (scripts/exp): wrong outputs
+                        mbar_arrive(full + s);
+                        (void)st;
+#else
                         mbar_expect_tx(full + s, p.a_tx);
                         tma_load_4d(st, q ? &mA1 : &mA0, 0, px0, y0 - 1, img, full + s);
+#endif
                     }
                 }
             }
@@ -1336,7 +1355,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                         }
                     } else if constexpr (C8) {
 #pragma unroll
-                        for (int ky = 0; ky < 3; ++ky) {
+                        for (int ky = 0; ky < LS_EXP_PX_C8_KY; ++ky) {
                             const uint32_t ar = (uint32_t)(ky * kTW) * kARow / 16;
                             const uint32_t bt = (uint32_t)ky * 4096 / 16;
                             mma_bf16(d0, ((uint64_t)ahi << 32) | (a_lo + ar),
@@ -1395,6 +1414,11 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
             const int img = walk.IMG(p), px0 = walk.TX(p) * kPxCols - 1, y0 = (p.ty0 + walk.TY(p)) * kTH;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
+            if (CO == 32 && p.stage_store) {
+                // the warp's staging buffer is free once its previous store has read it
+                if (lane == 0) tma_store_wait_read();
+                __syncwarp();
+            }
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
             const int gp = px0 + tp, gy = y0 + ty;
             const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
@@ -1456,7 +1480,18 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                 uint32_t pk[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-                if (valid) {
+                if (CO == 32 && p.stage_store) {
+                    // staging row (tile row parity, pair - 1): the pair's 2 x 32
+                    // channels, 16 B chunks XOR-swizzled by row (TMA 128 B)
+                    if (valid) {
+                        const int r = (ty & 1) * kPxCols + tp - 1, c = px * 4 + (n >> 3);
+                        uint8_t *row = smem + p.off_stage + (uint32_t)(warp - 2) * 4096u + r * 128;
+                        *reinterpret_cast<uint4 *>(row + ((c ^ (r & 7)) << 4)) =
+                            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        *reinterpret_cast<uint4 *>(row + (((c + 1) ^ (r & 7)) << 4)) =
+                            make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    }
+                } else if (valid LS_EXP_PX_STORE_GUARD) {
                     // element offsets from the item's per-lane base (cout = CO)
                     if (p.y) st_global_v8(ybase + px * CO + n, pk);
                     if (p.y_f32) {
@@ -1561,6 +1596,15 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
                 }
             }
             }
+            if (CO == 32 && p.stage_store) {
+                // the warp's two tile rows x 14 pairs: one TMA store (clipped at the
+                // image's right / bottom edge)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    tma_store_4d(&mY, smem + p.off_stage + (uint32_t)(warp - 2) * 4096u, 0, px0 + 1,
+                                 y0 + 2 * quarter, img);
+            }
             if (MODE == kHead && valid) {
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
                 if (p.head_c == 3) {
@@ -1600,6 +1644,8 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO>()) k_conv_
             }
         }
     }
+    if (CO == 32 && p.stage_store && warp >= 2 && lane == 0)
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     fence_before_sync();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, C::kTmemCols);
@@ -2065,6 +2111,21 @@ static bool encode_up_store64(CUtensorMap *map, void *base, int w_in, int h_in, 
               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 32-channel NHWC output viewed as [pair: 2 x 32 channels][w/2][h][image], box
+// {64, 14, 2, 1}: one epilogue warp's two tile rows of 14 output pairs, 128 B swizzle.
+static bool encode_pair_store(CUtensorMap *map, void *base, int w, int h, int batch) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t row = (cuuint64_t)w * 64;  // one row, bytes
+    cuuint64_t dims[4] = {64, (cuuint64_t)(w / 2), (cuuint64_t)h, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {128, row, (cuuint64_t)h * row};
+    cuuint32_t box[4] = {64, (cuuint32_t)kPxCols, 2, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace unet
 }  // namespace ls
 
@@ -2226,7 +2287,7 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     if (int e = smem_optin(k_conv_px2<MODE, C8, KX2, CO, CI>, attr_done)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)pl->grid);
-    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8, CO>()));
+    cfg.blockDim = dim3((unsigned)(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2>()));
     cfg.dynamicSmemBytes = pl->smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -2235,7 +2296,7 @@ static int launch_px2_m(const ls_conv_plan *pl, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return (int)cudaLaunchKernelEx(&cfg, k_conv_px2<MODE, C8, KX2, CO, CI>, pl->a0, pl->a1, pl->b,
-                                   pl->p);
+                                   pl->y, pl->p);
 }
 
 static int launch_upfuse(const ls_conv_plan *pl, cudaStream_t st) {
@@ -2500,7 +2561,16 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
                                        : (size_t)p.nq * 3 * 2 * (p.c0 / 16) * 2 * cout * 32);
     const size_t const_bytes =
         ((size_t)(2 * cout + (d_head_w ? head_c * 32 : 0)) * 4 + 1023) & ~size_t(1023);
-    const size_t fixed = CfgPx::kRingPad + res_bytes + const_bytes + 512;
+    // 32-channel bf16 outputs leave through per-warp shared-memory staging
+    // buffers (4 KB: two tile rows x 14 pairs x 128 B) and TMA stores
+    const bool c8kx2 = c8 && env_int("LS_CONV_C8KX2", 0) == 1;
+    const int groups = c8 ? (c8kx2 ? LS_KX2_GROUPS : LS_C8_GROUPS)
+                          : kx2 ? (cout == 64 ? LS_KX2_64_GROUPS : LS_KX2_GROUPS)
+                                : CfgPx::kEpiGroups;
+    p.stage_store = cout == 32 && d_y && !d_y_f32 && env_int("LS_PX_STAGE", 1) != 0;
+    const size_t stage_total = p.stage_store ? (size_t)groups * 4 * 4096 : 0;
+    const size_t fixed =
+        CfgPx::kRingPad + res_bytes + const_bytes + stage_total + (stage_total ? 1024 : 0) + 512;
     const uint32_t stage_bytes = (ci64 ? 2u : 1u) * p.a_bytes;  // 64-ch inputs: two element boxes
     int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
     if (stages < 3) {
@@ -2513,7 +2583,8 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     p.off_b = (uint32_t)(CfgPx::kRingPad + stages * p.stage_bytes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
     p.off_pool = (uint32_t)(p.off_const + const_bytes);
-    p.off_bar = p.off_pool;
+    p.off_stage = (p.off_pool + 1023u) & ~1023u;
+    p.off_bar = (uint32_t)(p.off_stage + stage_total);
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = cout;
     pl->chunk = c8 ? 16 : 2 * c0;  // pair-row channels (128: two 64-channel element boxes)
@@ -2521,7 +2592,7 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     // 3 marks the KX2 (spill-column) variant; the 8-channel layer stays on the
     // neighbour-row form unless LS_CONV_C8KX2=1 (one N = 128 MMA per ky instead of
     // three, but the spill-column epilogue: e0c1 47 -> 52 us, measured slower)
-    pl->mt = (kx2 && !c8) || (c8 && env_int("LS_CONV_C8KX2", 0) == 1) ? 3 : 1;
+    pl->mt = (kx2 && !c8) || c8kx2 ? 3 : 1;
     pl->mode = d_head_w ? kHead : (d_pool ? kPool : kPlain);
     const int n_sm = current_sm_count();
     pl->grid = p.n_items < n_sm ? p.n_items : n_sm;
@@ -2538,6 +2609,7 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
         ok = ok && encode_act(&pl->a1, c1 > 0 ? d_x1 : d_x0, pc, w / 2, h, batch, pc, kTH + 2);
     }
     ok = ok && encode_wts(&pl->b, d_w, p.ctot, cout, 9, 16, cout, 1);
+    ok = ok && (!p.stage_store || encode_pair_store(&pl->y, d_y, w, h, batch));
     if (!ok) {
         delete pl;
         return nullptr;
