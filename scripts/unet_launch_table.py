@@ -1,6 +1,6 @@
 """Per-layer table from an ncu launch-list CSV of one U-Net forward
 (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
- sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed -k regex:k_conv -c 22)."""
+ sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed -k regex:k_conv -c 22; 21 launches with the fused dec0_up)."""
 import collections
 import csv
 import io
@@ -17,7 +17,10 @@ per = collections.OrderedDict()
 for r in rows[1:]:
     per.setdefault(r[iid], {"k": r[ik]})[r[im]] = float(r[iv].replace(",", ""))
 tot = 0.0
-for n, i in zip(NAMES, list(per)[:22]):
+ids = list(per)
+if any("upfuse" in per[i]["k"] for i in ids[:21]):  # dec0_up inside dec0_conv1: 21 launches
+    NAMES = NAMES[:19] + ["d0up+c1", "d0c2h"]
+for n, i in zip(NAMES, ids[:len(NAMES)]):
     d = per[i]
     t = d["gpu__time_duration.sum"] / 1000
     tot += t
