@@ -2800,7 +2800,8 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
     }
     // transposed convs are epilogue-bound (K is small, 4x cout outputs per
     // input pixel): 128-column tiles leave room for 3 epilogue warpgroups
-    if (transposed && bn > 128) bn = 128;
+    // (LS_CONV_UPBN=256: 256-column tiles, A/B)
+    if (transposed && bn > 128 && env_int("LS_CONV_UPBN", 128) != 256) bn = 128;
     if (d_head_w && n_total > bn) return fail(LS_EINVAL);  // the head needs every channel
     int chunk = bn >= 256 ? 32 : 64;
     while (chunk > 16 && ((c0 % chunk) || (c1 % chunk))) chunk >>= 1;
