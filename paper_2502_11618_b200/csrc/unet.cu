@@ -2854,6 +2854,9 @@ ls_conv_plan *ls_conv_plan_create(const uint16_t *d_x0, int32_t c0, const uint16
         if (bn < pair_min_bn() || chunk < 16) pair = false;
         mt = pair ? (bn == 128 ? env_int("LS_CONV_PAIR_MT", 1) == 2 ? 2 : 1 : 1)
                   : mt_for(bn, h, w, batch, (n_total + bn - 1) / bn, transposed != 0);
+        // transposed convs without staged stores (cout >= 128): two 128-pixel
+        // sub-tiles per item share each streamed weight block (LS_CONV_UPMT)
+        if (transposed && !want_stage && bn == 128 && env_int("LS_CONV_UPMT", 1) == 2) mt = 2;
         const int box_h = kTH * mt + 2 * p.pad;
         p.pair_h = pair && pair_side(h, w, batch, (n_total + bn - 1) / bn) ? 1 : 0;
         const int tile_h = kTH * mt * (pair && !p.pair_h ? 2 : 1);
