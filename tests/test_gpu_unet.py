@@ -73,6 +73,42 @@ def test_conv_layer_vs_torch(case):
         assert out["head_err"] <= 1e-5
 
 
+# 32-channel pixel-pair layers store through per-warp staging buffers and TMA
+# when no f32 copy of the output is requested: bf16 outputs (and pool / head
+# outputs) equal the lane-store path's bit for bit -- ragged pair tiles, rows
+# not a multiple of 8, batches, the 8-channel input form
+@pytest.mark.parametrize("case", [
+    dict(c0=32, c1=0, cout=32, h=20, w=100, act=2, batch=2),
+    dict(c0=32, c1=0, cout=32, h=10, w=36, act=1, pool=True, batch=3),
+    dict(c0=32, c1=0, cout=32, h=18, w=58, act=2, head=True),
+    dict(c0=8, c1=0, cout=32, h=64, w=128, act=1),
+    dict(c0=8, c1=0, cout=32, h=13, w=58, act=1, batch=2),
+    dict(c0=32, c1=0, cout=32, h=136, w=240, act=1, pool=True),
+], ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))
+def test_staged_pair_stores_bit_identical(case):
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "scripts"))
+    from check_conv import conv_case
+
+    import torch
+
+    staged = conv_case(**case, f32_out=False)
+    old = os.environ.get("LS_PX_STAGE")
+    os.environ["LS_PX_STAGE"] = "0"  # read at plan creation
+    try:
+        lanes = conv_case(**case, f32_out=False)
+    finally:
+        if old is None:
+            del os.environ["LS_PX_STAGE"]
+        else:
+            os.environ["LS_PX_STAGE"] = old
+    for k in ("y", "pool", "head"):
+        if staged[k] is not None:
+            assert torch.equal(staged[k], lanes[k]), k
+
+
 # (cin, cout, h, w[, batch]): 32- and 64-channel outputs take the staged TMA
 # store (64: one output-row parity per n-tile), ragged rows, batches (64 with
 # ragged rows and batch > 1: lane stores)
