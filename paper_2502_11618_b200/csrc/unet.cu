@@ -86,7 +86,12 @@ using namespace ls::umma;
 
 constexpr int kTW = 16, kTH = 8;
 constexpr size_t kResidentMax = 80 * 1024;
-constexpr size_t kSmemBudget = 222 * 1024;
+// dynamic shared memory a plan may lay out (+ 1 KB alignment slack; the
+// opt-in maximum is 227 KB) -- A/B build switch
+#ifndef LS_SMEM_BUDGET_KB
+#define LS_SMEM_BUDGET_KB 222
+#endif
+constexpr size_t kSmemBudget = LS_SMEM_BUDGET_KB * 1024;
 
 enum EpiMode { kPlain = 0, kPool = 1, kHead = 2, kTransposed = 3 };
 
