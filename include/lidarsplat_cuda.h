@@ -180,8 +180,8 @@ int ls_tile_worklist(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
  *   must hold +inf (0x7FF0000000000000) on entry.
  * d_cache: NULL (pass 2 re-projects every candidate), or
  *   ls_frame_cache_bytes(scene) bytes of 16 B aligned scratch: pass 1 then
- *   records each candidate's pixel and f32-rounded-down depth and pass 2
- *   decides from them (a candidate within one f32 ulp of the soft z-buffer
+ *   records each candidate's pixel and f16-rounded-down depth and pass 2
+ *   decides from them (a candidate within one f16 ulp of the soft z-buffer
  *   threshold re-derives its exact f64 depth).  Same frame either way.
  *   Requires W*H < 2^32 - 1.
  * d_accum4: (H*W x 4) f32 accumulators {sum r, sum g, sum b, count}, zero on
@@ -193,7 +193,8 @@ int ls_frame_project(const ls_scene *scene, const uint32_t *d_keep_bits, uint32_
                      uint32_t *d_count, const ls_camera *cam, double eps_rel,
                      uint64_t *d_minz_bits, uint32_t *d_cache, float *d_accum4, void *stream);
 
-/* Bytes of the optional pass-1 -> pass-2 cache: 1 KB per warp tile. */
+/* Bytes of the optional pass-1 -> pass-2 cache: 768 B per warp tile
+ * ([128 x u32 pixel][128 x f16 depth]). */
 size_t ls_frame_cache_bytes(const ls_scene *scene);
 
 /* Pass 1 only / pass 2 only of ls_frame_project over an existing work list

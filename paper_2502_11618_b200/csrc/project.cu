@@ -15,6 +15,7 @@
 // scan) let a warp skip a fully culled tile without touching its points.
 #include <atomic>
 #include <mutex>
+#include <cuda_fp16.h>
 #include "ls_common.cuh"
 #include "umma.cuh"
 
@@ -294,7 +295,54 @@ __device__ __forceinline__ void red_add_v4f32(float *p, float r, float g, float 
 // both passes live off the L1 that the rest of the SM's 256 KB provides.
 constexpr int kPassWarps = 8;  // 256-thread CTAs
 constexpr int kPosBytes = LS_TILE_POINTS * 12, kColBytes = LS_TILE_POINTS * 3;
-constexpr int kCacheBytes = LS_TILE_POINTS * 8;  // [128 x u32 pixel][128 x f32 depth]
+// [128 x u32 pixel][128 x depth rounded down: f32, or f16 with LS_CACHE_Z16 (A/B)]
+#ifndef LS_CACHE_Z16
+#define LS_CACHE_Z16 1
+#endif
+constexpr int kCacheZBytes = LS_CACHE_Z16 ? 2 : 4;
+constexpr int kCacheBytes = LS_TILE_POINTS * (4 + kCacheZBytes);
+
+// A lane's 4 depth records: RD of the f64 camera depth in the cache's format
+__device__ __forceinline__ void cache_put_z(uint32_t *blk, int lane, const double (&zc)[4]) {
+    float f[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) f[k] = __double2float_rd(zc[k]);
+    if constexpr (LS_CACHE_Z16) {
+        // RD_f16(RD_f32(z)) = RD_f16(z): f16 values are f32 values
+        uint32_t h[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) h[k] = __half_as_ushort(__float2half_rd(f[k]));
+        reinterpret_cast<uint2 *>(blk + LS_TILE_POINTS)[lane] =
+            make_uint2(h[0] | (h[1] << 16), h[2] | (h[3] << 16));
+    } else {
+        reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] = make_float4(f[0], f[1], f[2], f[3]);
+    }
+}
+
+// ... and back: zlo <= z < znext (znext: the format's next value up, inf past
+// its largest finite one)
+__device__ __forceinline__ void cache_get_z(const void *zbase, int lane, bool streaming,
+                                            float (&zlo)[4], float (&znext)[4]) {
+    if constexpr (LS_CACHE_Z16) {
+        const uint2 *q = reinterpret_cast<const uint2 *>(zbase) + lane;
+        const uint2 v = streaming ? __ldcs(q) : *q;
+        const uint32_t h[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            zlo[k] = __half2float(__ushort_as_half((unsigned short)h[k]));
+            znext[k] = __half2float(__ushort_as_half((unsigned short)(h[k] + 1u)));
+        }
+    } else {
+        const float4 *q = reinterpret_cast<const float4 *>(zbase) + lane;
+        const float4 v = streaming ? __ldcs(q) : *q;
+        const float z[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            zlo[k] = z[k];
+            znext[k] = __int_as_float(__float_as_int(z[k]) + 1);
+        }
+    }
+}
 // kXyz: pass 1 | kXyzRgb: pass 2 recomputing | kCacheRgb: pass 2 from the cache
 // | kRgb: colours only (multi-view pass 2, whose per-view cache blocks are read
 // straight from global memory)
@@ -538,9 +586,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1(SceneArgs s, ProjCam c,
                            pix[1] >= 0 ? (uint32_t)pix[1] : kNoPixel,
                            pix[2] >= 0 ? (uint32_t)pix[2] : kNoPixel,
                            pix[3] >= 0 ? (uint32_t)pix[3] : kNoPixel);
-            reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
-                make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
-                            __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+            cache_put_z(blk, lane, zc);
         }
         unsigned long long key[4];
 #pragma unroll
@@ -588,9 +634,7 @@ __global__ void __launch_bounds__(256) k_frame_pass1_u32(SceneArgs s, ProjCam c,
             const int lane = threadIdx.x & 31;
             uint32_t *blk = cache + it.index * (kCacheBytes / 4);
             reinterpret_cast<uint4 *>(blk)[lane] = make_uint4(pix[0], pix[1], pix[2], pix[3]);
-            reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
-                make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
-                            __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+            cache_put_z(blk, lane, zc);
         }
         unsigned long long cur[4];
 #pragma unroll
@@ -668,9 +712,9 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
     pdl_wait();
     for_each_item<kPass2Stages, kCacheRgb>(s, list, count, cache, [&](const Item &it, uint3 W) {
         const uint4 pw = reinterpret_cast<const uint4 *>(it.st)[lane];
-        const float4 zw = reinterpret_cast<const float4 *>(it.st + 4 * LS_TILE_POINTS)[lane];
+        float zlo[4], znext[4];
+        cache_get_z(it.st + 4 * LS_TILE_POINTS, lane, false, zlo, znext);
         uint32_t pix[4] = {pw.x, pw.y, pw.z, pw.w};
-        const float zlo[4] = {zw.x, zw.y, zw.z, zw.w};
         unsigned long long m[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) m[k] = pix[k] != kNoPixel ? __ldg(minz + pix[k]) : 0ull;
@@ -683,8 +727,8 @@ __global__ void __launch_bounds__(256) k_frame_pass2_cached(SceneArgs s, ProjCam
                 // z > T  <=>  z > RD_f32(T) (no float lies strictly between
                 // RD(T) and RU(T)), so both tests run in f32 against one rounding
                 const float trd = __double2float_rd(t);
-                bool keep = __int_as_float(__float_as_int(zlo[k]) + 1) <= trd;
-                if (!keep && !(zlo[k] > trd)) {  // within one f32 ulp: exact depth
+                bool keep = znext[k] <= trd;
+                if (!keep && !(zlo[k] > trd)) {  // within one ulp: exact depth
                     const float *p = s.pos + 3 * (it.base + k);
                     const double x = (double)__ldg(p), y = (double)__ldg(p + 1),
                                  z = (double)__ldg(p + 2);
@@ -837,9 +881,7 @@ __global__ void __launch_bounds__(256, 3) k_frame_pass1_views(
                                pix[1] >= 0 ? (uint32_t)pix[1] : kNoPixel,
                                pix[2] >= 0 ? (uint32_t)pix[2] : kNoPixel,
                                pix[3] >= 0 ? (uint32_t)pix[3] : kNoPixel);
-                reinterpret_cast<float4 *>(blk + LS_TILE_POINTS)[lane] =
-                    make_float4(__double2float_rd(zc[0]), __double2float_rd(zc[1]),
-                                __double2float_rd(zc[2]), __double2float_rd(zc[3]));
+                cache_put_z(blk, lane, zc);
             }
             unsigned long long *mz = minz + v * npix;
             unsigned long long key[4], cur[4];
@@ -929,9 +971,9 @@ __global__ void __launch_bounds__(256) k_frame_pass2_views_cached(
             if (((st >> (2 * v)) & 3u) == 0u) continue;
             const uint32_t *blk = cache + (it.index * nv + v) * (kCacheBytes / 4);
             const uint4 pw = __ldcs(reinterpret_cast<const uint4 *>(blk) + lane);
-            const float4 zw = __ldcs(reinterpret_cast<const float4 *>(blk + LS_TILE_POINTS) + lane);
+            float zlo[4], znext[4];
+            cache_get_z(blk + LS_TILE_POINTS, lane, true, zlo, znext);
             const uint32_t pc[4] = {pw.x, pw.y, pw.z, pw.w};
-            const float zlo[4] = {zw.x, zw.y, zw.z, zw.w};
             const unsigned long long *mz = minz + v * npix;
             unsigned long long m[4];
 #pragma unroll
@@ -943,8 +985,8 @@ __global__ void __launch_bounds__(256) k_frame_pass2_views_cached(
                 if (pc[k] == kNoPixel) continue;
                 const double t = dmul(__longlong_as_double((long long)m[k]), ope);
                 const float trd = __double2float_rd(t);
-                bool keep = __int_as_float(__float_as_int(zlo[k]) + 1) <= trd;
-                if (!keep && !(zlo[k] > trd)) {  // within one f32 ulp: exact depth
+                bool keep = znext[k] <= trd;
+                if (!keep && !(zlo[k] > trd)) {  // within one ulp: exact depth
                     const float *p = s.pos + 3 * (it.base + k);
                     const double x = (double)__ldg(p), y = (double)__ldg(p + 1),
                                  z = (double)__ldg(p + 2);

@@ -117,7 +117,7 @@ class FrameBuffers:
 
 
 # Pass-1 -> pass-2 cache (ls_frame_cache_bytes): pass 2 decides from each
-# candidate's cached pixel + f32 depth instead of re-projecting.  Frames are
+# candidate's cached pixel + f16 rounded-down depth instead of re-projecting.  Frames are
 # identical either way; LS_FRAME_CACHE=0 selects re-projection.
 USE_FRAME_CACHE = os.environ.get("LS_FRAME_CACHE", "1") != "0"
 

@@ -265,6 +265,41 @@ def test_soft_zbuffer_threshold_edges_match_oracle(rng, port, monkeypatch, eps, 
         assert np.array_equal(a.alpha, alpha)
 
 
+@pytest.mark.parametrize("eps", [0.0, 0.01, 0.5])
+def test_cached_depth_band_matches_oracle(port, eps):
+    """The pass-1 cache keeps each candidate's depth rounded down to f16: pass 2
+    keeps a point when the next f16 value up is <= RD_f32(T), rejects it when
+    the cached value is > RD_f32(T) and re-derives the exact f64 depth only in
+    between.  Per pixel, a front point and points behind it packed around the
+    threshold T = minz * (1 + eps) at sub-f16-ulp spacing, at depths from 0.3
+    to past the f16 range (65504), must give the oracle's frame bit for bit."""
+    from lidarsplat import CameraModel, PointCloud, RenderParams, RigidTransform, project_points
+    from paper_2502_11618_b200 import render
+
+    cam = CameraModel(fx=64.0, fy=64.0, cx=32.0, cy=24.0, width=64, height=48,
+                      world_to_camera=RigidTransform.identity(), z_far=1e6)
+    assert render.USE_FRAME_CACHE
+    pts = []
+    for i, z0 in enumerate([0.3, 1.0, 3.7, 100.0, 1000.0, 30000.0, 65504.0, 70000.0]):
+        u, v = 4 + 7 * i + 0.5, 10.5  # pixel centre of column 4 + 7i
+        t = z0 * (1.0 + eps)
+        zs = [z0] + [t * (1.0 + k * 2.0 ** -14) for k in range(-24, 25)]
+        zs += list(np.nextafter(np.float32(t), [np.float32(0), np.float32(np.inf)]))
+        for z in zs:
+            z = float(np.float32(z))
+            pts.append([(u - cam.cx) * z / cam.fx, (v - cam.cy) * z / cam.fy, z])
+    pts = np.array(pts, np.float32)
+    rng = np.random.default_rng(1)
+    cols = rng.integers(0, 256, (len(pts), 3), dtype=np.uint8)
+    cloud = PointCloud(pts, cols)
+    fr = project_points(cloud, None, cam, RenderParams(zbuffer_epsilon_rel=eps))
+    ref = O.project(pts, cols, np.zeros(1, np.int64), np.array([len(pts)], np.int64), cam, eps,
+                    port)
+    assert np.array_equal(fr.rgb, ref[0]) and np.array_equal(fr.depth, ref[1])
+    assert np.array_equal(fr.alpha, ref[2])
+    assert int(fr.alpha.sum()) >= 6
+
+
 def test_frame_edges_match_oracle(port):
     """Points landing exactly on u = 0 / v = 0 (kept), u = W / v = H (dropped),
     just inside / outside either edge, and on -0.0: the frame passes' integer
