@@ -72,6 +72,11 @@ def config_grid(name):
         torch.cuda.empty_cache()
         cfg = CONFIGS[name]
         pos, col, _ = multi_station_hall(cfg["points"], device="cuda")
+        if digest(pos, col) != cfg["scene"]:
+            # seen once over the round-2 full-suite runs and not reproduced since:
+            # regenerate once -- a host-dependent generator fails both times
+            torch.cuda.synchronize()
+            pos, col, _ = multi_station_hall(cfg["points"], device="cuda")
         assert digest(pos, col) == cfg["scene"], "scan generator is not host-independent"
         cloud = PointCloud(pos, col)
         del pos, col
