@@ -1412,6 +1412,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2
         const f32x2 slope2 = f2(slope, slope);
         const int wp = p.w >> 1;
         uint32_t ab = (uint32_t)eg % kAcc, aph = ((uint32_t)eg / kAcc) & 1u;
+        // staging buffer of this warp and item (p.stage_store buffers per warp, used
+        // in turn): free once the store that last read it is done reading
+        uint32_t sbuf = (uint32_t)(warp - 2) * (uint32_t)p.stage_store;
         ItemWalk walk;
         walk.init(p, blockIdx.x + eg * gridDim.x, kGroups * gridDim.x);
         for (int item = blockIdx.x + eg * gridDim.x; item < p.n_items;
@@ -1420,8 +1423,10 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
             if (CO == 32 && p.stage_store) {
-                // the warp's staging buffer is free once its previous store has read it
-                if (lane == 0) tma_store_wait_read();
+                if (lane == 0) {
+                    if (p.stage_store == 2) tma_store_wait_read_1();
+                    else tma_store_wait_read();
+                }
                 __syncwarp();
             }
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
@@ -1490,7 +1495,7 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2
                     // channels, 16 B chunks XOR-swizzled by row (TMA 128 B)
                     if (valid) {
                         const int r = (ty & 1) * kPxCols + tp - 1, c = px * 4 + (n >> 3);
-                        uint8_t *row = smem + p.off_stage + (uint32_t)(warp - 2) * 4096u + r * 128;
+                        uint8_t *row = smem + p.off_stage + sbuf * 4096u + r * 128;
                         *reinterpret_cast<uint4 *>(row + ((c ^ (r & 7)) << 4)) =
                             make_uint4(pk[0], pk[1], pk[2], pk[3]);
                         *reinterpret_cast<uint4 *>(row + (((c + 1) ^ (r & 7)) << 4)) =
@@ -1607,8 +1612,9 @@ __global__ void __launch_bounds__(64 + 128 * px_groups<KX2 || C8, CO, C8 && !KX2
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
                 if (lane == 0)
-                    tma_store_4d(&mY, smem + p.off_stage + (uint32_t)(warp - 2) * 4096u, 0, px0 + 1,
+                    tma_store_4d(&mY, smem + p.off_stage + sbuf * 4096u, 0, px0 + 1,
                                  y0 + 2 * quarter, img);
+                if (p.stage_store == 2) sbuf ^= 1u;
             }
             if (MODE == kHead && valid) {
                 const int64_t pix = ((int64_t)img * p.h + gy) * p.w + 2 * gp;
@@ -2572,12 +2578,26 @@ static ls_conv_plan *plan_px2(bool kx2, const uint16_t *d_x0, int c0, const uint
     const int groups = c8 ? (c8kx2 ? LS_KX2_GROUPS : LS_C8_GROUPS)
                           : kx2 ? (cout == 64 ? LS_KX2_64_GROUPS : LS_KX2_GROUPS)
                                 : CfgPx::kEpiGroups;
-    p.stage_store = cout == 32 && d_y && !d_y_f32 && env_int("LS_PX_STAGE", 1) != 0;
-    const size_t stage_total = p.stage_store ? (size_t)groups * 4 * 4096 : 0;
-    const size_t fixed =
-        CfgPx::kRingPad + res_bytes + const_bytes + stage_total + (stage_total ? 1024 : 0) + 512;
+    // (LS_PX_STAGE: 2 buffers per warp, so a store's read of one overlaps the
+    // next item's writes into the other -- one when that leaves < 4 ring stages;
+    // 1: one buffer; 0: lane stores)
+    int bufs = cout == 32 && d_y && !d_y_f32 ? env_int("LS_PX_STAGE", 2) : 0;
+    if (bufs < 0 || bufs > 2) bufs = 2;
     const uint32_t stage_bytes = (ci64 ? 2u : 1u) * p.a_bytes;  // 64-ch inputs: two element boxes
-    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
+    size_t stage_total;
+    int stages;
+    for (;;) {
+        stage_total = (size_t)bufs * groups * 4 * 4096;
+        const size_t fixed =
+            CfgPx::kRingPad + res_bytes + const_bytes + stage_total + (stage_total ? 1024 : 0) + 512;
+        stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / stage_bytes) : 0;
+        if (bufs == 2 && stages < 4) {
+            bufs = 1;
+            continue;
+        }
+        break;
+    }
+    p.stage_store = bufs;
     if (stages < 3) {
         delete pl;
         return nullptr;

@@ -94,19 +94,20 @@ def test_staged_pair_stores_bit_identical(case):
 
     import torch
 
-    staged = conv_case(**case, f32_out=False)
+    staged = conv_case(**case, f32_out=False)  # default: two staging buffers per warp
     old = os.environ.get("LS_PX_STAGE")
-    os.environ["LS_PX_STAGE"] = "0"  # read at plan creation
     try:
-        lanes = conv_case(**case, f32_out=False)
+        for mode in ("1", "0"):  # one staging buffer per warp; lane stores
+            os.environ["LS_PX_STAGE"] = mode  # read at plan creation
+            other = conv_case(**case, f32_out=False)
+            for k in ("y", "pool", "head"):
+                if staged[k] is not None:
+                    assert torch.equal(staged[k], other[k]), (mode, k)
     finally:
         if old is None:
-            del os.environ["LS_PX_STAGE"]
+            os.environ.pop("LS_PX_STAGE", None)
         else:
             os.environ["LS_PX_STAGE"] = old
-    for k in ("y", "pool", "head"):
-        if staged[k] is not None:
-            assert torch.equal(staged[k], lanes[k]), k
 
 
 # (cin, cout, h, w[, batch]): 32- and 64-channel outputs take the staged TMA
