@@ -1690,7 +1690,7 @@ constexpr uint32_t kUpBox = 10u * 16u * 128u;  // source-0 A box (20 KB)
 __global__ void __launch_bounds__(64 + 128 * (kUpGroups + kUpXf)) k_conv_upfuse(
     const __grid_constant__ CUtensorMap mD1, const __grid_constant__ CUtensorMap mSkip,
     const __grid_constant__ CUtensorMap mB, const __grid_constant__ CUtensorMap mU,
-    const ConvParamsP p) {
+    const __grid_constant__ CUtensorMap mY, const ConvParamsP p) {
     using C = CfgPx;
     constexpr int kN = 128, kAcc = 3, kGroups = kUpGroups;
     constexpr uint32_t kUpCol = 384;
@@ -1949,6 +1949,12 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + kUpXf)) k_conv_upfuse(
                       y0 = (p.ty0 + walk.TY(p)) * kTH;
             mbar_wait(tfull + ab, aph);
             fence_after_sync();
+            // staged output (as k_conv_px2): this warp's 4 KB buffer at p.off_pool
+            uint8_t *const ybuf = smem + p.off_pool + (uint32_t)(warp - 2) * 4096u;
+            if (p.stage_store) {
+                if (lane == 0) tma_store_wait_read();
+                __syncwarp();
+            }
             const uint32_t tbase = tmem + ab * kN + ((uint32_t)(quarter * 32) << 16);
             const int gp = px0 + tp, gy = y0 + ty;
             const bool valid = tp >= 1 && tp <= kPxCols && gp < wp && gy < p.h;
@@ -2005,8 +2011,24 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + kUpXf)) k_conv_upfuse(
                     uint32_t pk[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) pk[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-                    if (valid) st_global_v8(ybase + px * 32 + n, pk);
+                    if (p.stage_store) {
+                        if (valid) {
+                            const int r = (ty & 1) * kPxCols + tp - 1, c = px * 4 + (int)(n >> 3);
+                            uint8_t *row = ybuf + r * 128;
+                            *reinterpret_cast<uint4 *>(row + ((c ^ (r & 7)) << 4)) =
+                                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            *reinterpret_cast<uint4 *>(row + (((c + 1) ^ (r & 7)) << 4)) =
+                                make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        }
+                    } else if (valid) {
+                        st_global_v8(ybase + px * 32 + n, pk);
+                    }
                 }
+            }
+            if (p.stage_store) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) tma_store_4d(&mY, ybuf, 0, px0 + 1, y0 + 2 * quarter, img);
             }
 #pragma unroll 1
             for (int kk = 0; kk < kGroups; ++kk) {
@@ -2014,6 +2036,8 @@ __global__ void __launch_bounds__(64 + 128 * (kUpGroups + kUpXf)) k_conv_upfuse(
                 aph ^= ab == 0;
             }
         }
+        if (p.stage_store && lane == 0)
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
     }
     fence_before_sync();
     __syncthreads();
@@ -2144,6 +2168,7 @@ using namespace ls::unet;
 
 struct ls_conv_plan {
     CUtensorMap a0, a1, b, y;
+    CUtensorMap ys;  // k_conv_upfuse: staged output store (y holds its up weights)
     ConvParamsP p;
     int bn, chunk, grid, mode;
     int mt;    // k_conv_p: 128-pixel sub-tiles per work item
@@ -2323,7 +2348,8 @@ static int launch_upfuse(const ls_conv_plan *pl, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_conv_upfuse, pl->a0, pl->a1, pl->b, pl->y, pl->p);
+    return (int)cudaLaunchKernelEx(&cfg, k_conv_upfuse, pl->a0, pl->a1, pl->b, pl->y, pl->ys,
+                                   pl->p);
 }
 
 static int launch_px2(const ls_conv_plan *pl, cudaStream_t st) {
@@ -3049,9 +3075,22 @@ ls_conv_plan *ls_conv_plan_create_upfused(const uint16_t *d_x, const uint16_t *d
     p.resident = 1;
     const size_t res_bytes = 12 * 3072 + 16384;  // KX2 tiles of both sources + up weights
     const size_t boxes = 2 * (size_t)kUpBox;     // the transform's two source-0 boxes
-    const size_t fixed = CfgPx::kRingPad + boxes + res_bytes + 512;
-    int stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.stage_bytes) : 0;
-    stages &= ~1;  // two ring stages per item
+    // staged output stores (4 KB per epilogue warp, LS_UPF_STAGE=1) when the ring
+    // keeps >= 4 stages
+    const size_t ystage = (size_t)kUpGroups * 4 * 4096;
+    p.stage_store = env_int("LS_UPF_STAGE", 1) == 1 ? 1 : 0;
+    int stages = 0;
+    for (;;) {
+        const size_t fixed =
+            CfgPx::kRingPad + boxes + res_bytes + (p.stage_store ? ystage + 1024 : 0) + 512;
+        stages = kSmemBudget > fixed ? (int)((kSmemBudget - fixed) / p.stage_bytes) : 0;
+        stages &= ~1;  // two ring stages per item
+        if (p.stage_store && stages < 4) {
+            p.stage_store = 0;
+            continue;
+        }
+        break;
+    }
     if (stages < 4) {
         delete pl;
         return fail(LS_EINVAL);
@@ -3061,8 +3100,8 @@ ls_conv_plan *ls_conv_plan_create_upfused(const uint16_t *d_x, const uint16_t *d
     p.off_stage = (uint32_t)(CfgPx::kRingPad + stages * p.stage_bytes);
     p.off_b = (uint32_t)(p.off_stage + boxes);
     p.off_const = (uint32_t)(p.off_b + res_bytes);
-    p.off_pool = p.off_const;
-    p.off_bar = p.off_pool;
+    p.off_pool = p.stage_store ? (p.off_const + 1023u) & ~1023u : p.off_const;  // output staging
+    p.off_bar = p.off_pool + (p.stage_store ? (uint32_t)ystage : 0u);
     pl->smem = 1024 + p.off_bar + 512;
     pl->bn = 32;
     pl->chunk = 64;
@@ -3077,6 +3116,7 @@ ls_conv_plan *ls_conv_plan_create_upfused(const uint16_t *d_x, const uint16_t *d
     ok = ok && encode_act(&pl->a1, d_skip, 64, w / 2, h, batch, 64, kTH + 2);
     ok = ok && encode_wts(&pl->b, d_w, 64, 32, 9, 16, 32, 1);
     ok = ok && encode_wts(&pl->y, d_up_w, 64, 128, 1, 64, 128, 1);
+    ok = ok && (!p.stage_store || encode_pair_store(&pl->ys, d_y, w, h, batch));
     if (!ok) {
         delete pl;
         return fail(LS_EINVAL);

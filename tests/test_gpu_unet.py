@@ -358,15 +358,17 @@ def test_fused_up_conv_bit_identical(tmp_path):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    # (the fused kernel with its staged TMA output stores, the default, and with
+    # lane stores: LS_UPF_STAGE=0)
     for h, w in ((128, 240), (1088, 1920)):
         outs = []
-        for mode in ("0", "1"):
-            f = tmp_path / f"o{mode}_{h}.npy"
-            env = dict(os.environ, LS_UNET_UPFUSE=mode, H=str(h), W=str(w))
+        for mode, stage in (("0", "1"), ("1", "1"), ("1", "0")):
+            f = tmp_path / f"o{mode}{stage}_{h}.npy"
+            env = dict(os.environ, LS_UNET_UPFUSE=mode, LS_UPF_STAGE=stage, H=str(h), W=str(w))
             subprocess.run([sys.executable, os.path.join(root, "scripts", "unet_out.py"), str(f)],
                            env=env, check=True, timeout=300)
             outs.append(np.load(f))
-        assert np.array_equal(outs[0], outs[1]), (h, w)
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), (h, w)
     # a batch of 3 (every layer's item walk crosses images): fused == unfused,
     # and image 0 of the batch == the single-image run of the same input
     outs = []
